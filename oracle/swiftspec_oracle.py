@@ -1,0 +1,391 @@
+"""Plain, slow, float64 CPU oracle of the target model's tree-verification step.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): imported by tests/,
+__graft_entry__.smoke() and bench.py (cpu_baseline, --impl reference), never
+by the product.  Shares no code with the CUDA path.
+
+Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n (SPEC
+is used for interfaces and test ideas only).  Readings R1..R17 are listed in
+DESIGN.md "Readings of the paper".
+
+What the method computes: the target "runs batch
+inferences to calculate the logits" of every node of the draft tree it
+received, then "samples through the logits to generate the tokens one by one"
+and sends the verified tokens back.  Batched tree verification is an exact
+re-organisation of sequential greedy decoding, so this oracle is
+the plain definition: an int4-AWQ (group 128) Llama decoder run in
+float64 per tree node with the square ancestor mask, greedy
+acceptance (R6) and KV compaction of the accepted path (BASELINE north_star).
+
+Pins (tests/test_oracle.py): every function below is checked against
+something other than itself -- brute force, closed forms, golden fixtures in
+tests/golden/, HuggingFace's LlamaForCausalLM in float64 on a chain tree, the
+sequential single-token decode of each root path, and the sharded sum.
+Absolute logit values of a random-weight model have no printed value in the
+paper; they are pinned by the HF-Llama equivalence and the decode invariants
+(DESIGN.md "Parity").
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "bf16_to_f64", "tree_meta", "dequant", "rmsnorm", "silu", "rope", "softmax",
+    "attend_node", "argmax_lowest", "accept_walk", "OracleModel", "KVCache",
+    "layer_forward", "verify", "commit", "forced_decode", "greedy_decode",
+    "verify_sharded",
+]
+
+GROUP = 128  # AWQ group size, P:501 ("4-bit AWQ quantization with a group size of 128")
+
+
+def bf16_to_f64(bits) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> float64, exact (BF16 embedding/LM head)."""
+    b = np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)
+    return b.view(np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------------------
+# a0 -- tree metadata.  Square mask: "each token will only mask out the
+# attention with those tokens that are not the ancestors within the current
+# input".  Positions: reading R8, pos = L + depth.
+# ---------------------------------------------------------------------------
+def tree_meta(parents, L: int):
+    """Returns (depth int[T], pos int[T], anc bool[T][T]); anc[i][j] = j is an
+    ancestor-or-self of i.  Brute-force parent walk (no bit tricks)."""
+    parents = [int(p) for p in parents]
+    T = len(parents)
+    if T < 1 or parents[0] != -1:
+        raise ValueError("parents[0] must be -1 (root first, S:47)")
+    for i in range(1, T):
+        if not (0 <= parents[i] < i):
+            raise ValueError("parents[i] must be in [0, i) (topological order, S:47)")
+    depth = [0] * T
+    anc = np.zeros((T, T), dtype=bool)
+    for i in range(T):
+        j = i
+        d = 0
+        while j != -1:
+            anc[i, j] = True
+            j = parents[j]
+            d += 1
+        depth[i] = d - 1
+    depth = np.array(depth, dtype=np.int64)
+    return depth, L + depth, anc
+
+
+# ---------------------------------------------------------------------------
+# Dequantisation: AWQ asymmetric uint4 with per-(group, column) zero and bf16
+# scale (reading R3): W[k, n] = (q[k, n] - z[k // 128, n]) * s[k // 128, n].
+# ---------------------------------------------------------------------------
+def dequant(q, z, s_bits, group: int = GROUP) -> np.ndarray:
+    q = np.asarray(q)
+    z = np.asarray(z)
+    K, N = q.shape
+    if K % group:
+        raise ValueError("K must be a multiple of the group size")
+    s = bf16_to_f64(s_bits)
+    g = np.arange(K) // group
+    return (q.astype(np.float64) - z[g, :].astype(np.float64)) * s[g, :]
+
+
+def rmsnorm(x, g_bits, eps: float) -> np.ndarray:
+    """Llama pre-norm (reading R5): x / sqrt(mean(x^2) + eps) * g, per row."""
+    x = np.asarray(x, dtype=np.float64)
+    g = bf16_to_f64(g_bits)
+    return x / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps) * g
+
+
+def silu(x):
+    """SiLU, the sigma of the paper's garbled SwiGLU formula (reading R4)."""
+    return x / (1.0 + np.exp(-x))
+
+
+def rope(v, pos, theta: float) -> np.ndarray:
+    """Rotary position embedding, rotate-half convention (reading R2), float64 angles.
+    v: [..., d] for one position `pos` (scalar)."""
+    v = np.asarray(v, dtype=np.float64)
+    d = v.shape[-1]
+    half = d // 2
+    j = np.arange(half, dtype=np.float64)
+    ang = float(pos) * theta ** (-2.0 * j / d)
+    c, s = np.cos(ang), np.sin(ang)
+    a, b = v[..., :half], v[..., half:]
+    return np.concatenate([a * c - b * s, b * c + a * s], axis=-1)
+
+
+def softmax(x):
+    x = np.asarray(x, dtype=np.float64)
+    e = np.exp(x - np.max(x))
+    return e / np.sum(e)
+
+
+def attend_node(q, keys, values, n_kv_heads: int):
+    """Causal/tree attention of ONE node: q [Hq][d]; keys/values [n_keys][Hkv][d]
+    hold exactly the keys this node may see (reading R11: scale 1/sqrt(d),
+    softmax, no soft-cap).  GQA: q head h reads kv head h // (Hq / Hkv)."""
+    Hq, d = q.shape
+    rep = Hq // n_kv_heads
+    out = np.zeros((Hq, d))
+    for h in range(Hq):
+        kv = h // rep
+        sc = keys[:, kv, :] @ q[h] / math.sqrt(d)
+        p = softmax(sc)
+        out[h] = p @ values[:, kv, :]
+    return out
+
+
+def argmax_lowest(row) -> int:
+    """Greedy sampling (reading R6): linear scan, ties -> lowest token id."""
+    best, bi = -np.inf, 0
+    for i, v in enumerate(row):
+        if v > best:
+            best, bi = v, i
+    return bi
+
+
+def accept_walk(tokens, parents, argmax):
+    """a11, greedy acceptance ("samples through the logits ... one by one";
+    Fig. 4 walkthrough P:250).  Starting at the root, repeatedly take the
+    target's greedy token at the current node; if a child of the current node
+    carries it (lowest index on duplicates, reading R7), accept and descend.
+    Returns (accepted node indices, root first; bonus token)."""
+    T = len(tokens)
+    cur = 0
+    acc = [0]
+    while True:
+        t = int(argmax[cur])
+        nxt = None
+        for c in range(T):
+            if parents[c] == cur and int(tokens[c]) == t:
+                nxt = c
+                break
+        if nxt is None:
+            return acc, t
+        acc.append(nxt)
+        cur = nxt
+
+
+# ---------------------------------------------------------------------------
+# Model containers.
+# ---------------------------------------------------------------------------
+@dataclass
+class OracleModel:
+    """Canonical (quantised) weights from synth.gen_model; dequantised lazily."""
+    cfg: object
+    canon: dict
+    cache_dense: bool = True
+
+    def __post_init__(self):
+        self._dense = {}
+
+    def w(self, layer: int, name: str) -> np.ndarray:
+        key = (layer, name)
+        if key in self._dense:
+            return self._dense[key]
+        q, z, s = self.canon["layers"][layer][name]
+        W = dequant(q, z, s)
+        if self.cache_dense:
+            self._dense[key] = W
+        return W
+
+    def norm(self, layer: int, name: str):
+        return self.canon["layers"][layer][name]
+
+    def embed_rows(self, tokens) -> np.ndarray:
+        return bf16_to_f64(self.canon["embed"][np.asarray(tokens)])
+
+    def logits(self, xn: np.ndarray, chunk: int = 16384) -> np.ndarray:
+        """logits = xn @ lm_head^T (bf16 LM head); vocab rows in chunks
+        only to bound memory -- each logit is one plain dot product."""
+        W = self.canon["lm_head"]
+        V = W.shape[0]
+        out = np.empty((xn.shape[0], V))
+        for a in range(0, V, chunk):
+            out[:, a:a + chunk] = xn @ bf16_to_f64(W[a:a + chunk]).T
+        return out
+
+
+class KVCache:
+    """Committed cache per layer: K, V float64 [max_ctx][Hkv][d]; rows [0, L) valid."""
+
+    def __init__(self, cfg, max_ctx: int):
+        self.cfg = cfg
+        self.K = [np.zeros((max_ctx, cfg.n_kv_heads, cfg.head_dim)) for _ in range(cfg.n_layers)]
+        self.V = [np.zeros((max_ctx, cfg.n_kv_heads, cfg.head_dim)) for _ in range(cfg.n_layers)]
+        self.L = 0
+
+    def set_prefix(self, layer: int, k_bits, v_bits):
+        L = k_bits.shape[0]
+        self.K[layer][:L] = bf16_to_f64(k_bits)
+        self.V[layer][:L] = bf16_to_f64(v_bits)
+
+    def copy(self):
+        c = KVCache.__new__(KVCache)
+        c.cfg = self.cfg
+        c.K = [k.copy() for k in self.K]
+        c.V = [v.copy() for v in self.V]
+        c.L = self.L
+        return c
+
+
+def layer_forward(cfg, model: OracleModel, layer: int, x, kv: KVCache, L: int, pos, anc):
+    """One decoder layer over all T tree nodes (a2-a9), per node, float64.
+
+    x [T][h] residual stream.  Returns (x', tree K [T][Hkv][d], tree V)."""
+    T = x.shape[0]
+    Hq, Hkv, d = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+    xn = rmsnorm(x, model.norm(layer, "attn_norm"), cfg.rms_eps)          # a2
+    q = (xn @ model.w(layer, "wq")).reshape(T, Hq, d)                     # a3
+    k = (xn @ model.w(layer, "wk")).reshape(T, Hkv, d)
+    v = (xn @ model.w(layer, "wv")).reshape(T, Hkv, d)
+    for i in range(T):                                                    # a4: RoPE at L + depth
+        q[i] = rope(q[i], pos[i], cfg.rope_theta)
+        k[i] = rope(k[i], pos[i], cfg.rope_theta)
+    attn = np.zeros((T, Hq * d))
+    Kp, Vp = kv.K[layer][:L], kv.V[layer][:L]
+    for i in range(T):                                                    # a5: prefix + ancestors
+        sel = np.nonzero(anc[i])[0]
+        keys = np.concatenate([Kp, k[sel]], axis=0)
+        vals = np.concatenate([Vp, v[sel]], axis=0)
+        attn[i] = attend_node(q[i], keys, vals, Hkv).reshape(-1)
+    x = x + attn @ model.w(layer, "wo")                                   # a6
+    xn2 = rmsnorm(x, model.norm(layer, "mlp_norm"), cfg.rms_eps)          # a7
+    hmid = silu(xn2 @ model.w(layer, "wgate")) * (xn2 @ model.w(layer, "wup"))  # a8
+    x = x + hmid @ model.w(layer, "wdown")                                # a9
+    return x, k, v
+
+
+def verify(cfg, model: OracleModel, kv: KVCache, tokens, parents, want_logits: bool = True):
+    """One tree-verification step (a0-a11) against the committed cache kv (L = kv.L).
+
+    Returns dict(logits [T][V], argmax [T], accepted, bonus, tree_k, tree_v,
+    depth, pos, anc)."""
+    tokens = np.asarray(tokens)
+    L = kv.L
+    depth, pos, anc = tree_meta(parents, L)                               # a0
+    x = model.embed_rows(tokens)                                          # a1
+    tk, tv = [], []
+    for l in range(cfg.n_layers):
+        x, k, v = layer_forward(cfg, model, l, x, kv, L, pos, anc)
+        tk.append(k)
+        tv.append(v)
+    xn = rmsnorm(x, model.canon["final_norm"], cfg.rms_eps)              # a10
+    logits = model.logits(xn)
+    am = np.array([argmax_lowest(r) for r in logits], dtype=np.int64)
+    acc, bonus = accept_walk(tokens, parents, am)                         # a11
+    return dict(logits=logits if want_logits else None, argmax=am, accepted=acc,
+                bonus=bonus, tree_k=tk, tree_v=tv, depth=depth, pos=pos, anc=anc)
+
+
+def commit(kv: KVCache, res: dict, accepted) -> KVCache:
+    """a12, KV compaction + commit: K/V[L + k] <- tree K/V[accepted[k]] for every
+    layer; L += n (root + accepted nodes, never the bonus; reading R9)."""
+    L = kv.L
+    for l in range(len(kv.K)):
+        for kk, node in enumerate(accepted):
+            kv.K[l][L + kk] = res["tree_k"][l][node]
+            kv.V[l][L + kk] = res["tree_v"][l][node]
+    kv.L = L + len(accepted)
+    return kv
+
+
+def forced_decode(cfg, model, kv: KVCache, path_tokens):
+    """Sequential mode: feed path_tokens one at a time (T = 1 trees), committing
+    each.  Returns per-step logits [n][V]; kv is advanced in place."""
+    out = []
+    for t in path_tokens:
+        r = verify(cfg, model, kv, [int(t)], [-1])
+        out.append(r["logits"][0])
+        commit(kv, r, [0])
+    return np.array(out)
+
+
+def greedy_decode(cfg, model, kv: KVCache, root: int, n_tokens: int):
+    """Plain autoregressive greedy decoding from `root` (root not yet cached).
+    Returns the n_tokens generated tokens; kv advanced by n_tokens rows."""
+    toks = []
+    cur = int(root)
+    for _ in range(n_tokens):
+        r = verify(cfg, model, kv, [cur], [-1], want_logits=True)
+        nxt = int(r["argmax"][0])
+        commit(kv, r, [0])
+        toks.append(nxt)
+        cur = nxt
+    return toks
+
+
+# ---------------------------------------------------------------------------
+# Sharded mode (Megatron TP): each rank owns Hq/P q heads and
+# Hkv/P kv heads (column-parallel QKV), the matching O rows (row-parallel),
+# an I/P slice of gate/up/down, and a V/P vocab slice of the LM head.  The
+# two all-reduces per layer are plain sums of the ranks' partials in rank
+# order; argmax is taken over the concatenated vocab shards.
+# ---------------------------------------------------------------------------
+def verify_sharded(cfg, model: OracleModel, kv: KVCache, tokens, parents, P: int):
+    Hq, Hkv, d, h, I, V = (cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden,
+                           cfg.intermediate, cfg.vocab)
+    if Hkv % P or I % P:
+        raise ValueError("TP size must divide n_kv_heads and intermediate")
+    tokens = np.asarray(tokens)
+    L = kv.L
+    depth, pos, anc = tree_meta(parents, L)
+    T = len(tokens)
+    x = model.embed_rows(tokens)
+    hq, hk, ip = Hq // P, Hkv // P, I // P
+    tk, tv = [], []
+    for l in range(cfg.n_layers):
+        xn = rmsnorm(x, model.norm(l, "attn_norm"), cfg.rms_eps)
+        parts = []
+        k_all = np.zeros((T, Hkv, d))
+        v_all = np.zeros((T, Hkv, d))
+        for r in range(P):
+            Wq = model.w(l, "wq")[:, r * hq * d:(r + 1) * hq * d]
+            Wk = model.w(l, "wk")[:, r * hk * d:(r + 1) * hk * d]
+            Wv = model.w(l, "wv")[:, r * hk * d:(r + 1) * hk * d]
+            q = (xn @ Wq).reshape(T, hq, d)
+            k = (xn @ Wk).reshape(T, hk, d)
+            v = (xn @ Wv).reshape(T, hk, d)
+            for i in range(T):
+                q[i] = rope(q[i], pos[i], cfg.rope_theta)
+                k[i] = rope(k[i], pos[i], cfg.rope_theta)
+            k_all[:, r * hk:(r + 1) * hk] = k
+            v_all[:, r * hk:(r + 1) * hk] = v
+            Kp = kv.K[l][:L, r * hk:(r + 1) * hk]
+            Vp = kv.V[l][:L, r * hk:(r + 1) * hk]
+            attn = np.zeros((T, hq * d))
+            for i in range(T):
+                sel = np.nonzero(anc[i])[0]
+                attn[i] = attend_node(q[i], np.concatenate([Kp, k[sel]]),
+                                      np.concatenate([Vp, v[sel]]), hk).reshape(-1)
+            parts.append(attn @ model.w(l, "wo")[r * hq * d:(r + 1) * hq * d, :])
+        s = parts[0]
+        for p_ in parts[1:]:
+            s = s + p_
+        x = x + s
+        xn2 = rmsnorm(x, model.norm(l, "mlp_norm"), cfg.rms_eps)
+        parts = []
+        for r in range(P):
+            sl = slice(r * ip, (r + 1) * ip)
+            hmid = silu(xn2 @ model.w(l, "wgate")[:, sl]) * (xn2 @ model.w(l, "wup")[:, sl])
+            parts.append(hmid @ model.w(l, "wdown")[sl, :])
+        s = parts[0]
+        for p_ in parts[1:]:
+            s = s + p_
+        x = x + s
+        tk.append(k_all)
+        tv.append(v_all)
+    xn = rmsnorm(x, model.canon["final_norm"], cfg.rms_eps)
+    vp = -(-V // P)
+    shards = []
+    W = model.canon["lm_head"]
+    for r in range(P):
+        shards.append(xn @ bf16_to_f64(W[r * vp:min(V, (r + 1) * vp)]).T)
+    logits = np.concatenate(shards, axis=1)
+    am = np.array([argmax_lowest(rw) for rw in logits], dtype=np.int64)
+    acc, bonus = accept_walk(tokens, parents, am)
+    return dict(logits=logits, argmax=am, accepted=acc, bonus=bonus, tree_k=tk, tree_v=tv,
+                depth=depth, pos=pos, anc=anc)

@@ -1,0 +1,384 @@
+#!/usr/bin/env python3
+"""bench.py -- tree-verify step latency of the B200-native SwiftSpec target path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config llama3-70b] [--T 8] [--L 4096]
+
+N = 1 runs the BASELINE metric's model (Llama3-70B-shaped int4 AWQ g128,
+random weights from the device-side synthetic generator) at TP = 1 -- it fits
+one B200.  N > 1 is launched by torchrun, one rank per GPU, TP = N with the
+fused flag-based all-reduces over NVLink (strong scaling: the same 70B step on
+more GPUs).  One JSON line is printed by rank 0.
+
+A "step" = one pass of the whole hot path: tree ingest + embedding, 80 x
+(RMSNorm, QKV+RoPE+KV write, tree attention, O + all-reduce + residual,
+RMSNorm, gate/up+SwiGLU, down + all-reduce + residual), final norm, LM head +
+argmax, greedy accept walk, KV compaction + commit (auto-commit).
+
+--impl reference times the float64 CPU oracle (oracle/) on the host cores on
+a bounded sample of the same workload and extrapolates to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+GROUP = 128
+
+
+# ---------------------------------------------------------------- perf model
+def step_bytes(cfg, T, L, P=1):
+    """Algorithmic HBM bytes per step per GPU:
+    int4 weights + bf16 scales + int4 zeros of QKV/O/gate/up/down, bf16 LM-head
+    shard, KV prefix read, tree KV written."""
+    h, I, d = cfg.hidden, cfg.intermediate, cfg.head_dim
+    per_w = 0.5 + 2.0 / GROUP + 0.5 / GROUP
+    mats = h * (cfg.n_heads + 2 * cfg.n_kv_heads) * d + cfg.n_heads * d * h + 2 * h * I + I * h
+    b = cfg.n_layers * mats * per_w / P
+    b += math.ceil(cfg.vocab / P) * h * 2
+    b += cfg.n_layers * (L + T) * 2 * (cfg.n_kv_heads / P) * d * 2
+    return b
+
+
+def gateup_bytes(cfg, P=1):
+    """Algorithmic bytes of one gate/up launch (the dominant kernel: 55% of the layer)."""
+    return cfg.hidden * 2 * cfg.intermediate / P * (0.5 + 2.0 / GROUP + 0.5 / GROUP)
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- distributed helpers
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def exchange_handles(blob: bytes, world: int):
+    """All-gather every rank's peer-buffer handle blob (host logic; gloo-testable)."""
+    import torch.distributed as dist
+    if world == 1:
+        return [blob]
+    out = [None] * world
+    dist.all_gather_object(out, blob)
+    return out
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- trees
+def make_trees(cfg, T, n, seed=2):
+    rng = np.random.default_rng(seed)
+    return [synth.tree_paperlike(T, cfg.vocab, rng) for _ in range(n)]
+
+
+# ---------------------------------------------------------------- CPU oracle sample
+class OracleSample:
+    """The float64 oracle (as it stands) on a bounded sample of the step:
+    `n_layers_sample` decoder layers (dequant + attention + MLP for all T
+    nodes against an L-row prefix) plus 1/vocab_frac of the LM head, scaled to
+    the full step (x n_layers / n_layers_sample, x vocab_frac).  Input
+    generation happens once in the constructor and is not timed."""
+
+    def __init__(self, cfg, T, L, n_layers_sample=1, vocab_frac=16, seed=0):
+        import oracle as O
+        self.O, self.cfg, self.T, self.L = O, cfg, T, L
+        self.nls, self.vf = n_layers_sample, vocab_frac
+        self.sub = synth.ModelCfg(cfg.name + "-sample", n_layers_sample, cfg.hidden, cfg.intermediate,
+                                  cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.vocab // vocab_frac)
+        self.m = O.OracleModel(self.sub, synth.gen_model(self.sub, seed), cache_dense=False)
+        self.kv = O.KVCache(self.sub, L + T + 1)
+        for l in range(n_layers_sample):
+            k, v = synth.gen_prefix_kv(seed + 1, l, L, cfg.n_kv_heads, cfg.head_dim)
+            self.kv.set_prefix(l, k, v)
+        self.kv.L = L
+        self.trees = make_trees(self.sub, T, 4)
+        self.cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        self.sample = (f"{n_layers_sample} of {cfg.n_layers} layers + 1/{vocab_frac} of the LM head "
+                       f"(T={T}, L={L}), wall time scaled to the full step")
+
+    def step_seconds(self, i=0):
+        toks, parents = self.trees[i % len(self.trees)]
+        t0 = time.perf_counter()
+        self.O.verify(self.sub, self.m, self.kv, toks, parents, want_logits=False)
+        dt = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        self.m.logits(np.ones((self.T, self.cfg.hidden)))
+        dt_lm = time.perf_counter() - t1
+        per_layer = max(dt - dt_lm, 1e-9) / self.nls
+        return per_layer * self.cfg.n_layers + dt_lm * self.vf
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    smp = OracleSample(cfg, args.T, args.L)
+    steps = []
+    for i in range(args.warmup + args.steps):
+        s = smp.step_seconds(i)
+        if i >= args.warmup:
+            steps.append(s)
+    us = float(np.mean(steps)) * 1e6
+    line = {
+        "impl": "reference", "metric": METRIC(cfg, args), "value": us, "unit": "us",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, random weights)",
+        "config": CONFIG(cfg, args, world),
+        "cpu_baseline": {"value": us, "unit": "us", "cores": smp.cores, "kind": "oracle", "sample": smp.sample},
+        "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def METRIC(cfg, args):
+    return f"tree-verify step latency (Llama3-70B-shaped int4 AWQ, T={args.T}, L={args.L}, TP={args.gpus})" \
+        if cfg.name == "llama3-70b" else f"tree-verify step latency ({cfg.name}, T={args.T}, L={args.L}, TP={args.gpus})"
+
+
+def CONFIG(cfg, args, world):
+    return {"workload": f"{cfg.name} int4 AWQ g128 target, {args.T}-node paper-like tree, {args.L}-token KV, "
+                        f"TP={world}", "model": cfg.name, "T": args.T, "L": args.L, "tp": world,
+            "parallelism": f"tp{world}", "global_batch": 1, "seq_len": args.L,
+            "l2": "inputs larger than L2 (weights streamed every step)"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    import paper_2506_11309_b200 as pkg
+    from paper_2506_11309_b200 import swiftspec as ssp
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    T, L = args.T, args.L
+    n_steps = args.warmup + args.steps
+    max_ctx = L + T * (3 * n_steps + 8) + 64
+    sh = pkg.Shard(cfg, rank, world, local, max_ctx=max_ctx, max_tree=max(T, 8))
+    sh.synth_weights(args.seed)
+    sh.synth_prefix_kv(args.seed + 1, L)
+    if world > 1:
+        blobs = exchange_handles(sh.export_handle(), world)
+        sh.import_peers(blobs)
+        dist.barrier()
+    trees = make_trees(cfg, T, n_steps)
+    d_tok = torch.tensor(np.stack([t for t, _ in trees]), dtype=torch.int32, device=dev)
+    d_par = torch.tensor(np.stack([p for _, p in trees]), dtype=torch.int32, device=dev)
+    rwords = ssp.result_nbytes() // 4
+    d_res = torch.zeros((n_steps, rwords), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        sh.verify_dev(d_tok[i], d_par[i], T, d_result=d_res[i], auto_commit=True, stream=stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for i in range(args.warmup, n_steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, world, dev)
+    res = [ssp.parse_result(r, T) for r in d_res[args.warmup:].cpu().numpy()]
+    emitted = float(np.mean([r["n_accepted"] for r in res]))  # (n-1) accepted + 1 bonus
+    statuses = set(r["status"] for r in res)
+    kps = sh.kernels_per_step(T, auto_commit=True)
+
+    # ---- e2e: same metric through the public C-ABI with HOST buffers
+    # (H2D of the tree, D2H of the result inside ss_verify_tree, every step)
+    e2e_steps = max(3, args.steps // 2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    h_trees = make_trees(cfg, T, e2e_steps + 2, seed=7)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sh.verify(*h_trees[0], stream=stream)
+    sh.commit_accepted(stream=stream)
+    torch.cuda.synchronize()
+    f0.record(stream)
+    for i in range(e2e_steps):
+        sh.verify(*h_trees[1 + i], stream=stream)
+        sh.commit_accepted(stream=stream)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1) / e2e_steps, world, dev)
+
+    # ---- per-kernel device times (eager step, CUDA events around every launch)
+    prof = None
+    try:
+        i0 = n_steps - 1
+        for _ in range(2):
+            prof = sh.profile_step(d_tok[i0], d_par[i0], T, stream=stream)
+    except Exception as ex:  # pragma: no cover
+        prof = {"error": str(ex)}
+    torch.cuda.synchronize()
+
+    peak, peak_src = read_peaks()
+    bytes_step = step_bytes(cfg, T, L + 1, world)
+    line = {
+        "metric": METRIC(cfg, args), "value": ms * 1e3, "unit": "us", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int4 weights (AWQ g128) x fp16/bf16 activations, fp32 accumulate",
+        "data": "synthetic (seeded counter-based generator, random weights, paper-like trees)",
+        "config": CONFIG(cfg, args, world),
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 2 * 64 * 4,
+                "d2h_bytes_per_step": ssp.result_nbytes()},
+        "gpu_launches": kps * args.steps,
+        "decode_tokens_per_s": emitted / (ms / 1e3),
+        "emitted_tokens_per_step": emitted,
+        "step_roofline_frac": bytes_step / (ms / 1e3) / 1e9 / peak,
+        "step_bytes": bytes_step,
+        "status_ok": statuses == {0},
+    }
+    if isinstance(prof, dict) and "gate_up_swiglu" in prof:
+        gu_ms, gu_n = prof["gate_up_swiglu"]
+        tot = sum(v[0] for v in prof.values())
+        per = gu_ms / max(gu_n, 1)
+        ach = gateup_bytes(cfg, world) / (per / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(f"{cfg.name}/tp{world}/T{T}/gate_up")
+            except Exception:
+                traffic = None
+        line["roofline"] = {"kernel": "gate_up_swiglu (W4A16 GEMM, fused SwiGLU)", "bound": "hbm",
+                            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                            "traffic": traffic, "peak_source": peak_src,
+                            "algorithmic_bytes_per_launch": gateup_bytes(cfg, world),
+                            "avg_launch_us": per * 1e3, "share_of_step": gu_ms / tot if tot else None}
+        line["kernel_times_us"] = {k: {"total": v[0] * 1e3, "launches": v[1]} for k, v in prof.items()}
+    if rank == 0 and not args.no_cpu_baseline:
+        smp = OracleSample(cfg, T, L)
+        sec = smp.step_seconds(0)
+        line["cpu_baseline"] = {"value": sec * 1e6, "unit": "us", "cores": smp.cores, "kind": "oracle",
+                                "sample": smp.sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sh.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama3-70b", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--T", type=int, default=8)
+    ap.add_argument("--L", type=int, default=4096)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

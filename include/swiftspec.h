@@ -1,0 +1,222 @@
+/*
+ * swiftspec.h -- C-ABI of the B200-native tensor-parallel tree-verification
+ * step of SwiftSpec (arXiv 2506.11309).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n (interfaces only);
+ * Rn = reading n in DESIGN.md "Readings of the paper".
+ *
+ * The operation (Alg. 1 target branch P:288-298): the target worker
+ * "gets the draft tokens from the draft tree and runs batch inferences to
+ * calculate the logits. After that, it samples through the logits to generate
+ * the tokens one by one and then sends the verified tokens back".  One call of
+ * ss_verify_tree runs a T-node token tree (root first, parents[i] < i)
+ * through an int4-AWQ group-128 Llama decoder sharded over tp_size
+ * GPUs, with the square ancestor mask, the two
+ * tensor-parallel all-reduces per layer fused into the O / down projection
+ * epilogues, greedy acceptance (R6) and -- via
+ * ss_commit_kv / ss_commit_accepted -- KV compaction of the accepted path.
+ *
+ * Conventions
+ *  - Every function returns an ss_status; on error nothing was launched and
+ *    the shard state is unchanged; ss_last_error() gives a message
+ *    (thread-local).
+ *  - Collective semantics (NCCL-style): every rank of a TP group calls
+ *    ss_verify_tree* / ss_commit_* with identical arguments, in the same order.
+ *  - Ownership: the library owns every device allocation it makes (weights in
+ *    kernel layout, KV cache, workspaces, peer buffers).  Host inputs are
+ *    caller-owned and fully consumed before the call returns.  Device inputs
+ *    of the *_dev variants are caller-owned and must stay valid until the
+ *    stream reaches the enqueued work.
+ *  - Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - No torch types appear here; the Python binding only marshals arguments.
+ */
+#ifndef SWIFTSPEC_H
+#define SWIFTSPEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_MAX_TREE 64   /* maximum T (tree nodes) per verify call */
+#define SS_GROUP 128     /* AWQ group size */
+
+typedef enum {
+  SS_OK = 0,
+  SS_EINVAL = -1,        /* bad argument: tree not root-first/topological, T out of range,
+                            token out of vocab, chain not root-anchored, bad shape/kind/bytes */
+  SS_ECAPACITY = -2,     /* L + T > max_ctx (no eviction) */
+  SS_ECONSISTENCY = -3,  /* ranks disagree (debug checksum) or device-side validation failed */
+  SS_ECUDA = -4,         /* a CUDA runtime error; message has cudaGetErrorString */
+  SS_ETIMEOUT = -5,      /* a peer flag poll exceeded its budget */
+  SS_ESTATE = -6         /* call order violated (commit without a verify, weights missing, ...) */
+} ss_status;
+
+/* Model shape (public Llama3 configs, R1).  head_dim must be 64 or 128;
+ * hidden, n_heads*head_dim/tp and intermediate/tp must be multiples of 256;
+ * n_kv_heads and intermediate must be divisible by tp_size. */
+typedef struct {
+  int32_t n_layers, hidden, intermediate, n_heads, n_kv_heads, head_dim, vocab;
+  int32_t group_size;  /* must be 128 */
+  int32_t max_ctx;     /* KV capacity per layer and kv head, committed + tree rows */
+  int32_t max_tree;    /* largest T this shard will be called with, <= SS_MAX_TREE */
+  float rms_eps;       /* 1e-5 (R1) */
+  float rope_theta;    /* 500000 (R1) */
+} ss_model_cfg;
+
+typedef struct ss_shard ss_shard;
+
+/* Result of one verify step (Fig. 4).
+ *  n_accepted  = number of tree nodes on the accepted path INCLUDING the root
+ *                (>= 1); these are the rows ss_commit_accepted commits (R9).
+ *  accepted[k] = tree-node index of the k-th path node (accepted[0] == 0).
+ *  bonus_token = the target's greedy token after the last accepted node; it is
+ *                emitted but not committed (it is the next call's root, R9).
+ *  argmax[i]   = the target's greedy token at tree node i (ties -> lowest id).
+ *  status      = device-side validation result (SS_OK or SS_EINVAL). */
+typedef struct {
+  int32_t n_accepted;
+  int32_t accepted[SS_MAX_TREE];
+  int32_t bonus_token;
+  int32_t argmax[SS_MAX_TREE];
+  int32_t status;
+} ss_verify_result;
+
+/* Weight kinds for ss_load_weights.  Linear layers W map x -> x @ W with
+ * K = in-features, N = out-features (int4 AWQ g128, BF16 compute).
+ * The caller passes the FULL unsharded canonical tensor; the library slices
+ * its tensor-parallel shard (QKV / gate / up column-parallel by heads / I,
+ * O / down row-parallel, LM head vocab-parallel, embedding replicated) and
+ * repacks it into the kernel layout. */
+typedef enum {
+  SS_W_EMBED = 0,       /* uint16 bf16 bits [vocab][hidden]                       */
+  SS_W_ATTN_NORM = 1,   /* uint16 bf16 bits [hidden]                               */
+  SS_W_Q = 2,           /* linear, K = hidden, N = n_heads*head_dim                */
+  SS_W_K = 3,           /* linear, K = hidden, N = n_kv_heads*head_dim             */
+  SS_W_V = 4,           /* linear, K = hidden, N = n_kv_heads*head_dim             */
+  SS_W_O = 5,           /* linear, K = n_heads*head_dim, N = hidden                */
+  SS_W_MLP_NORM = 6,    /* uint16 bf16 bits [hidden]                               */
+  SS_W_GATE = 7,        /* linear, K = hidden, N = intermediate                    */
+  SS_W_UP = 8,          /* linear, K = hidden, N = intermediate                    */
+  SS_W_DOWN = 9,        /* linear, K = intermediate, N = hidden                    */
+  SS_W_FINAL_NORM = 10, /* uint16 bf16 bits [hidden]                               */
+  SS_W_LM_HEAD = 11     /* uint16 bf16 bits [vocab][hidden]                        */
+} ss_weight_kind;
+
+/* Sub-tensors of a linear kind (the `sub` argument). */
+typedef enum {
+  SS_SUB_QWEIGHT = 0,   /* uint8 [K][N], one nibble value 0..15 per byte           */
+  SS_SUB_QZEROS = 1,    /* uint8 [K/128][N], values 0..15                          */
+  SS_SUB_SCALES = 2,    /* uint16 bf16 bits [K/128][N]                              */
+  SS_SUB_DENSE = 0      /* for non-linear kinds                                     */
+} ss_weight_sub;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Create the shard of TP rank tp_rank (0 <= tp_rank < tp_size, tp_size in
+ * {1,2,4,8}) on CUDA device `device`: allocates weights, the KV cache
+ * [n_layers][n_kv_heads/tp][max_ctx][head_dim] (bf16), workspaces and the
+ * peer receive buffers.  *out receives the handle (owned by the caller, free
+ * with ss_destroy).  Errors: SS_EINVAL (shape rules above), SS_ECUDA. */
+ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
+                        int32_t device, ss_shard** out);
+
+/* Peer setup for tp_size > 1 ("GPUs computing the same model are
+ * connected tightly using NVLink"; P:413-420 fused all-reduce).
+ * ss_export_handle writes this rank's cudaIpc handle blob (<= 4096 bytes) to
+ * buf and its length to *len.  ss_import_peers takes all tp_size blobs in
+ * rank order (own blob included) and maps the peers' receive buffers.
+ * ss_import_local_peers is the single-process variant ("fake-peer" mode, or
+ * one process driving several GPUs): it takes the other shard handles
+ * directly.  Must be called before the first verify when tp_size > 1. */
+ss_status ss_export_handle(ss_shard* s, void* buf, size_t* len);
+ss_status ss_import_peers(ss_shard* s, const void* const* blobs, const size_t* lens);
+ss_status ss_import_local_peers(ss_shard* s, ss_shard* const* shards);
+
+/* Launch-resource cap (fake-peer mode: several ranks share one GPU and every
+ * rank's persistent kernels must be co-resident).  max_ctas_per_kernel <= 0
+ * restores the default (all SMs). */
+ss_status ss_set_launch_cap(ss_shard* s, int32_t max_ctas_per_kernel);
+
+ss_status ss_destroy(ss_shard* s);
+const char* ss_last_error(void);
+
+/* ---- weights and KV ------------------------------------------------------ */
+
+/* Copy one canonical host tensor (layer ignored for global kinds) into the
+ * shard, slicing and repacking on the host.  `bytes` must equal the canonical
+ * size.  Synchronous. */
+ss_status ss_load_weights(ss_shard* s, int32_t layer, int32_t kind, int32_t sub,
+                          const void* host, size_t bytes);
+
+/* Device-side synthetic weights: the same counter-based generator as
+ * synth/generators.py (DESIGN.md input recipe) evaluated on the GPU, written
+ * straight into the kernel layout.  Used for 8B/70B shapes where a host copy
+ * would be pointless.  Synchronous. */
+ss_status ss_synth_weights(ss_shard* s, uint64_t seed);
+
+/* Committed prefix rows [0, len) of one layer: k, v host uint16 bf16 bits
+ * [len][n_kv_heads][head_dim] (FULL heads; the shard keeps its own).  Keys are
+ * post-RoPE as cached.  Sets L = len when called for the last layer. */
+ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k, const void* v, int32_t len);
+/* Device-side synthetic prefix for all layers (synth.gen_prefix_kv), L = len. */
+ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len);
+/* Read committed rows [row0, row0+n) of layer `layer` back to host, full-head
+ * canonical layout of this shard's heads: [n][n_kv_heads/tp][head_dim] bf16. */
+ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, void* k_out, void* v_out);
+/* Set the committed length (truncate; cannot grow beyond rows ever written). */
+ss_status ss_set_committed_len(ss_shard* s, int32_t L);
+/* Committed length L (synchronises with the device if the last commit was
+ * device-driven).  Negative on error. */
+int32_t ss_committed_len(ss_shard* s);
+
+/* ---- the step ------------------------------------------------------------ */
+
+/* Verify one tree (host buffers).  tokens/parents: int32[T], parents[0] = -1,
+ * 0 <= parents[i] < i, tokens in [0, vocab).  Writes the tree's K/V into the
+ * scratch rows [L, L+T) (node i at row L+i, R10) without committing.
+ * out: filled before return (the call synchronises `stream`).
+ * logits_out: nullable float[T][vocab_shard] (this rank's vocab slice
+ * [rank*ceil(V/tp), ...)), for parity checks.
+ * Errors: SS_EINVAL, SS_ECAPACITY (L + T > max_ctx), SS_ESTATE, SS_ECUDA. */
+ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T,
+                         ss_verify_result* out, float* logits_out, void* stream);
+
+/* Same step, all-device and asynchronous (no host synchronisation): d_tokens,
+ * d_parents are device int32[T]; the result is written to the device struct
+ * d_result (nullable), logits to d_logits (nullable).  The tree is validated
+ * on the device (result->status).  Replays a captured CUDA graph per
+ * ceil(T/8).  If auto_commit != 0 the accepted path is committed on the
+ * device in the same launch sequence (bit-identical to ss_commit_accepted). */
+ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents,
+                             int32_t T, ss_verify_result* d_result, float* d_logits,
+                             int32_t auto_commit, void* stream);
+
+/* Commit a root-anchored chain of tree nodes from the last verify:
+ * accepted[0] == 0 and accepted[k] a child of accepted[k-1] (any such chain,
+ * not only the accepted one: chain prefill, EOS truncation).  K/V rows
+ * L + accepted[k] move to L + k in every layer; L += n.
+ * Errors: SS_EINVAL (not a chain / n out of range), SS_ESTATE (no verify). */
+ss_status ss_commit_kv(ss_shard* s, const int32_t* accepted, int32_t n, void* stream);
+/* Commit the accepted path of the last verify, decided on the device. */
+ss_status ss_commit_accepted(ss_shard* s, void* stream);
+
+/* Number of kernels the verify (+ commit) launch sequence contains. */
+int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_commit);
+
+/* Measurement helper (bench.py's roofline): run one all-device step like
+ * ss_verify_tree_dev(auto_commit=1) but launched eagerly with a CUDA event
+ * pair around every kernel on `stream`; synchronises and writes the summed
+ * device time (ms) and launch count per kernel kind to ms[SS_PROF_KINDS],
+ * count[SS_PROF_KINDS].  Kinds: 0 embed+tree, 1 QKV, 2 attention, 3 O-proj,
+ * 4 RMSNorm, 5 gate/up+SwiGLU, 6 down, 7 LM head+argmax+accept, 8 commit. */
+#define SS_PROF_KINDS 9
+ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
+                          float* ms, int32_t* count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWIFTSPEC_H */

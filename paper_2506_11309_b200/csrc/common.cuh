@@ -1,0 +1,204 @@
+// common.cuh -- sm_100a device helpers shared by the swiftspec kernels:
+// mbarrier + cp.async.bulk (TMA bulk engine) pipeline primitives, mma.sync
+// wrappers, int4 -> bf16 dequant, LL-style flagged 16-byte lines, packed
+// layouts.  No model arithmetic lives here.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#define SS_DEV __device__ __forceinline__
+
+namespace ss {
+
+// ---------------------------------------------------------------- layouts
+// W4 unit (tile-group of 128 output rows x one K-stage of 256):
+//   [warp 0..7][kblock 0..3][lane 0..31][4 x u32 nibble words] = 16384 B
+//   [warp][group 0..1][16 bf16 scales]                          =   512 B
+//   [warp][group 0..1][16 int4 zeros packed in 8 B]             =   128 B
+// BF16 unit (LM head; 128 rows x K-stage of 64):
+//   [warp][k16 step 0..3][lane][4 x u32 bf16x2]                 = 16384 B
+constexpr int kTG = 128;             // rows per tile-group (8 warps x 16)
+constexpr int kW4KS = 256;           // K per W4 unit
+constexpr int kBFKS = 64;            // K per BF16 unit
+constexpr int kW4Bytes = 16384;
+constexpr int kW4MetaBytes = 640;
+constexpr int kW4UnitBytes = kW4Bytes + kW4MetaBytes;   // 17024
+constexpr int kBFUnitBytes = 16384;
+constexpr int kKvTile = 64;          // keys per attention tile
+
+// Activation "fragment order" (B operand of mma.m16n8k16, col layout).  W4
+// GEMM inputs are fp16 (exact integer weights (q - z) in fp16, DESIGN.md
+// "Precision"); the LM-head input is split bf16 hi/lo in 2*NT n-tiles.
+// element (token tt, k) of a [T][K] activation lives at
+//   ((k/16 * NT + tt/8) * 32 + lane) * 8 + word * 4 + half * 2   bytes,
+//   lane = (tt%8)*4 + ((k%16)%8)/2, word = (k%16)/8, half = k%2.
+SS_DEV uint32_t act_frag_offset(int tt, int k, int NT) {
+  int kk = k & 15;
+  int lane = ((tt & 7) << 2) | ((kk & 7) >> 1);
+  int word = kk >> 3;
+  return ((uint32_t)(((k >> 4) * NT + (tt >> 3)) * 32 + lane) << 3) + (word << 2) + ((k & 1) << 1);
+}
+
+// Swizzled KV cache row layout: 64-row blocks, 16-byte chunk index XORed
+// with (row % 8) so ldmatrix reads of 8 rows are bank-conflict free.
+SS_DEV uint32_t kv_elem_offset(int pos, int j, int d) {
+  int r = pos & 63;
+  int c = (j >> 3) ^ (r & 7);
+  return (uint32_t)(pos - r) * d + r * d + c * 8 + (j & 7);
+}
+
+// ---------------------------------------------------------------- PTX
+SS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SS_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+SS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+SS_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+SS_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared (TMA bulk engine, SASS UBLKCP),
+// completion counted on an mbarrier; L2 evict-first policy for streamed data.
+SS_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+SS_DEV void bulk_g2s_nohint(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+SS_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+SS_DEV uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+SS_DEV void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D, fp32 accumulate.
+SS_DEV void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+SS_DEV void ldmatrix_x4(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+SS_DEV void ldmatrix_x4_trans(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
+// Vector fp32 reduction into global memory (sm_90+).
+SS_DEV void red_add_v2(float* p, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
+// int4 nibble word -> 4 x f16x2 holding (1024 + q): lop3 with the 0x6400
+// exponent (1024.0 in fp16, ulp 1).  Nibble positions (0,4) -> r0, (1,5) ->
+// r1, (2,6) -> r2, (3,7) -> r3.
+SS_DEV void dequant8(uint32_t w, uint32_t* r) {
+  const uint32_t mask = 0x000F000Fu, magic = 0x64006400u;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[0]) : "r"(w), "r"(mask), "r"(magic));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[1]) : "r"(w >> 4), "r"(mask), "r"(magic));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[2]) : "r"(w >> 8), "r"(mask), "r"(magic));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[3]) : "r"(w >> 12), "r"(mask), "r"(magic));
+}
+SS_DEV uint32_t f16x2_sub(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// D = A(16x16 f16, row) * B(16x8 f16, col) + D, fp32 accumulate.
+SS_DEV void mma_f16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+SS_DEV uint32_t pack_half2(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+SS_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+SS_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+SS_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+SS_DEV float bf16_bits_to_f32(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+SS_DEV uint16_t f32_to_bf16_bits(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+
+SS_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+SS_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Order-preserving float key for packed (value, index) argmax with
+// lowest-index tie break: key = (ordered(v) << 32) | (0xFFFFFFFF - idx).
+SS_DEV uint64_t argmax_key(float v, uint32_t idx) {
+  uint32_t b = __float_as_uint(v);
+  uint32_t o = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((uint64_t)o << 32) | (uint64_t)(0xFFFFFFFFu - idx);
+}
+SS_DEV uint32_t argmax_key_index(uint64_t k) { return 0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu); }
+
+// LL line (Alg. 2, reading R15: NCCL order data1, flag1, data2, flag2):
+// each 8-byte (data, flag) half is written/read atomically by one v4 access.
+SS_DEV void ll_store(uint4* dst, uint32_t d1, uint32_t d2, uint32_t flag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(d1), "r"(flag), "r"(d2),
+               "r"(flag)
+               : "memory");
+}
+SS_DEV bool ll_try_load(const uint4* src, uint32_t flag, uint32_t& d1, uint32_t& d2) {
+  uint32_t a, f1, b, f2;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a), "=r"(f1), "=r"(b), "=r"(f2)
+               : "l"(src)
+               : "memory");
+  d1 = a;
+  d2 = b;
+  return f1 == flag && f2 == flag;
+}
+
+}  // namespace ss

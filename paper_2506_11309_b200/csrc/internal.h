@@ -1,0 +1,131 @@
+// internal.h -- shard state shared by the host C-ABI implementation and the
+// kernel launchers.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+#include <map>
+
+#include "../../include/swiftspec.h"
+
+namespace ss {
+
+constexpr int kMaxPeers = 8;
+
+// Device-resident per-step state (read by every kernel through a pointer so
+// that captured CUDA graphs replay with new trees).
+struct DevState {
+  int32_t L;                 // committed length
+  int32_t T;                 // nodes of the current tree
+  int32_t status;            // SS_OK / SS_EINVAL for the current tree
+  int32_t have_verify;       // 1 after a verify, 0 after a commit
+  int32_t tokens[SS_MAX_TREE];
+  int32_t parents[SS_MAX_TREE];
+  int32_t pos[SS_MAX_TREE];
+  int32_t pad0;
+  unsigned long long anc[SS_MAX_TREE];        // ancestor-or-self bitmask (bit j = node j)
+  unsigned long long argmax_key[SS_MAX_TREE]; // packed (ordered logit, ~id) per node (this rank)
+  ss_verify_result result;   // accept-walk result of the last verify
+  int32_t commit_n;          // chain to commit (ss_commit_kv): length
+  int32_t commit_chain[SS_MAX_TREE];
+  int32_t lm_done;           // LM-head tile-groups finished (self-resetting)
+  int32_t commit_done;       // commit CTAs finished (self-resetting)
+  uint32_t epoch;            // LL flag epoch of the current step (TP)
+  int32_t timeout;           // set when a peer poll exceeded its budget
+};
+
+// One packed linear (W4 format, see common.cuh) or bf16 matrix.
+struct PackedLinear {
+  uint8_t* d = nullptr;      // device units
+  size_t bytes = 0;
+  int K = 0, N = 0;          // local (sharded) shape; N padded to 128 multiple
+  int n_tg = 0, S = 0;       // tile-groups, K stages
+};
+
+struct LayerW {
+  PackedLinear qkv, o, gu, down;
+  uint16_t* attn_norm = nullptr;
+  uint16_t* mlp_norm = nullptr;
+};
+
+// Host-side staging of canonical tensors until a linear's parts are complete.
+struct CanonLinear {
+  std::vector<uint8_t> q, z;
+  std::vector<uint16_t> s;
+  bool hq = false, hz = false, hs = false;
+};
+
+struct GemmScratch {
+  float* accum = nullptr;    // [n_tg*128][8*NT_max] fp32, self-zeroing
+  int* counters = nullptr;   // [n_tg]
+  size_t accum_elems = 0;
+};
+
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t first = nullptr;
+  int kernels = 0;
+};
+
+}  // namespace ss
+
+struct ss_shard {
+  ss_model_cfg cfg;
+  int rank = 0, P = 1, device = 0;
+  int n_sm = 148;
+  int launch_cap = 0;
+  // local shapes
+  int Hq_l = 0, Hkv_l = 0, I_l = 0, G = 1, V_pad = 0, V_l = 0, V_off = 0, V_l_pad = 0;
+  int max_ctx_pad = 0;
+
+  // weights
+  std::vector<ss::LayerW> layers;
+  uint16_t* embed = nullptr;       // [V][h] bf16 (replicated)
+  uint16_t* final_norm = nullptr;
+  ss::PackedLinear lm_head;        // bf16 units
+  std::map<long, ss::CanonLinear> staging;  // (layer, kind) -> canonical parts
+  std::vector<uint32_t> loaded_mask;        // per layer bitmask of complete kinds
+  uint32_t global_mask = 0;
+
+  // KV cache [layer][kvh_l][max_ctx_pad][d] bf16, swizzled 64-row blocks
+  uint16_t* kcache = nullptr;
+  uint16_t* vcache = nullptr;
+  float2* rope_cs = nullptr;       // [max_ctx_pad][d/2] (cos, sin)
+
+  // activations / workspaces
+  float* x = nullptr;              // residual [64][h] fp32
+  uint8_t* act_h = nullptr;        // frag-ordered bf16, K = h, NT up to 8
+  uint8_t* act_o = nullptr;        // K = Hq_l*d
+  uint8_t* act_d = nullptr;        // K = I_l
+  uint8_t* act_lm = nullptr;       // LM-head input, bf16 hi/lo, K = h, 2*NT tiles
+  uint16_t* qbuf = nullptr;        // [Hkv_l][G*64][d] bf16 (post-RoPE q)
+  float* attn_ws = nullptr;        // partial O [Hkv_l][Z][S][256][d]
+  float* attn_ml = nullptr;        // partial (m, l)
+  int* attn_bar = nullptr;         // [Hkv_l*Z*2] arrive/depart counters
+  ss::GemmScratch sc_qkv, sc_o, sc_gu, sc_down, sc_lm;
+  float* logits_dev = nullptr;     // optional [64][V_l_pad]
+
+  // state
+  ss::DevState* dstate = nullptr;  // device
+  ss::DevState* hstate = nullptr;  // pinned host mirror for results
+  int32_t* d_tree_in = nullptr;    // device staging for host trees [2*64]
+  int32_t* h_tree_in = nullptr;    // pinned staging
+  int L_host = 0;
+  bool L_known = true;
+  int L_upper = 0;
+  int max_rows_written = 0;
+  bool have_verify = false;
+  int last_T = 0;
+
+  // TP peers
+  float* recv = nullptr;            // this rank's LL receive buffer
+  size_t recv_bytes = 0;
+  float* peer_recv[ss::kMaxPeers] = {nullptr};
+  bool peers_ready = false;
+  bool ipc_opened[ss::kMaxPeers] = {false};
+
+  // graphs: key = NT*4 + auto_commit*2 + logits
+  std::map<int, ss::Graph> graphs;
+  cudaStream_t cap_stream = nullptr;
+};

@@ -1,0 +1,89 @@
+// kernels.h -- kernel argument structs and launchers (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <algorithm>
+#include "internal.h"
+
+namespace ss {
+
+enum { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_ARGMAX = 3 };
+
+struct EpiArgs {
+  int kind = 0;
+  DevState* st = nullptr;
+  int layer = 0;
+  // QKV
+  int d = 128, Hq_l = 0, Hkv_l = 0, G = 1, max_ctx_pad = 0;
+  uint16_t* qbuf = nullptr;
+  uint16_t* kc = nullptr;
+  uint16_t* vc = nullptr;
+  const float2* rope_cs = nullptr;
+  // RESID (+ all-reduce)
+  float* x = nullptr;
+  int h = 0;
+  int rank = 0, P = 1, n_tg_total = 0, ar_seq = 0;
+  float* recv = nullptr;
+  float* peer_recv[kMaxPeers] = {nullptr};
+  // SWIGLU
+  uint8_t* act_out = nullptr;
+  // ARGMAX
+  int V_l = 0, V_off = 0, logits_ld = 0;
+  float* logits = nullptr;
+};
+
+struct GemmArgs {
+  const uint8_t* W = nullptr;
+  const uint8_t* act = nullptr;
+  int n_tg = 0, S = 0;
+  float* accum = nullptr;
+  int* counters = nullptr;
+  int n_sm = 148;
+  EpiArgs epi;
+};
+
+struct AttnArgs {
+  DevState* st = nullptr;
+  int layer = 0, Hkv_l = 0, G = 1, d = 128, max_ctx_pad = 0, NT = 1;
+  int splits = 1, zchunks = 1;
+  const uint16_t* qbuf = nullptr;
+  const uint16_t* kc = nullptr;
+  const uint16_t* vc = nullptr;
+  float* ws = nullptr;     // [Hkv_l][Z][S][256][d]
+  float* ml = nullptr;     // [Hkv_l][Z][S][256][2]
+  int* bar = nullptr;      // [Hkv_l*Z][2]
+  uint8_t* act_out = nullptr;  // O-proj input, frag order, K = Hq_l*d
+};
+
+int launch_gemm(const GemmArgs& g, int wfmt, int NT, int max_ctas, cudaStream_t st);
+int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st);
+
+// embed + tree metadata (a0, a1) + first RMSNorm into the frag activation
+void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
+                       cudaStream_t st);
+// RMSNorm of the residual into frag activations (a2 / a7 / final)
+void launch_prep_norm(ss_shard* s, const uint16_t* gain, int NT, int split, cudaStream_t st);
+// KV compaction + commit (a12); chain from the device result or commit list
+void launch_commit(ss_shard* s, int from_result, cudaStream_t st);
+// device synthetic generator (same counter-based hash as synth/generators.py)
+struct LinMap {
+  int mode;  // 0 QKV, 1 O, 2 GU, 3 DOWN
+  int rank, Hq_l, Hkv_l, d, I_l, Kl, Nl_valid;
+};
+struct SynthLinArgs {
+  uint64_t keys[3][3];  // [part][qweight, qzeros, scales] stream keys
+  float scale_c[3];
+  int N_full[3];
+  LinMap m;
+  int n_tg, S;
+};
+void launch_synth_linear_args(uint8_t* dst, const SynthLinArgs& a, cudaStream_t st);
+void launch_synth_dense_key(uint16_t* dst, size_t n, uint64_t key, size_t idx0, int mode, float scale,
+                            cudaStream_t st);
+void launch_synth_lm_key(uint8_t* dst, int V_l, int V_off, int V_full, int h, int n_tg, uint64_t key, float scale,
+                         cudaStream_t st);
+void launch_synth_kv_key(uint16_t* cache, int layer, int Hkv_full, int Hkv_l, int kv0, int d, int L,
+                         int max_ctx_pad, uint64_t key, cudaStream_t st);
+void launch_rope_table(float2* cs, int max_pos, int d, double theta, cudaStream_t st);
+
+}  // namespace ss

@@ -1,0 +1,433 @@
+// misc.cu -- small kernels of the step: tree ingest + embedding (a0, a1),
+// RMSNorm into fragment-ordered bf16 activations (a2, a7, final), KV
+// compaction + commit (a12), the RoPE table, and the device-side synthetic
+// input generator (same counter-based hash as synth/generators.py).
+#include "common.cuh"
+#include "internal.h"
+#include "kernels.h"
+
+namespace ss {
+
+// ---------------------------------------------------------------- a0 + a1
+// One CTA per token slot (8*NT of them).  Every CTA validates the tree the
+// same way (root first, 0 <= parents[i] < i, token in vocab: S:45-47); CTA 0
+// publishes T, status, depth-derived positions pos = L + depth (R8) and the
+// ancestor-or-self bitmasks.  CTA t < T gathers E[token] (P:501 bf16
+// embedding) into the fp32 residual and writes RMSNorm(x) * g (layer 0 attn
+// norm) into the fragment-ordered activation; slots t >= T are zeroed.
+__global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int32_t* tokens,
+                                                         const int32_t* parents, int T_in, const uint16_t* E,
+                                                         int V, int h, float* x, const uint16_t* gain,
+                                                         uint8_t* act, int NT, float eps, int epoch_stride) {
+  __shared__ int s_tok[SS_MAX_TREE], s_par[SS_MAX_TREE];
+  __shared__ int s_bad;
+  __shared__ float s_red[8];
+  const int tid = threadIdx.x;
+  const int T = min(max(T_in, 1), SS_MAX_TREE);
+  if (tid == 0) s_bad = (T_in < 1 || T_in > SS_MAX_TREE) ? 1 : 0;
+  __syncthreads();
+  if (tid < T) {
+    int p = parents[tid], tk = tokens[tid];
+    bool bad = (tid == 0) ? (p != -1) : (p < 0 || p >= tid);
+    bad = bad || tk < 0 || tk >= V;
+    if (bad) atomicOr(&s_bad, 1);
+    s_par[tid] = (tid == 0) ? -1 : ((p < 0 || p >= tid) ? 0 : p);
+    s_tok[tid] = (tk < 0 || tk >= V) ? 0 : tk;
+  }
+  __syncthreads();
+  const int t = blockIdx.x;
+  if (t == 0 && tid < SS_MAX_TREE) {
+    if (tid < T) {
+      unsigned long long anc = 0;
+      int dep = -1;
+      for (int j = tid; j != -1; j = s_par[j]) {
+        anc |= 1ull << j;
+        ++dep;
+      }
+      st->anc[tid] = anc;
+      st->pos[tid] = st->L + dep;
+      st->tokens[tid] = s_tok[tid];
+      st->parents[tid] = s_par[tid];
+    } else {
+      st->anc[tid] = 0ull;
+      st->pos[tid] = st->L;
+      st->tokens[tid] = -1;
+      st->parents[tid] = -2;
+    }
+    if (tid == 0) {
+      st->T = T;
+      st->status = s_bad ? SS_EINVAL : SS_OK;
+      // LL flag epoch of this step: flags epoch + [0, epoch_stride) are used
+      // by the all-reduces and the argmax exchange; 0 is never a live flag.
+      uint32_t e = st->epoch + (uint32_t)epoch_stride;
+      if (e < st->epoch || e + (uint32_t)epoch_stride < e) e = 1;
+      st->epoch = e;
+    }
+  }
+  if (t >= T) {  // padded token slot: zero its activation column
+    for (int k = 2 * tid; k < h; k += 512) *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = 0u;
+    return;
+  }
+  const uint16_t* e = E + (size_t)s_tok[t] * h;
+  float* xr = x + (size_t)t * h;
+  float ss = 0.f;
+  for (int k = 2 * tid; k < h; k += 512) {
+    uint32_t w = *reinterpret_cast<const uint32_t*>(e + k);
+    float a = bf16_lo(w), b = bf16_hi(w);
+    xr[k] = a;
+    xr[k + 1] = b;
+    ss += a * a + b * b;
+  }
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) s_red[tid >> 5] = ss;
+  __syncthreads();
+  if (tid < 32) {
+    float v = tid < 8 ? s_red[tid] : 0.f;
+    v = warp_sum(v);
+    if (tid == 0) s_red[0] = v;
+  }
+  __syncthreads();
+  const float r = rsqrtf(s_red[0] / (float)h + eps);
+  for (int k = 2 * tid; k < h; k += 512) {
+    uint32_t gw = *reinterpret_cast<const uint32_t*>(gain + k);
+    float a = xr[k] * r * bf16_lo(gw), b = xr[k + 1] * r * bf16_hi(gw);
+    *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = pack_half2(a, b);
+  }
+}
+
+void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
+                       cudaStream_t st) {
+  const uint16_t* g0 = s->layers[0].attn_norm;
+  embed_meta_kernel<<<8 * NT, 256, 0, st>>>(s->dstate, tokens, parents, T, s->embed, s->cfg.vocab,
+                                            s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
+                                            2 * s->cfg.n_layers + 2);
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// xn = x * rsqrt(mean(x^2) + eps) * g (R5).  split == 0: fp16 fragment-ordered
+// input of a W4 GEMM.  split == 1: the LM-head input as bf16 hi = bf16(xn) in
+// n-tiles [0, NT) and lo = bf16(xn - hi) in [NT, 2NT) (the LM head is bf16,
+// P:501; hi + lo carries ~16 mantissa bits).
+SS_DEV uint32_t split_pack(float a, float b, int lo) {
+  uint32_t hi = pack_bf16x2(a, b);
+  if (!lo) return hi;
+  return pack_bf16x2(a - bf16_lo(hi), b - bf16_hi(hi));
+}
+
+__global__ void __launch_bounds__(256) prep_norm_kernel(const DevState* st, const float* x, int h,
+                                                        const uint16_t* gain, uint8_t* act, int NT, float eps,
+                                                        int split) {
+  __shared__ float s_red[8];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  if (t >= st->T) return;
+  const float* xr = x + (size_t)t * h;
+  float ss = 0.f;
+  for (int k = 4 * tid; k < h; k += 1024) {
+    float4 v = *reinterpret_cast<const float4*>(xr + k);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) s_red[tid >> 5] = ss;
+  __syncthreads();
+  if (tid < 32) {
+    float v = tid < 8 ? s_red[tid] : 0.f;
+    v = warp_sum(v);
+    if (tid == 0) s_red[0] = v;
+  }
+  __syncthreads();
+  const float r = rsqrtf(s_red[0] / (float)h + eps);
+  for (int k = 4 * tid; k < h; k += 1024) {
+    float4 v = *reinterpret_cast<const float4*>(xr + k);
+    uint2 gw = *reinterpret_cast<const uint2*>(gain + k);
+    float a0 = v.x * r * bf16_lo(gw.x), a1 = v.y * r * bf16_hi(gw.x);
+    float a2 = v.z * r * bf16_lo(gw.y), a3 = v.w * r * bf16_hi(gw.y);
+    if (!split) {
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = pack_half2(a0, a1);
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, NT)) = pack_half2(a2, a3);
+    } else {
+      // 2*NT n-tiles: token t in tile t/8 (hi) and NT + t/8 (lo)
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, 2 * NT)) = split_pack(a0, a1, 0);
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, 2 * NT)) = split_pack(a2, a3, 0);
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k, 2 * NT)) = split_pack(a0, a1, 1);
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k + 2, 2 * NT)) = split_pack(a2, a3, 1);
+    }
+  }
+}
+
+void launch_prep_norm(ss_shard* s, const uint16_t* gain, int NT, int split, cudaStream_t st) {
+  prep_norm_kernel<<<8 * NT, 256, 0, st>>>(s->dstate, s->x, s->cfg.hidden, gain, split ? s->act_lm : s->act_h, NT,
+                                           s->cfg.rms_eps, split);
+}
+
+// ---------------------------------------------------------------- a12 commit
+// For every (layer, local kv head): K/V[L + k] <- K/V[L + chain[k]], k < n
+// (BASELINE north_star "KV-cache compaction that keeps only the accepted
+// path").  Two-phase (all loads, barrier, all stores) because the
+// source and destination row ranges overlap.  The CTA that finishes last
+// advances L by n (root + accepted, never the bonus: R9).
+__global__ void __launch_bounds__(256) commit_kernel(DevState* st, uint16_t* kc, uint16_t* vc, int Hkv_l, int d,
+                                                     int max_ctx_pad, int from_result) {
+  const int kvh = blockIdx.x, layer = blockIdx.y;
+  int n;
+  const int* chain;
+  if (from_result) {
+    bool ok = st->have_verify && st->result.status == SS_OK;
+    n = ok ? st->result.n_accepted : 0;
+    chain = st->result.accepted;
+  } else {
+    n = st->commit_n;
+    chain = st->commit_chain;
+  }
+  const int L = st->L;
+  const int cpr = d / 8;  // 16-byte chunks per row
+  const size_t base = ((size_t)layer * Hkv_l + kvh) * max_ctx_pad * d;
+  uint4 buf[2][8];
+  const int total = n * cpr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int idx = threadIdx.x + i * 256;
+    if (idx < total) {
+      int k = idx / cpr, c = idx % cpr;
+      int src = L + chain[k];
+      size_t off = base + (size_t)(src - (src & 63)) * d + (src & 63) * d + ((c ^ (src & 7)) << 3);
+      buf[0][i] = *reinterpret_cast<const uint4*>(kc + off);
+      buf[1][i] = *reinterpret_cast<const uint4*>(vc + off);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int idx = threadIdx.x + i * 256;
+    if (idx < total) {
+      int k = idx / cpr, c = idx % cpr;
+      int dst = L + k;
+      size_t off = base + (size_t)(dst - (dst & 63)) * d + (dst & 63) * d + ((c ^ (dst & 7)) << 3);
+      *reinterpret_cast<uint4*>(kc + off) = buf[0][i];
+      *reinterpret_cast<uint4*>(vc + off) = buf[1][i];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    int old = atomicAdd(&st->commit_done, 1);
+    if (old == (int)(gridDim.x * gridDim.y) - 1) {
+      st->commit_done = 0;
+      st->L = L + n;
+      st->have_verify = 0;
+    }
+  }
+}
+
+void launch_commit(ss_shard* s, int from_result, cudaStream_t st) {
+  dim3 grid(s->Hkv_l, s->cfg.n_layers);
+  commit_kernel<<<grid, 256, 0, st>>>(s->dstate, s->kcache, s->vcache, s->Hkv_l, s->cfg.head_dim,
+                                      s->max_ctx_pad, from_result);
+}
+
+// ---------------------------------------------------------------- RoPE table
+// cos/sin(pos * theta^(-2j/d)) evaluated in fp64 (R2), stored fp32.
+__global__ void rope_table_kernel(float2* cs, int max_pos, int d, double theta) {
+  int half = d / 2;
+  size_t n = (size_t)max_pos * half;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    int pos = (int)(i / half), j = (int)(i % half);
+    double ang = (double)pos * pow(theta, -2.0 * j / d);
+    double s, c;
+    sincos(ang, &s, &c);
+    cs[i] = make_float2((float)c, (float)s);
+  }
+}
+
+void launch_rope_table(float2* cs, int max_pos, int d, double theta, cudaStream_t st) {
+  rope_table_kernel<<<592, 256, 0, st>>>(cs, max_pos, d, theta);
+}
+
+// ---------------------------------------------------------------- synthetic inputs
+// Device re-implementation of synth/generators.py (counter-based SplitMix64
+// finaliser; exactly-rounded fp32 conversions in the same order).
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t C1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t C2 = 0x94D049BB133111EBull;
+
+SS_DEV uint64_t fmix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= C1;
+  z ^= z >> 27;
+  z *= C2;
+  z ^= z >> 31;
+  return z;
+}
+SS_DEV uint64_t hash_u64(uint64_t key, uint64_t idx) { return fmix64(key + (idx + 1) * GOLDEN); }
+SS_DEV float approx_normal(uint64_t hv) {
+  const float inv16 = 1.0f / 65536.0f;
+  float u0 = __fmul_rn((float)(uint32_t)(hv & 0xFFFF), inv16);
+  float u1 = __fmul_rn((float)(uint32_t)((hv >> 16) & 0xFFFF), inv16);
+  float u2 = __fmul_rn((float)(uint32_t)((hv >> 32) & 0xFFFF), inv16);
+  float u3 = __fmul_rn((float)(uint32_t)((hv >> 48) & 0xFFFF), inv16);
+  float s = __fadd_rn(__fadd_rn(__fadd_rn(u0, u1), u2), u3);
+  return __fmul_rn(__fsub_rn(s, 2.0f), 1.7320508075688772f);
+}
+SS_DEV uint16_t bf16_rne_bits(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+__constant__ uint64_t c_keys[3];  // qweight, qzeros, scales stream keys of the current tensor
+
+// canonical coordinates (part = which of the fused canonical tensors, n, k)
+SS_DEV bool lin_map(const LinMap& m, int row, int k, int& part, int& n, int& kk) {
+  kk = k;
+  if (m.mode == 0) {
+    int nq = m.Hq_l * m.d, nk = m.Hkv_l * m.d;
+    if (row < nq) { part = 0; n = m.rank * nq + row; }
+    else if (row < nq + nk) { part = 1; n = m.rank * nk + row - nq; }
+    else if (row < nq + 2 * nk) { part = 2; n = m.rank * nk + row - nq - nk; }
+    else return false;
+  } else if (m.mode == 1) {
+    part = 0; n = row; kk = m.rank * m.Kl + k;
+  } else if (m.mode == 2) {
+    int tg = row >> 7, r = row & 127;
+    part = r < 64 ? 0 : 1;
+    n = m.rank * m.I_l + tg * 64 + (r & 63);
+    if (tg * 64 + (r & 63) >= m.I_l) return false;
+  } else {
+    part = 0; n = row; kk = m.rank * m.Kl + k;
+  }
+  return true;
+}
+
+// One thread per 32-bit nibble word of the packed W4 layout + metadata.
+__global__ void synth_linear_kernel(uint8_t* dst, SynthLinArgs a) {
+  const size_t units = (size_t)a.n_tg * a.S;
+  const size_t words_per_unit = kW4Bytes / 4;      // 4096
+  const size_t total = units * (words_per_unit + 32);  // + 32 meta "slots" (16 rows x 2 groups) per warp... see below
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    size_t u = i / (words_per_unit + 32);
+    int w_in = (int)(i % (words_per_unit + 32));
+    int tg = (int)(u / a.S), s = (int)(u % a.S);
+    uint8_t* ub = dst + u * kW4UnitBytes;
+    if (w_in < (int)words_per_unit) {
+      int warp = w_in >> 9, rem = w_in & 511;
+      int kb = rem >> 7, lane = (rem >> 2) & 31, j = rem & 3;
+      int gq = lane >> 2, tq = lane & 3;
+      uint32_t word = 0;
+      for (int p = 0; p < 8; ++p) {
+        int row = tg * 128 + warp * 16 + gq + 8 * (p & 1);
+        int k = s * 256 + kb * 64 + j * 16 + 2 * tq + (p >> 2) + 8 * ((p >> 1) & 1);
+        int part, n, kk;
+        uint32_t q = 0;
+        if (lin_map(a.m, row, k, part, n, kk)) {
+          q = (uint32_t)(hash_u64(a.keys[part][0], (uint64_t)kk * a.N_full[part] + n) & 15u);
+        } else {
+          q = 8;  // padding rows: q == z == 8 -> weight 0
+        }
+        word |= q << (4 * p);
+      }
+      reinterpret_cast<uint32_t*>(ub)[w_in] = word;
+    } else {
+      // metadata: 32 slots per unit = 8 warps x 2 groups x (16 scales + 16 zeros)
+      int slot = w_in - (int)words_per_unit;
+      int warp = slot >> 2, grp = (slot >> 1) & 1, which = slot & 1;
+      int g = s * 2 + grp;
+      if (which == 0) {
+        uint16_t* sc = reinterpret_cast<uint16_t*>(ub + kW4Bytes) + warp * 32 + grp * 16;
+        for (int i2 = 0; i2 < 16; ++i2) {
+          int row = tg * 128 + warp * 16 + i2;
+          int part, n, kk;
+          float sv = 0.f;
+          if (lin_map(a.m, row, g * 128, part, n, kk)) {
+            int gg = kk / 128;
+            uint64_t hs = hash_u64(a.keys[part][2], (uint64_t)gg * a.N_full[part] + n);
+            float u = __fmul_rn((float)(uint32_t)((hs >> 41) + (1u << 22)), 1.1920928955078125e-07f);
+            sv = __fmul_rn(u, a.scale_c[part]);
+          }
+          sc[i2] = bf16_rne_bits(sv);
+        }
+      } else {
+        uint64_t zw = 0;
+        for (int i2 = 0; i2 < 16; ++i2) {
+          int row = tg * 128 + warp * 16 + i2;
+          int part, n, kk;
+          uint32_t zv = 8;
+          if (lin_map(a.m, row, g * 128, part, n, kk)) {
+            int gg = kk / 128;
+            zv = 6u + (uint32_t)(hash_u64(a.keys[part][1], (uint64_t)gg * a.N_full[part] + n) & 3u);
+          }
+          zw |= (uint64_t)zv << (4 * i2);
+        }
+        reinterpret_cast<uint64_t*>(ub + kW4Bytes + 512)[warp * 2 + grp] = zw;
+      }
+    }
+  }
+}
+
+void launch_synth_linear_args(uint8_t* dst, const SynthLinArgs& a, cudaStream_t st) {
+  synth_linear_kernel<<<148 * 8, 256, 0, st>>>(dst, a);
+}
+
+// dense bf16 tensors: mode 0 = N(0,1)-like * scale, mode 1 = 1 + 0.1 * N(0,1)-like
+__global__ void synth_dense_kernel(uint16_t* dst, size_t n, uint64_t key, size_t idx0, int mode, float scale) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float v = approx_normal(hash_u64(key, idx0 + i));
+    if (mode == 0) v = scale == 1.0f ? v : __fmul_rn(v, scale);
+    else v = __fadd_rn(1.0f, __fmul_rn(v, 0.1f));
+    dst[i] = bf16_rne_bits(v);
+  }
+}
+
+void launch_synth_dense_key(uint16_t* dst, size_t n, uint64_t key, size_t idx0, int mode, float scale,
+                            cudaStream_t st) {
+  synth_dense_kernel<<<148 * 8, 256, 0, st>>>(dst, n, key, idx0, mode, scale);
+}
+
+// LM head, bf16 A-fragment units: [tg][s][warp][j][lane][4 words]
+__global__ void synth_lm_kernel(uint8_t* dst, int V_l, int V_off, int V_full, int h, int n_tg, uint64_t key,
+                                float scale) {
+  const int S = h / 64;
+  const size_t words = (size_t)n_tg * S * (kBFUnitBytes / 4);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x) {
+    size_t u = i / 4096;
+    int w_in = (int)(i % 4096);
+    int tg = (int)(u / S), s = (int)(u % S);
+    int warp = w_in >> 9, j = (w_in >> 7) & 3, lane = (w_in >> 2) & 31, r = w_in & 3;
+    int gq = lane >> 2, tq = lane & 3;
+    int row = tg * 128 + warp * 16 + gq + 8 * (r & 1);
+    int k = s * 64 + j * 16 + 2 * tq + 8 * (r >> 1);
+    uint32_t word = 0;
+    int v = V_off + row;
+    if (row < V_l && v < V_full) {
+      uint16_t lo = bf16_rne_bits(__fmul_rn(approx_normal(hash_u64(key, (uint64_t)v * h + k)), scale));
+      uint16_t hi = bf16_rne_bits(__fmul_rn(approx_normal(hash_u64(key, (uint64_t)v * h + k + 1)), scale));
+      word = (uint32_t)lo | ((uint32_t)hi << 16);
+    }
+    reinterpret_cast<uint32_t*>(dst)[i] = word;
+  }
+}
+
+void launch_synth_lm_key(uint8_t* dst, int V_l, int V_off, int V_full, int h, int n_tg, uint64_t key, float scale,
+                         cudaStream_t st) {
+  synth_lm_kernel<<<148 * 8, 256, 0, st>>>(dst, V_l, V_off, V_full, h, n_tg, key, scale);
+}
+
+// prefix KV rows [0, L) of one layer: canonical idx (pos*Hkv + kvh)*d + j
+__global__ void synth_kv_kernel(uint16_t* cache, int layer, int Hkv_full, int Hkv_l, int kv0, int d, int L,
+                                int max_ctx_pad, uint64_t key) {
+  size_t n = (size_t)Hkv_l * L * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    int j = (int)(i % d);
+    size_t r = i / d;
+    int pos = (int)(r % L);
+    int kvh = (int)(r / L);
+    uint64_t idx = ((uint64_t)pos * Hkv_full + kv0 + kvh) * d + j;
+    float v = approx_normal(hash_u64(key, idx));
+    size_t base = ((size_t)layer * Hkv_l + kvh) * max_ctx_pad * d;
+    cache[base + kv_elem_offset(pos, j, d)] = bf16_rne_bits(v);
+  }
+}
+
+void launch_synth_kv_key(uint16_t* cache, int layer, int Hkv_full, int Hkv_l, int kv0, int d, int L,
+                         int max_ctx_pad, uint64_t key, cudaStream_t st) {
+  synth_kv_kernel<<<148 * 8, 256, 0, st>>>(cache, layer, Hkv_full, Hkv_l, kv0, d, L, max_ctx_pad, key);
+}
+
+}  // namespace ss

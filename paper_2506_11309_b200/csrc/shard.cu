@@ -1,0 +1,1012 @@
+// shard.cu -- host implementation of the C-ABI in include/swiftspec.h:
+// shard lifecycle and validation, host repack of canonical AWQ tensors into
+// the kernel layout (TP slicing), device synthetic weights, the KV manager
+// (committed length, scratch rows, capacity checks), CUDA-graph capture of
+// the step per ceil(T/8), peer mapping for tensor parallelism, error state.
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "kernels.h"
+
+using namespace ss;
+
+
+static thread_local std::string g_err;
+
+#define FAIL(code, msg)  \
+  do {                   \
+    g_err = (msg);       \
+    return (code);       \
+  } while (0)
+#define CUDA_TRY(x)                                                            \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess) {                                                   \
+      g_err = std::string(#x) + ": " + cudaGetErrorString(e_);                 \
+      return SS_ECUDA;                                                         \
+    }                                                                          \
+  } while (0)
+
+extern "C" const char* ss_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------ generator keys
+// Mirror of synth/generators.py stream_key / tensor_id.
+static uint64_t fmix64_h(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+static uint64_t tensor_id(int layer, int kind, int sub) {
+  return ((uint64_t)(layer + 1) << 16) | ((uint64_t)kind << 4) | (uint64_t)sub;
+}
+static uint64_t stream_key(uint64_t seed, uint64_t tid) {
+  return fmix64_h(fmix64_h(seed * 0x9E3779B97F4A7C15ull + 1) ^ (tid * 0xD1B54A32D192ED03ull));
+}
+static float scale_const(int K) { return (float)(1.0 / (4.64 * std::sqrt((double)K))); }
+
+// ------------------------------------------------------------ helpers
+static int round_up(int a, int b) { return (a + b - 1) / b * b; }
+static int nt_of(int T) {
+  int nt = (T + 7) / 8;
+  return nt <= 1 ? 1 : nt <= 2 ? 2 : nt <= 4 ? 4 : 8;
+}
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t bytes) {
+  cudaError_t e = cudaMalloc((void**)p, bytes ? bytes : 16);
+  if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes ? bytes : 16);
+  return e;
+}
+
+static void setup_linear(PackedLinear& pl, int K, int N) {
+  pl.K = K;
+  pl.N = round_up(N, 128);
+  pl.n_tg = pl.N / 128;
+  pl.S = K / kW4KS;
+  pl.bytes = (size_t)pl.n_tg * pl.S * kW4UnitBytes;
+}
+
+// mapping of packed local rows / k to canonical parts (same as misc.cu lin_map)
+static bool lin_map_h(const LinMap& m, int row, int k, int& part, int& n, int& kk) {
+  kk = k;
+  if (m.mode == 0) {
+    int nq = m.Hq_l * m.d, nk = m.Hkv_l * m.d;
+    if (row < nq) { part = 0; n = m.rank * nq + row; }
+    else if (row < nq + nk) { part = 1; n = m.rank * nk + row - nq; }
+    else if (row < nq + 2 * nk) { part = 2; n = m.rank * nk + row - nq - nk; }
+    else return false;
+  } else if (m.mode == 1 || m.mode == 3) {
+    part = 0; n = row; kk = m.rank * m.Kl + k;
+  } else {
+    int tg = row >> 7, r = row & 127;
+    part = r < 64 ? 0 : 1;
+    if (tg * 64 + (r & 63) >= m.I_l) return false;
+    n = m.rank * m.I_l + tg * 64 + (r & 63);
+  }
+  return true;
+}
+
+static LinMap make_map(const ss_shard* s, int mode, int Kl) {
+  LinMap m{};
+  m.mode = mode;
+  m.rank = s->rank;
+  m.Hq_l = s->Hq_l;
+  m.Hkv_l = s->Hkv_l;
+  m.d = s->cfg.head_dim;
+  m.I_l = s->I_l;
+  m.Kl = Kl;
+  return m;
+}
+
+// Host repack of canonical parts into W4 units (mirror of synth_linear_kernel).
+static void pack_w4_host(const PackedLinear& pl, const LinMap& m, const CanonLinear* parts[3], const int Nfull[3],
+                         std::vector<uint8_t>& out) {
+  out.assign(pl.bytes, 0);
+  for (int tg = 0; tg < pl.n_tg; ++tg)
+    for (int s = 0; s < pl.S; ++s) {
+      uint8_t* ub = out.data() + ((size_t)tg * pl.S + s) * kW4UnitBytes;
+      uint32_t* words = reinterpret_cast<uint32_t*>(ub);
+      for (int warp = 0; warp < 8; ++warp)
+        for (int kb = 0; kb < 4; ++kb)
+          for (int lane = 0; lane < 32; ++lane)
+            for (int j = 0; j < 4; ++j) {
+              int gq = lane >> 2, tq = lane & 3;
+              uint32_t word = 0;
+              for (int p = 0; p < 8; ++p) {
+                int row = tg * 128 + warp * 16 + gq + 8 * (p & 1);
+                int k = s * 256 + kb * 64 + j * 16 + 2 * tq + (p >> 2) + 8 * ((p >> 1) & 1);
+                int part, n, kk;
+                uint32_t q = 8;
+                if (lin_map_h(m, row, k, part, n, kk)) q = parts[part]->q[(size_t)kk * Nfull[part] + n];
+                word |= (q & 15u) << (4 * p);
+              }
+              words[((warp * 4 + kb) * 32 + lane) * 4 + j] = word;
+            }
+      for (int warp = 0; warp < 8; ++warp)
+        for (int grp = 0; grp < 2; ++grp) {
+          uint16_t* sc = reinterpret_cast<uint16_t*>(ub + kW4Bytes) + warp * 32 + grp * 16;
+          uint64_t zw = 0;
+          for (int i = 0; i < 16; ++i) {
+            int row = tg * 128 + warp * 16 + i;
+            int part, n, kk;
+            uint16_t sv = 0;
+            uint32_t zv = 8;
+            if (lin_map_h(m, row, (s * 2 + grp) * 128, part, n, kk)) {
+              size_t gi = (size_t)(kk / 128) * Nfull[part] + n;
+              sv = parts[part]->s[gi];
+              zv = parts[part]->z[gi] & 15u;
+            }
+            sc[i] = sv;
+            zw |= (uint64_t)zv << (4 * i);
+          }
+          reinterpret_cast<uint64_t*>(ub + kW4Bytes + 512)[warp * 2 + grp] = zw;
+        }
+    }
+}
+
+static void pack_lm_host(const std::vector<uint16_t>& W, int V_full, int V_l, int V_off, int h, int n_tg,
+                         std::vector<uint8_t>& out) {
+  const int S = h / 64;
+  out.assign((size_t)n_tg * S * kBFUnitBytes, 0);
+  uint32_t* words = reinterpret_cast<uint32_t*>(out.data());
+  size_t nw = out.size() / 4;
+  for (size_t i = 0; i < nw; ++i) {
+    size_t u = i / 4096;
+    int w_in = (int)(i % 4096);
+    int tg = (int)(u / S), s = (int)(u % S);
+    int warp = w_in >> 9, j = (w_in >> 7) & 3, lane = (w_in >> 2) & 31, r = w_in & 3;
+    int gq = lane >> 2, tq = lane & 3;
+    int row = tg * 128 + warp * 16 + gq + 8 * (r & 1);
+    int k = s * 64 + j * 16 + 2 * tq + 8 * (r >> 1);
+    int v = V_off + row;
+    uint32_t word = 0;
+    if (row < V_l && v < V_full) word = (uint32_t)W[(size_t)v * h + k] | ((uint32_t)W[(size_t)v * h + k + 1] << 16);
+    words[i] = word;
+  }
+}
+
+// ------------------------------------------------------------ lifecycle
+extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, int32_t device,
+                                   ss_shard** out) {
+  if (!cfg || !out) FAIL(SS_EINVAL, "null argument");
+  *out = nullptr;
+  const ss_model_cfg& c = *cfg;
+  if (tp_size != 1 && tp_size != 2 && tp_size != 4 && tp_size != 8) FAIL(SS_EINVAL, "tp_size must be 1, 2, 4 or 8");
+  if (tp_rank < 0 || tp_rank >= tp_size) FAIL(SS_EINVAL, "tp_rank out of range");
+  if (c.group_size != SS_GROUP) FAIL(SS_EINVAL, "group_size must be 128");
+  if (c.head_dim != 64 && c.head_dim != 128) FAIL(SS_EINVAL, "head_dim must be 64 or 128");
+  if (c.n_layers < 1 || c.hidden < 256 || c.vocab < 2 || c.n_heads < 1 || c.n_kv_heads < 1)
+    FAIL(SS_EINVAL, "bad model shape");
+  if (c.n_heads % c.n_kv_heads) FAIL(SS_EINVAL, "n_heads must be a multiple of n_kv_heads");
+  if (c.n_kv_heads % tp_size || c.intermediate % tp_size) FAIL(SS_EINVAL, "tp_size must divide n_kv_heads and intermediate");
+  if (c.hidden % kW4KS) FAIL(SS_EINVAL, "hidden must be a multiple of 256");
+  if ((c.n_heads / tp_size * c.head_dim) % kW4KS) FAIL(SS_EINVAL, "n_heads*head_dim/tp must be a multiple of 256");
+  if ((c.intermediate / tp_size) % kW4KS) FAIL(SS_EINVAL, "intermediate/tp must be a multiple of 256");
+  if (c.max_tree < 1 || c.max_tree > SS_MAX_TREE) FAIL(SS_EINVAL, "max_tree must be in [1, 64]");
+  if (c.max_ctx < c.max_tree) FAIL(SS_EINVAL, "max_ctx too small");
+  int G = c.n_heads / c.n_kv_heads;
+  if (G * nt_of(c.max_tree) * 8 > 512) FAIL(SS_EINVAL, "(n_heads/n_kv_heads) * max_tree too large (<= 512 rows)");
+
+  CUDA_TRY(cudaSetDevice(device));
+  ss_shard* s = new ss_shard();
+  s->cfg = c;
+  s->rank = tp_rank;
+  s->P = tp_size;
+  s->device = device;
+  cudaDeviceGetAttribute(&s->n_sm, cudaDevAttrMultiProcessorCount, device);
+  s->Hq_l = c.n_heads / tp_size;
+  s->Hkv_l = c.n_kv_heads / tp_size;
+  s->I_l = c.intermediate / tp_size;
+  s->G = G;
+  int vp = (c.vocab + tp_size - 1) / tp_size;
+  s->V_off = tp_rank * vp;
+  s->V_l = std::max(0, std::min(c.vocab, (tp_rank + 1) * vp) - s->V_off);
+  s->V_l_pad = round_up(std::max(s->V_l, 1), 128);
+  s->max_ctx_pad = round_up(c.max_ctx, 64);
+  const int h = c.hidden, d = c.head_dim;
+
+  auto fail = [&](ss_status st) {
+    ss_destroy(s);
+    return st;
+  };
+#define A(ptr, bytes)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = dalloc(&(ptr), (bytes));                                \
+    if (e_ != cudaSuccess) {                                                 \
+      g_err = std::string("cudaMalloc ") + #ptr + ": " + cudaGetErrorString(e_); \
+      return fail(SS_ECUDA);                                                 \
+    }                                                                        \
+  } while (0)
+
+  s->layers.resize(c.n_layers);
+  s->loaded_mask.assign(c.n_layers, 0);
+  for (auto& lw : s->layers) {
+    setup_linear(lw.qkv, h, (s->Hq_l + 2 * s->Hkv_l) * d);
+    setup_linear(lw.o, s->Hq_l * d, h);
+    setup_linear(lw.gu, h, 2 * s->I_l);
+    setup_linear(lw.down, s->I_l, h);
+    A(lw.qkv.d, lw.qkv.bytes);
+    A(lw.o.d, lw.o.bytes);
+    A(lw.gu.d, lw.gu.bytes);
+    A(lw.down.d, lw.down.bytes);
+    A(lw.attn_norm, h * 2);
+    A(lw.mlp_norm, h * 2);
+  }
+  A(s->embed, (size_t)c.vocab * h * 2);
+  A(s->final_norm, h * 2);
+  s->lm_head.K = h;
+  s->lm_head.N = s->V_l_pad;
+  s->lm_head.n_tg = s->V_l_pad / 128;
+  s->lm_head.S = h / kBFKS;
+  s->lm_head.bytes = (size_t)s->lm_head.n_tg * s->lm_head.S * kBFUnitBytes;
+  A(s->lm_head.d, s->lm_head.bytes);
+
+  size_t kv_elems = (size_t)c.n_layers * s->Hkv_l * s->max_ctx_pad * d;
+  A(s->kcache, kv_elems * 2);
+  A(s->vcache, kv_elems * 2);
+  A(s->rope_cs, (size_t)s->max_ctx_pad * (d / 2) * sizeof(float2));
+  launch_rope_table(s->rope_cs, s->max_ctx_pad, d, (double)c.rope_theta, 0);
+
+  A(s->x, (size_t)SS_MAX_TREE * h * 4);
+  A(s->act_h, (size_t)h * 128);
+  A(s->act_o, (size_t)s->Hq_l * d * 128);
+  A(s->act_d, (size_t)s->I_l * 128);
+  A(s->act_lm, (size_t)h * 256);
+  A(s->qbuf, (size_t)s->Hkv_l * G * SS_MAX_TREE * d * 2);
+  A(s->attn_ws, (size_t)s->Hkv_l * 2 * 64 * 256 * d * 4);
+  A(s->attn_ml, (size_t)s->Hkv_l * 2 * 64 * 256 * 2 * 4);
+  A(s->attn_bar, (size_t)s->Hkv_l * 2 * 2 * 4);
+  auto mk_scratch = [&](GemmScratch& g, int n_tg) -> bool {
+    g.accum_elems = (size_t)n_tg * 128 * 64;
+    if (dalloc(&g.accum, g.accum_elems * 4) != cudaSuccess) return false;
+    if (dalloc(&g.counters, (size_t)n_tg * 4) != cudaSuccess) return false;
+    return true;
+  };
+  if (!mk_scratch(s->sc_qkv, s->layers[0].qkv.n_tg) || !mk_scratch(s->sc_o, s->layers[0].o.n_tg) ||
+      !mk_scratch(s->sc_gu, s->layers[0].gu.n_tg) || !mk_scratch(s->sc_down, s->layers[0].down.n_tg) ||
+      !mk_scratch(s->sc_lm, s->lm_head.n_tg)) {
+    g_err = "cudaMalloc scratch failed";
+    return fail(SS_ECUDA);
+  }
+  A(s->logits_dev, (size_t)SS_MAX_TREE * s->V_l_pad * 4);
+  A(s->dstate, sizeof(DevState));
+  A(s->d_tree_in, 2 * SS_MAX_TREE * 4);
+  if (cudaMallocHost((void**)&s->hstate, sizeof(DevState)) != cudaSuccess ||
+      cudaMallocHost((void**)&s->h_tree_in, 2 * SS_MAX_TREE * 4) != cudaSuccess) {
+    g_err = "cudaMallocHost failed";
+    return fail(SS_ECUDA);
+  }
+  {
+    DevState init{};
+    init.epoch = 1;
+    if (cudaMemcpy(s->dstate, &init, sizeof(DevState), cudaMemcpyHostToDevice) != cudaSuccess) {
+      g_err = "init state copy failed";
+      return fail(SS_ECUDA);
+    }
+  }
+  // LL receive buffer: [P][n_tg_total][128 rows][32 lines] x 16 B (fp32 pairs + flags)
+  if (tp_size > 1) {
+    s->recv_bytes = ((size_t)2 * tp_size * (h / 128) * 128 * 32 + (size_t)tp_size * 64) * 16;
+    A(s->recv, s->recv_bytes);
+  }
+  if (cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    g_err = "stream create failed";
+    return fail(SS_ECUDA);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    g_err = std::string("init: ") + cudaGetErrorString(cudaGetLastError());
+    return fail(SS_ECUDA);
+  }
+#undef A
+  *out = s;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_destroy(ss_shard* s) {
+  if (!s) return SS_OK;
+  cudaSetDevice(s->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& lw : s->layers) {
+    cudaFree(lw.qkv.d); cudaFree(lw.o.d); cudaFree(lw.gu.d); cudaFree(lw.down.d);
+    cudaFree(lw.attn_norm); cudaFree(lw.mlp_norm);
+  }
+  for (int p = 0; p < s->P; ++p)
+    if (s->ipc_opened[p] && s->peer_recv[p]) cudaIpcCloseMemHandle(s->peer_recv[p]);
+  void* ptrs[] = {s->embed, s->final_norm, s->lm_head.d, s->kcache, s->vcache, s->rope_cs, s->x, s->act_h,
+                  s->act_o, s->act_d, s->act_lm, s->qbuf, s->attn_ws, s->attn_ml, s->attn_bar, s->logits_dev, s->dstate,
+                  s->d_tree_in, s->recv, s->sc_qkv.accum, s->sc_qkv.counters, s->sc_o.accum, s->sc_o.counters,
+                  s->sc_gu.accum, s->sc_gu.counters, s->sc_down.accum, s->sc_down.counters, s->sc_lm.accum,
+                  s->sc_lm.counters};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (s->hstate) cudaFreeHost(s->hstate);
+  if (s->h_tree_in) cudaFreeHost(s->h_tree_in);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  delete s;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_set_launch_cap(ss_shard* s, int32_t cap) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  s->launch_cap = cap > 0 ? cap : 0;
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+// ------------------------------------------------------------ weights
+static const int kLinearKinds[] = {SS_W_Q, SS_W_K, SS_W_V, SS_W_O, SS_W_GATE, SS_W_UP, SS_W_DOWN};
+static bool is_linear(int kind) {
+  for (int k : kLinearKinds)
+    if (k == kind) return true;
+  return false;
+}
+
+static void linear_shape(const ss_model_cfg& c, int kind, int& K, int& N) {
+  const int h = c.hidden, d = c.head_dim;
+  switch (kind) {
+    case SS_W_Q: K = h; N = c.n_heads * d; break;
+    case SS_W_K: case SS_W_V: K = h; N = c.n_kv_heads * d; break;
+    case SS_W_O: K = c.n_heads * d; N = h; break;
+    case SS_W_GATE: case SS_W_UP: K = h; N = c.intermediate; break;
+    default: K = c.intermediate; N = h; break;
+  }
+}
+
+static ss_status try_pack_layer(ss_shard* s, int layer, int group_kind) {
+  // group_kind: 0 = qkv (Q,K,V), 1 = o, 2 = gu (GATE,UP), 3 = down
+  static const int members[4][3] = {{SS_W_Q, SS_W_K, SS_W_V}, {SS_W_O, -1, -1}, {SS_W_GATE, SS_W_UP, -1},
+                                    {SS_W_DOWN, -1, -1}};
+  const CanonLinear* parts[3] = {nullptr, nullptr, nullptr};
+  int Nfull[3] = {0, 0, 0};
+  for (int i = 0; i < 3; ++i) {
+    int k = members[group_kind][i];
+    if (k < 0) continue;
+    auto it = s->staging.find((long)layer * 64 + k);
+    if (it == s->staging.end() || !(it->second.hq && it->second.hz && it->second.hs)) return SS_OK;  // not yet
+    parts[i] = &it->second;
+    int K, N;
+    linear_shape(s->cfg, k, K, N);
+    Nfull[i] = N;
+  }
+  LayerW& lw = s->layers[layer];
+  PackedLinear* pl = group_kind == 0 ? &lw.qkv : group_kind == 1 ? &lw.o : group_kind == 2 ? &lw.gu : &lw.down;
+  int mode = group_kind;  // 0 QKV, 1 O, 2 GU, 3 DOWN
+  LinMap m = make_map(s, mode, pl->K);
+  std::vector<uint8_t> packed;
+  pack_w4_host(*pl, m, parts, Nfull, packed);
+  CUDA_TRY(cudaMemcpy(pl->d, packed.data(), packed.size(), cudaMemcpyHostToDevice));
+  for (int i = 0; i < 3; ++i) {
+    int k = members[group_kind][i];
+    if (k >= 0) {
+      s->staging.erase((long)layer * 64 + k);
+      s->loaded_mask[layer] |= 1u << k;
+    }
+  }
+  return SS_OK;
+}
+
+extern "C" ss_status ss_load_weights(ss_shard* s, int32_t layer, int32_t kind, int32_t sub, const void* host,
+                                     size_t bytes) {
+  if (!s || !host) FAIL(SS_EINVAL, "null argument");
+  const ss_model_cfg& c = s->cfg;
+  const int h = c.hidden;
+  cudaSetDevice(s->device);
+  if (is_linear(kind)) {
+    if (layer < 0 || layer >= c.n_layers) FAIL(SS_EINVAL, "layer out of range");
+    int K, N;
+    linear_shape(c, kind, K, N);
+    size_t want = sub == SS_SUB_QWEIGHT ? (size_t)K * N : sub == SS_SUB_QZEROS ? (size_t)(K / 128) * N
+                                                                               : (size_t)(K / 128) * N * 2;
+    if (sub < 0 || sub > 2) FAIL(SS_EINVAL, "bad sub-tensor");
+    if (bytes != want) FAIL(SS_EINVAL, "byte count does not match the canonical shape");
+    CanonLinear& cl = s->staging[(long)layer * 64 + kind];
+    if (sub == SS_SUB_QWEIGHT) {
+      cl.q.assign((const uint8_t*)host, (const uint8_t*)host + bytes);
+      cl.hq = true;
+    } else if (sub == SS_SUB_QZEROS) {
+      cl.z.assign((const uint8_t*)host, (const uint8_t*)host + bytes);
+      cl.hz = true;
+    } else {
+      cl.s.assign((const uint16_t*)host, (const uint16_t*)host + bytes / 2);
+      cl.hs = true;
+    }
+    int grp = (kind == SS_W_Q || kind == SS_W_K || kind == SS_W_V) ? 0 : kind == SS_W_O ? 1
+              : (kind == SS_W_GATE || kind == SS_W_UP) ? 2 : 3;
+    return try_pack_layer(s, layer, grp);
+  }
+  switch (kind) {
+    case SS_W_ATTN_NORM:
+    case SS_W_MLP_NORM: {
+      if (layer < 0 || layer >= c.n_layers) FAIL(SS_EINVAL, "layer out of range");
+      if (bytes != (size_t)h * 2) FAIL(SS_EINVAL, "norm must be hidden bf16 values");
+      uint16_t* dst = kind == SS_W_ATTN_NORM ? s->layers[layer].attn_norm : s->layers[layer].mlp_norm;
+      CUDA_TRY(cudaMemcpy(dst, host, bytes, cudaMemcpyHostToDevice));
+      s->loaded_mask[layer] |= 1u << kind;
+      return SS_OK;
+    }
+    case SS_W_FINAL_NORM:
+      if (bytes != (size_t)h * 2) FAIL(SS_EINVAL, "norm must be hidden bf16 values");
+      CUDA_TRY(cudaMemcpy(s->final_norm, host, bytes, cudaMemcpyHostToDevice));
+      s->global_mask |= 1u << kind;
+      return SS_OK;
+    case SS_W_EMBED:
+      if (bytes != (size_t)c.vocab * h * 2) FAIL(SS_EINVAL, "embed must be [vocab][hidden] bf16");
+      CUDA_TRY(cudaMemcpy(s->embed, host, bytes, cudaMemcpyHostToDevice));
+      s->global_mask |= 1u << kind;
+      return SS_OK;
+    case SS_W_LM_HEAD: {
+      if (bytes != (size_t)c.vocab * h * 2) FAIL(SS_EINVAL, "lm_head must be [vocab][hidden] bf16");
+      std::vector<uint16_t> W((const uint16_t*)host, (const uint16_t*)host + bytes / 2);
+      std::vector<uint8_t> packed;
+      pack_lm_host(W, c.vocab, s->V_l, s->V_off, h, s->lm_head.n_tg, packed);
+      CUDA_TRY(cudaMemcpy(s->lm_head.d, packed.data(), packed.size(), cudaMemcpyHostToDevice));
+      s->global_mask |= 1u << kind;
+      return SS_OK;
+    }
+    default:
+      FAIL(SS_EINVAL, "unknown weight kind");
+  }
+}
+
+extern "C" ss_status ss_synth_weights(ss_shard* s, uint64_t seed) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  cudaSetDevice(s->device);
+  const ss_model_cfg& c = s->cfg;
+  const int h = c.hidden, d = c.head_dim;
+  for (int l = 0; l < c.n_layers; ++l) {
+    LayerW& lw = s->layers[l];
+    struct G {
+      PackedLinear* pl;
+      int mode;
+      int kinds[3];
+    } groups[4] = {{&lw.qkv, 0, {SS_W_Q, SS_W_K, SS_W_V}},
+                   {&lw.o, 1, {SS_W_O, -1, -1}},
+                   {&lw.gu, 2, {SS_W_GATE, SS_W_UP, -1}},
+                   {&lw.down, 3, {SS_W_DOWN, -1, -1}}};
+    for (auto& g : groups) {
+      SynthLinArgs a{};
+      for (int i = 0; i < 3; ++i) {
+        int k = g.kinds[i];
+        if (k < 0) continue;
+        for (int sub = 0; sub < 3; ++sub) a.keys[i][sub] = stream_key(seed, tensor_id(l, k, sub));
+        int K, N;
+        linear_shape(c, k, K, N);
+        a.scale_c[i] = scale_const(K);
+        a.N_full[i] = N;
+      }
+      a.m = make_map(s, g.mode, g.pl->K);
+      a.n_tg = g.pl->n_tg;
+      a.S = g.pl->S;
+      launch_synth_linear_args(g.pl->d, a, 0);
+    }
+    launch_synth_dense_key(lw.attn_norm, h, stream_key(seed, tensor_id(l, SS_W_ATTN_NORM, 0)), 0, 1, 0.f, 0);
+    launch_synth_dense_key(lw.mlp_norm, h, stream_key(seed, tensor_id(l, SS_W_MLP_NORM, 0)), 0, 1, 0.f, 0);
+    s->loaded_mask[l] = 0xFFFFFFFFu;
+  }
+  launch_synth_dense_key(s->embed, (size_t)c.vocab * h, stream_key(seed, tensor_id(-1, SS_W_EMBED, 0)), 0, 0, 1.0f, 0);
+  launch_synth_dense_key(s->final_norm, h, stream_key(seed, tensor_id(-1, SS_W_FINAL_NORM, 0)), 0, 1, 0.f, 0);
+  float lm_scale = (float)(4.0 / std::sqrt((double)h));
+  launch_synth_lm_key(s->lm_head.d, s->V_l, s->V_off, c.vocab, h, s->lm_head.n_tg,
+                      stream_key(seed, tensor_id(-1, SS_W_LM_HEAD, 0)), lm_scale, 0);
+  s->global_mask = 0xFFFFFFFFu;
+  CUDA_TRY(cudaDeviceSynchronize());
+  (void)d;
+  return SS_OK;
+}
+
+static bool weights_complete(const ss_shard* s) {
+  const uint32_t need = (1u << SS_W_ATTN_NORM) | (1u << SS_W_Q) | (1u << SS_W_K) | (1u << SS_W_V) | (1u << SS_W_O) |
+                        (1u << SS_W_MLP_NORM) | (1u << SS_W_GATE) | (1u << SS_W_UP) | (1u << SS_W_DOWN);
+  for (uint32_t m : s->loaded_mask)
+    if ((m & need) != need) return false;
+  const uint32_t gneed = (1u << SS_W_EMBED) | (1u << SS_W_FINAL_NORM) | (1u << SS_W_LM_HEAD);
+  return (s->global_mask & gneed) == gneed;
+}
+
+// ------------------------------------------------------------ KV
+static ss_status write_L(ss_shard* s, int L) {
+  CUDA_TRY(cudaMemcpy(&s->dstate->L, &L, 4, cudaMemcpyHostToDevice));
+  s->L_host = L;
+  s->L_known = true;
+  s->L_upper = L;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k, const void* v, int32_t len) {
+  if (!s || (!k && len) || (!v && len)) FAIL(SS_EINVAL, "null argument");
+  const ss_model_cfg& c = s->cfg;
+  if (layer < 0 || layer >= c.n_layers) FAIL(SS_EINVAL, "layer out of range");
+  if (len < 0 || len + c.max_tree > c.max_ctx) FAIL(SS_ECAPACITY, "prefix + max_tree exceeds max_ctx");
+  cudaSetDevice(s->device);
+  const int d = c.head_dim, Hf = c.n_kv_heads, kv0 = s->rank * s->Hkv_l;
+  const int rows = round_up(std::max(len, 1), 64);
+  std::vector<uint16_t> buf((size_t)rows * d);
+  for (int which = 0; which < 2; ++which) {
+    const uint16_t* src = (const uint16_t*)(which ? v : k);
+    uint16_t* cache = which ? s->vcache : s->kcache;
+    for (int kh = 0; kh < s->Hkv_l; ++kh) {
+      std::fill(buf.begin(), buf.end(), 0);
+      for (int pos = 0; pos < len; ++pos)
+        for (int j = 0; j < d; ++j) {
+          int r = pos & 63, cidx = (j >> 3) ^ (r & 7);
+          buf[(size_t)(pos - r) * d + r * d + cidx * 8 + (j & 7)] = src[((size_t)pos * Hf + kv0 + kh) * d + j];
+        }
+      size_t base = ((size_t)layer * s->Hkv_l + kh) * s->max_ctx_pad * d;
+      CUDA_TRY(cudaMemcpy(cache + base, buf.data(), (size_t)rows * d * 2, cudaMemcpyHostToDevice));
+    }
+  }
+  s->max_rows_written = std::max(s->max_rows_written, len);
+  if (layer == c.n_layers - 1) return write_L(s, len);
+  return SS_OK;
+}
+
+extern "C" ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  const ss_model_cfg& c = s->cfg;
+  if (len < 0 || len + c.max_tree > c.max_ctx) FAIL(SS_ECAPACITY, "prefix + max_tree exceeds max_ctx");
+  cudaSetDevice(s->device);
+  for (int l = 0; l < c.n_layers; ++l) {
+    if (len == 0) break;
+    launch_synth_kv_key(s->kcache, l, c.n_kv_heads, s->Hkv_l, s->rank * s->Hkv_l, c.head_dim, len, s->max_ctx_pad,
+                        stream_key(seed, tensor_id(l, 12, 0)), 0);
+    launch_synth_kv_key(s->vcache, l, c.n_kv_heads, s->Hkv_l, s->rank * s->Hkv_l, c.head_dim, len, s->max_ctx_pad,
+                        stream_key(seed, tensor_id(l, 13, 0)), 0);
+  }
+  CUDA_TRY(cudaDeviceSynchronize());
+  s->max_rows_written = std::max(s->max_rows_written, len);
+  return write_L(s, len);
+}
+
+extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, void* k_out, void* v_out) {
+  if (!s || !k_out || !v_out) FAIL(SS_EINVAL, "null argument");
+  const ss_model_cfg& c = s->cfg;
+  if (layer < 0 || layer >= c.n_layers || row0 < 0 || n < 0 || row0 + n > s->max_ctx_pad)
+    FAIL(SS_EINVAL, "row range out of bounds");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  const int d = c.head_dim;
+  int b0 = row0 / 64 * 64, b1 = round_up(row0 + n, 64);
+  std::vector<uint16_t> buf((size_t)(b1 - b0) * d);
+  for (int which = 0; which < 2; ++which) {
+    uint16_t* dst = (uint16_t*)(which ? v_out : k_out);
+    const uint16_t* cache = which ? s->vcache : s->kcache;
+    for (int kh = 0; kh < s->Hkv_l; ++kh) {
+      size_t base = ((size_t)layer * s->Hkv_l + kh) * s->max_ctx_pad * d + (size_t)b0 * d;
+      CUDA_TRY(cudaMemcpy(buf.data(), cache + base, buf.size() * 2, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) {
+        int pos = row0 + i, r = pos & 63;
+        for (int j = 0; j < d; ++j) {
+          int cidx = (j >> 3) ^ (r & 7);
+          dst[((size_t)i * s->Hkv_l + kh) * d + j] = buf[(size_t)(pos - r - b0) * d + r * d + cidx * 8 + (j & 7)];
+        }
+      }
+    }
+  }
+  return SS_OK;
+}
+
+extern "C" ss_status ss_set_committed_len(ss_shard* s, int32_t L) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  if (L < 0 || L + s->cfg.max_tree > s->cfg.max_ctx) FAIL(SS_ECAPACITY, "length out of range");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  s->have_verify = false;
+  int zero = 0;
+  CUDA_TRY(cudaMemcpy(&s->dstate->have_verify, &zero, 4, cudaMemcpyHostToDevice));
+  return write_L(s, L);
+}
+
+extern "C" int32_t ss_committed_len(ss_shard* s) {
+  if (!s) return -1;
+  if (!s->L_known) {
+    cudaSetDevice(s->device);
+    int L = -1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpy(&L, &s->dstate->L, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    s->L_host = L;
+    s->L_upper = L;
+    s->L_known = true;
+  }
+  return s->L_host;
+}
+
+// ------------------------------------------------------------ the step
+static GemmArgs gemm_args(ss_shard* s, const PackedLinear& pl, const uint8_t* act, GemmScratch& sc, int kind,
+                          int layer) {
+  GemmArgs g;
+  g.W = pl.d;
+  g.act = act;
+  g.n_tg = pl.n_tg;
+  g.S = pl.S;
+  g.accum = sc.accum;
+  g.counters = sc.counters;
+  g.n_sm = s->n_sm;
+  EpiArgs& e = g.epi;
+  e.kind = kind;
+  e.st = s->dstate;
+  e.layer = layer;
+  e.d = s->cfg.head_dim;
+  e.Hq_l = s->Hq_l;
+  e.Hkv_l = s->Hkv_l;
+  e.G = s->G;
+  e.max_ctx_pad = s->max_ctx_pad;
+  e.qbuf = s->qbuf;
+  e.kc = s->kcache;
+  e.vc = s->vcache;
+  e.rope_cs = s->rope_cs;
+  e.x = s->x;
+  e.h = s->cfg.hidden;
+  e.rank = s->rank;
+  e.P = s->P;
+  e.n_tg_total = s->cfg.hidden / 128;
+  e.recv = s->recv;
+  for (int p = 0; p < s->P; ++p) e.peer_recv[p] = s->peer_recv[p];
+  e.act_out = s->act_d;
+  e.V_l = s->V_l;
+  e.V_off = s->V_off;
+  e.logits_ld = s->V_l_pad;
+  return g;
+}
+
+// Optional per-kernel event bracketing (ss_profile_step, eager launches only).
+struct Prof {
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  size_t next = 0;
+  cudaStream_t st = nullptr;
+  void begin(int kind) {
+    if (next == ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      ev.push_back({kind, {a, b}});
+    }
+    ev[next].first = kind;
+    cudaEventRecord(ev[next].second.first, st);
+  }
+  void end() { cudaEventRecord(ev[next++].second.second, st); }
+};
+static Prof* g_prof = nullptr;
+#define PROF_BEGIN(k) \
+  if (g_prof) g_prof->begin(k)
+#define PROF_END() \
+  if (g_prof) g_prof->end()
+
+// Enqueue everything after a0/a1 (the graph body).  Returns the kernel count.
+static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, cudaStream_t st) {
+  const ss_model_cfg& c = s->cfg;
+  int n = 0;
+  const int cap = s->launch_cap;
+  for (int l = 0; l < c.n_layers; ++l) {
+    LayerW& lw = s->layers[l];
+    GemmArgs g = gemm_args(s, lw.qkv, s->act_h, s->sc_qkv, EPI_QKV, l);
+    PROF_BEGIN(1);
+    n += launch_gemm(g, 0, NT, cap, st);
+    PROF_END();
+    AttnArgs a;
+    a.st = s->dstate;
+    a.layer = l;
+    a.Hkv_l = s->Hkv_l;
+    a.G = s->G;
+    a.d = c.head_dim;
+    a.max_ctx_pad = s->max_ctx_pad;
+    a.NT = NT;
+    a.qbuf = s->qbuf;
+    a.kc = s->kcache;
+    a.vc = s->vcache;
+    a.ws = s->attn_ws;
+    a.ml = s->attn_ml;
+    a.bar = s->attn_bar;
+    a.act_out = s->act_o;
+    PROF_BEGIN(2);
+    n += launch_attention(a, cap, st);
+    PROF_END();
+    g = gemm_args(s, lw.o, s->act_o, s->sc_o, EPI_RESID, l);
+    g.epi.ar_seq = 2 * l;
+    PROF_BEGIN(3);
+    n += launch_gemm(g, 0, NT, cap, st);
+    PROF_END();
+    PROF_BEGIN(4);
+    launch_prep_norm(s, lw.mlp_norm, NT, 0, st);
+    PROF_END();
+    ++n;
+    g = gemm_args(s, lw.gu, s->act_h, s->sc_gu, EPI_SWIGLU, l);
+    PROF_BEGIN(5);
+    n += launch_gemm(g, 0, NT, cap, st);
+    PROF_END();
+    g = gemm_args(s, lw.down, s->act_d, s->sc_down, EPI_RESID, l);
+    g.epi.ar_seq = 2 * l + 1;
+    PROF_BEGIN(6);
+    n += launch_gemm(g, 0, NT, cap, st);
+    PROF_END();
+    PROF_BEGIN(4);
+    launch_prep_norm(s, l + 1 < c.n_layers ? s->layers[l + 1].attn_norm : s->final_norm, NT,
+                     l + 1 < c.n_layers ? 0 : 1, st);
+    PROF_END();
+    ++n;
+  }
+  GemmArgs g = gemm_args(s, s->lm_head, s->act_lm, s->sc_lm, EPI_ARGMAX, 0);
+  g.epi.logits = want_logits ? s->logits_dev : nullptr;
+  g.epi.ar_seq = 2 * c.n_layers;
+  PROF_BEGIN(7);
+  n += launch_gemm(g, 1, NT, cap, st);
+  PROF_END();
+  if (auto_commit) {
+    PROF_BEGIN(8);
+    launch_commit(s, 1, st);
+    PROF_END();
+    ++n;
+  }
+  return n;
+}
+
+static ss_status get_graph(ss_shard* s, int NT, int auto_commit, int want_logits, Graph** out) {
+  int key = NT * 4 + auto_commit * 2 + want_logits;
+  auto it = s->graphs.find(key);
+  if (it != s->graphs.end()) {
+    *out = &it->second;
+    return SS_OK;
+  }
+  // warm the launch helpers (function attributes, occupancy) outside capture
+  Graph gr;
+  cudaGraph_t graph;
+  CUDA_TRY(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+  gr.kernels = enqueue_body(s, NT, auto_commit, want_logits, s->cap_stream);
+  cudaError_t e = cudaStreamEndCapture(s->cap_stream, &graph);
+  if (e != cudaSuccess) FAIL(SS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&gr.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) FAIL(SS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  s->graphs[key] = gr;
+  *out = &s->graphs[key];
+  return SS_OK;
+}
+
+static ss_status validate_tree(const ss_shard* s, const int32_t* tokens, const int32_t* parents, int T) {
+  if (!tokens || !parents) FAIL(SS_EINVAL, "null tree");
+  if (T < 1 || T > s->cfg.max_tree) FAIL(SS_EINVAL, "T out of [1, max_tree]");
+  if (parents[0] != -1) FAIL(SS_EINVAL, "parents[0] must be -1 (root first)");
+  for (int i = 1; i < T; ++i)
+    if (parents[i] < 0 || parents[i] >= i) FAIL(SS_EINVAL, "parents[i] must be in [0, i)");
+  for (int i = 0; i < T; ++i)
+    if (tokens[i] < 0 || tokens[i] >= s->cfg.vocab) FAIL(SS_EINVAL, "token out of vocab");
+  return SS_OK;
+}
+
+static ss_status check_ready(ss_shard* s, int T) {
+  if (!weights_complete(s)) FAIL(SS_ESTATE, "weights not fully loaded");
+  if (s->P > 1 && !s->peers_ready) FAIL(SS_ESTATE, "peers not imported (tp_size > 1)");
+  int L = s->L_known ? s->L_host : s->L_upper;
+  if (L + T > s->cfg.max_ctx) {
+    L = ss_committed_len(s);
+    if (L + T > s->cfg.max_ctx) FAIL(SS_ECAPACITY, "L + T exceeds max_ctx");
+  }
+  return SS_OK;
+}
+
+static ss_status run_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int T, int auto_commit,
+                          int want_logits, cudaStream_t st) {
+  const int NT = nt_of(T);
+  Graph* gr;
+  ss_status r = get_graph(s, NT, auto_commit, want_logits, &gr);
+  if (r != SS_OK) return r;
+  launch_embed_meta(s, d_tokens, d_parents, T, NT, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaGraphLaunch(gr->exec, st));
+  s->last_T = T;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T,
+                                    ss_verify_result* out, float* logits_out, void* stream) {
+  if (!s || !out) FAIL(SS_EINVAL, "null argument");
+  ss_status r = validate_tree(s, tokens, parents, T);
+  if (r != SS_OK) return r;
+  cudaSetDevice(s->device);
+  r = check_ready(s, T);
+  if (r != SS_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::memcpy(s->h_tree_in, tokens, T * 4);
+  std::memcpy(s->h_tree_in + SS_MAX_TREE, parents, T * 4);
+  CUDA_TRY(cudaMemcpyAsync(s->d_tree_in, s->h_tree_in, 2 * SS_MAX_TREE * 4, cudaMemcpyHostToDevice, st));
+  r = run_step(s, s->d_tree_in, s->d_tree_in + SS_MAX_TREE, T, 0, logits_out != nullptr, st);
+  if (r != SS_OK) return r;
+  CUDA_TRY(cudaMemcpyAsync(&s->hstate->result, &s->dstate->result, sizeof(ss_verify_result), cudaMemcpyDeviceToHost,
+                           st));
+  if (logits_out)
+    CUDA_TRY(cudaMemcpy2DAsync(logits_out, (size_t)s->V_l * 4, s->logits_dev, (size_t)s->V_l_pad * 4,
+                               (size_t)s->V_l * 4, T, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::memcpy(out, &s->hstate->result, sizeof(ss_verify_result));
+  s->have_verify = true;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
+                                        ss_verify_result* d_result, float* d_logits, int32_t auto_commit,
+                                        void* stream) {
+  if (!s || !d_tokens || !d_parents) FAIL(SS_EINVAL, "null argument");
+  if (T < 1 || T > s->cfg.max_tree) FAIL(SS_EINVAL, "T out of [1, max_tree]");
+  cudaSetDevice(s->device);
+  ss_status r = check_ready(s, T);
+  if (r != SS_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  r = run_step(s, d_tokens, d_parents, T, auto_commit ? 1 : 0, d_logits != nullptr, st);
+  if (r != SS_OK) return r;
+  if (d_result)
+    CUDA_TRY(cudaMemcpyAsync(d_result, &s->dstate->result, sizeof(ss_verify_result), cudaMemcpyDeviceToDevice, st));
+  if (d_logits)
+    CUDA_TRY(cudaMemcpy2DAsync(d_logits, (size_t)s->V_l * 4, s->logits_dev, (size_t)s->V_l_pad * 4,
+                               (size_t)s->V_l * 4, T, cudaMemcpyDeviceToDevice, st));
+  if (auto_commit) {
+    s->L_known = false;
+    s->L_upper += T;
+    s->have_verify = false;
+  } else {
+    s->have_verify = true;
+  }
+  return SS_OK;
+}
+
+extern "C" ss_status ss_commit_kv(ss_shard* s, const int32_t* accepted, int32_t n, void* stream) {
+  if (!s || !accepted) FAIL(SS_EINVAL, "null argument");
+  if (!s->have_verify) FAIL(SS_ESTATE, "commit without a preceding verify");
+  if (n < 1 || n > s->last_T) FAIL(SS_EINVAL, "n out of [1, T]");
+  if (accepted[0] != 0) FAIL(SS_EINVAL, "chain must start at the root (node 0)");
+  // chain: accepted[k] must be a child of accepted[k-1] in the last tree
+  int32_t hpar[SS_MAX_TREE];
+  cudaSetDevice(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(hpar, s->dstate->parents, sizeof(hpar), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int k = 1; k < n; ++k) {
+    if (accepted[k] <= 0 || accepted[k] >= s->last_T || hpar[accepted[k]] != accepted[k - 1])
+      FAIL(SS_EINVAL, "accepted is not a root-anchored chain of the last tree");
+  }
+  int L = ss_committed_len(s);
+  if (L < 0) FAIL(SS_ECUDA, "cannot read committed length");
+  std::vector<int32_t> buf(1 + SS_MAX_TREE, 0);
+  buf[0] = n;
+  for (int k = 0; k < n; ++k) buf[1 + k] = accepted[k];
+  static_assert(offsetof(DevState, commit_chain) == offsetof(DevState, commit_n) + 4, "layout");
+  CUDA_TRY(cudaMemcpyAsync(&s->dstate->commit_n, buf.data(), (1 + SS_MAX_TREE) * 4, cudaMemcpyHostToDevice, st));
+  launch_commit(s, 0, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  s->L_host = L + n;
+  s->L_upper = s->L_host;
+  s->L_known = true;
+  s->max_rows_written = std::max(s->max_rows_written, s->L_host);
+  s->have_verify = false;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_commit_accepted(ss_shard* s, void* stream) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  if (!s->have_verify) FAIL(SS_ESTATE, "commit without a preceding verify");
+  cudaSetDevice(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_commit(s, 1, st);
+  CUDA_TRY(cudaGetLastError());
+  s->L_known = false;
+  s->L_upper += s->last_T;
+  s->have_verify = false;
+  return SS_OK;
+}
+
+extern "C" int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_commit) {
+  if (!s || T < 1 || T > SS_MAX_TREE) return -1;
+  Graph* gr;
+  if (get_graph(s, nt_of(T), auto_commit ? 1 : 0, 0, &gr) != SS_OK) return -1;
+  return gr->kernels + 1;  // + the a0/a1 ingest kernel launched outside the graph
+}
+
+// ------------------------------------------------------------ peers (TP)
+extern "C" ss_status ss_export_handle(ss_shard* s, void* buf, size_t* len) {
+  if (!s || !buf || !len) FAIL(SS_EINVAL, "null argument");
+  if (s->P == 1) {
+    *len = 0;
+    return SS_OK;
+  }
+  cudaSetDevice(s->device);
+  cudaIpcMemHandle_t hnd;
+  CUDA_TRY(cudaIpcGetMemHandle(&hnd, s->recv));
+  std::memcpy(buf, &hnd, sizeof(hnd));
+  *len = sizeof(hnd);
+  return SS_OK;
+}
+
+extern "C" ss_status ss_import_peers(ss_shard* s, const void* const* blobs, const size_t* lens) {
+  if (!s || !blobs || !lens) FAIL(SS_EINVAL, "null argument");
+  cudaSetDevice(s->device);
+  for (int p = 0; p < s->P; ++p) {
+    if (p == s->rank) {
+      s->peer_recv[p] = s->recv;
+      continue;
+    }
+    if (lens[p] != sizeof(cudaIpcMemHandle_t)) FAIL(SS_EINVAL, "bad handle blob");
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, blobs[p], sizeof(hnd));
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, hnd, cudaIpcMemLazyEnablePeerAccess));
+    s->peer_recv[p] = (float*)ptr;
+    s->ipc_opened[p] = true;
+  }
+  s->peers_ready = true;
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" ss_status ss_import_local_peers(ss_shard* s, ss_shard* const* shards) {
+  if (!s || !shards) FAIL(SS_EINVAL, "null argument");
+  cudaSetDevice(s->device);
+  for (int p = 0; p < s->P; ++p) {
+    if (!shards[p] || shards[p]->P != s->P || shards[p]->rank != p) FAIL(SS_EINVAL, "shards must be given in rank order");
+    if (shards[p]->device != s->device) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(shards[p]->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) FAIL(SS_ECUDA, "peer access not available");
+      cudaGetLastError();
+    }
+    s->peer_recv[p] = shards[p]->recv;
+  }
+  s->peers_ready = true;
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
+                                     float* ms, int32_t* count, void* stream) {
+  if (!s || !d_tokens || !d_parents || !ms || !count) FAIL(SS_EINVAL, "null argument");
+  if (T < 1 || T > s->cfg.max_tree) FAIL(SS_EINVAL, "T out of [1, max_tree]");
+  cudaSetDevice(s->device);
+  ss_status r = check_ready(s, T);
+  if (r != SS_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  static Prof prof;
+  prof.next = 0;
+  prof.st = st;
+  const int NT = nt_of(T);
+  // make sure function attributes are set before timing
+  Graph* gr;
+  r = get_graph(s, NT, 1, 0, &gr);
+  if (r != SS_OK) return r;
+  g_prof = &prof;
+  prof.begin(0);
+  launch_embed_meta(s, d_tokens, d_parents, T, NT, st);
+  prof.end();
+  enqueue_body(s, NT, 1, 0, st);
+  g_prof = nullptr;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int k = 0; k < SS_PROF_KINDS; ++k) {
+    ms[k] = 0.f;
+    count[k] = 0;
+  }
+  for (size_t i = 0; i < prof.next; ++i) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, prof.ev[i].second.first, prof.ev[i].second.second));
+    ms[prof.ev[i].first] += t;
+    count[prof.ev[i].first] += 1;
+  }
+  s->L_known = false;
+  s->L_upper += T;
+  s->have_verify = false;
+  return SS_OK;
+}

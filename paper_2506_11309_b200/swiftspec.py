@@ -1,0 +1,261 @@
+"""Thin ctypes binding of libswiftspec.so (include/swiftspec.h).
+
+Argument marshalling only: every step of the verify path runs in the CUDA
+kernels behind the C-ABI.  There is no CPU fallback -- if the library (or a
+CUDA device) is missing, the import / the call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libswiftspec.so")
+
+SS_MAX_TREE = 64
+STATUS = {0: "SS_OK", -1: "SS_EINVAL", -2: "SS_ECAPACITY", -3: "SS_ECONSISTENCY", -4: "SS_ECUDA",
+          -5: "SS_ETIMEOUT", -6: "SS_ESTATE"}
+KIND = dict(EMBED=0, ATTN_NORM=1, WQ=2, WK=3, WV=4, WO=5, MLP_NORM=6, WGATE=7, WUP=8, WDOWN=9,
+            FINAL_NORM=10, LM_HEAD=11)
+SUB = dict(QWEIGHT=0, QZEROS=1, SCALES=2, DENSE=0)
+
+
+class SwiftSpecError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class ModelCfgC(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("hidden", C.c_int32), ("intermediate", C.c_int32),
+                ("n_heads", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("vocab", C.c_int32), ("group_size", C.c_int32), ("max_ctx", C.c_int32),
+                ("max_tree", C.c_int32), ("rms_eps", C.c_float), ("rope_theta", C.c_float)]
+
+
+class VerifyResultC(C.Structure):
+    _fields_ = [("n_accepted", C.c_int32), ("accepted", C.c_int32 * SS_MAX_TREE),
+                ("bonus_token", C.c_int32), ("argmax", C.c_int32 * SS_MAX_TREE), ("status", C.c_int32)]
+
+
+_lib = None
+
+EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_local_peers",
+           "ss_set_launch_cap", "ss_destroy", "ss_last_error", "ss_load_weights", "ss_synth_weights",
+           "ss_set_prefix_kv", "ss_synth_prefix_kv", "ss_read_kv", "ss_set_committed_len",
+           "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
+           "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step"]
+
+
+def lib():
+    """Load libswiftspec.so (built in-tree by paper_2506_11309_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2506_11309_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, u64, sz = C.c_void_p, C.c_int32, C.c_uint64, C.c_size_t
+    sig = {
+        "ss_init_shard": (i32, [C.POINTER(ModelCfgC), i32, i32, i32, C.POINTER(vp)]),
+        "ss_export_handle": (i32, [vp, vp, C.POINTER(sz)]),
+        "ss_import_peers": (i32, [vp, C.POINTER(vp), C.POINTER(sz)]),
+        "ss_import_local_peers": (i32, [vp, C.POINTER(vp)]),
+        "ss_set_launch_cap": (i32, [vp, i32]),
+        "ss_destroy": (i32, [vp]),
+        "ss_last_error": (C.c_char_p, []),
+        "ss_load_weights": (i32, [vp, i32, i32, i32, vp, sz]),
+        "ss_synth_weights": (i32, [vp, u64]),
+        "ss_set_prefix_kv": (i32, [vp, i32, vp, vp, i32]),
+        "ss_synth_prefix_kv": (i32, [vp, u64, i32]),
+        "ss_read_kv": (i32, [vp, i32, i32, i32, vp, vp]),
+        "ss_set_committed_len": (i32, [vp, i32]),
+        "ss_committed_len": (i32, [vp]),
+        "ss_verify_tree": (i32, [vp, vp, vp, i32, C.POINTER(VerifyResultC), vp, vp]),
+        "ss_verify_tree_dev": (i32, [vp, vp, vp, i32, vp, vp, i32, vp]),
+        "ss_commit_kv": (i32, [vp, vp, i32, vp]),
+        "ss_commit_accepted": (i32, [vp, vp]),
+        "ss_kernels_per_step": (i32, [vp, i32, i32]),
+        "ss_profile_step": (i32, [vp, vp, vp, i32, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code != 0:
+        raise SwiftSpecError(code, lib().ss_last_error().decode())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+class Shard:
+    """One tensor-parallel shard of the target model on one CUDA device."""
+
+    def __init__(self, cfg, tp_rank: int = 0, tp_size: int = 1, device: int = 0,
+                 max_ctx: int = 4096 + 128, max_tree: int = 64):
+        self.cfg = cfg
+        self.tp_rank, self.tp_size, self.device = tp_rank, tp_size, device
+        c = ModelCfgC(cfg.n_layers, cfg.hidden, cfg.intermediate, cfg.n_heads, cfg.n_kv_heads,
+                      cfg.head_dim, cfg.vocab, 128, max_ctx, max_tree, cfg.rms_eps, cfg.rope_theta)
+        h = C.c_void_p()
+        _check(lib().ss_init_shard(C.byref(c), tp_rank, tp_size, device, C.byref(h)))
+        self.h = h
+        self.max_ctx, self.max_tree = max_ctx, max_tree
+        vp = -(-cfg.vocab // tp_size)
+        self.v_off = tp_rank * vp
+        self.v_l = max(0, min(cfg.vocab, (tp_rank + 1) * vp) - self.v_off)
+        self.hkv_l = cfg.n_kv_heads // tp_size
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ss_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # ---- weights / KV
+    def load_tensor(self, layer: int, kind: int, sub: int, arr: np.ndarray):
+        a = np.ascontiguousarray(arr)
+        _check(lib().ss_load_weights(self.h, layer, kind, sub, _ptr(a), a.nbytes))
+
+    def load_canonical(self, m: dict):
+        """Load a canonical model dict (synth.gen_model layout)."""
+        names = dict(wq=KIND["WQ"], wk=KIND["WK"], wv=KIND["WV"], wo=KIND["WO"],
+                     wgate=KIND["WGATE"], wup=KIND["WUP"], wdown=KIND["WDOWN"])
+        for l, lw in enumerate(m["layers"]):
+            self.load_tensor(l, KIND["ATTN_NORM"], 0, lw["attn_norm"])
+            self.load_tensor(l, KIND["MLP_NORM"], 0, lw["mlp_norm"])
+            for n, k in names.items():
+                q, z, s = lw[n]
+                self.load_tensor(l, k, SUB["QWEIGHT"], q)
+                self.load_tensor(l, k, SUB["QZEROS"], z)
+                self.load_tensor(l, k, SUB["SCALES"], s)
+        self.load_tensor(0, KIND["EMBED"], 0, m["embed"])
+        self.load_tensor(0, KIND["FINAL_NORM"], 0, m["final_norm"])
+        self.load_tensor(0, KIND["LM_HEAD"], 0, m["lm_head"])
+
+    def synth_weights(self, seed: int):
+        _check(lib().ss_synth_weights(self.h, seed))
+
+    def set_prefix_kv(self, layer: int, k_bits: np.ndarray, v_bits: np.ndarray):
+        k = np.ascontiguousarray(k_bits, dtype=np.uint16)
+        v = np.ascontiguousarray(v_bits, dtype=np.uint16)
+        _check(lib().ss_set_prefix_kv(self.h, layer, _ptr(k), _ptr(v), k.shape[0]))
+
+    def synth_prefix_kv(self, seed: int, L: int):
+        _check(lib().ss_synth_prefix_kv(self.h, seed, L))
+
+    def read_kv(self, layer: int, row0: int, n: int):
+        d = self.cfg.head_dim
+        k = np.zeros((n, self.hkv_l, d), dtype=np.uint16)
+        v = np.zeros((n, self.hkv_l, d), dtype=np.uint16)
+        _check(lib().ss_read_kv(self.h, layer, row0, n, _ptr(k), _ptr(v)))
+        return k, v
+
+    def set_committed_len(self, L: int):
+        _check(lib().ss_set_committed_len(self.h, L))
+
+    @property
+    def L(self) -> int:
+        r = lib().ss_committed_len(self.h)
+        if r < 0:
+            raise SwiftSpecError(-4, lib().ss_last_error().decode())
+        return r
+
+    # ---- the step
+    def verify(self, tokens, parents, want_logits: bool = False, stream=None):
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        p = np.ascontiguousarray(parents, dtype=np.int32)
+        T = len(t)
+        res = VerifyResultC()
+        logits = np.zeros((T, self.v_l), dtype=np.float32) if want_logits else None
+        _check(lib().ss_verify_tree(self.h, _ptr(t), _ptr(p), T, C.byref(res),
+                                    _ptr(logits) if want_logits else None, _stream_handle(stream)))
+        n = res.n_accepted
+        return dict(n_accepted=n, accepted=list(res.accepted[:n]), bonus=res.bonus_token,
+                    argmax=list(res.argmax[:T]), status=res.status, logits=logits)
+
+    def verify_dev(self, d_tokens, d_parents, T: int, d_result=None, d_logits=None,
+                   auto_commit: bool = False, stream=None):
+        """All-device step: d_* are torch CUDA tensors (or raw pointers)."""
+        ptr = lambda x: None if x is None else (x if isinstance(x, int) else x.data_ptr())
+        _check(lib().ss_verify_tree_dev(self.h, ptr(d_tokens), ptr(d_parents), T, ptr(d_result),
+                                        ptr(d_logits), 1 if auto_commit else 0, _stream_handle(stream)))
+
+    def commit_kv(self, accepted, stream=None):
+        a = np.ascontiguousarray(accepted, dtype=np.int32)
+        _check(lib().ss_commit_kv(self.h, _ptr(a), len(a), _stream_handle(stream)))
+
+    def commit_accepted(self, stream=None):
+        _check(lib().ss_commit_accepted(self.h, _stream_handle(stream)))
+
+    def kernels_per_step(self, T: int, auto_commit: bool = False) -> int:
+        return lib().ss_kernels_per_step(self.h, T, 1 if auto_commit else 0)
+
+    PROF_KINDS = ["embed+tree", "qkv", "attention", "o_proj", "rmsnorm", "gate_up_swiglu", "down",
+                  "lm_head_argmax_accept", "commit"]
+
+    def profile_step(self, d_tokens, d_parents, T: int, stream=None):
+        """Eager step with CUDA events around every kernel -> {kind: (ms, launches)}."""
+        ms = np.zeros(9, dtype=np.float32)
+        cnt = np.zeros(9, dtype=np.int32)
+        ptr = lambda x: x if isinstance(x, int) else x.data_ptr()
+        _check(lib().ss_profile_step(self.h, ptr(d_tokens), ptr(d_parents), T, _ptr(ms), _ptr(cnt),
+                                     _stream_handle(stream)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PROF_KINDS)}
+
+    # ---- tensor parallel peers
+    def export_handle(self) -> bytes:
+        buf = C.create_string_buffer(4096)
+        n = C.c_size_t(0)
+        _check(lib().ss_export_handle(self.h, buf, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def import_peers(self, blobs):
+        arr = (C.c_void_p * len(blobs))()
+        keep = [C.create_string_buffer(b, len(b)) for b in blobs]
+        for i, k in enumerate(keep):
+            arr[i] = C.cast(k, C.c_void_p)
+        lens = (C.c_size_t * len(blobs))(*[len(b) for b in blobs])
+        _check(lib().ss_import_peers(self.h, arr, lens))
+
+    @staticmethod
+    def import_local_peers(shards):
+        arr = (C.c_void_p * len(shards))(*[s.h.value for s in shards])
+        for s in shards:
+            _check(lib().ss_import_local_peers(s.h, arr))
+
+    def set_launch_cap(self, cap: int):
+        _check(lib().ss_set_launch_cap(self.h, cap))
+
+
+def result_nbytes() -> int:
+    return C.sizeof(VerifyResultC)
+
+
+def parse_result(buf: np.ndarray, T: int) -> dict:
+    """Decode an ss_verify_result copied back from the device as raw int32s."""
+    a = np.asarray(buf, dtype=np.int32).reshape(-1)
+    n = int(a[0])
+    return dict(n_accepted=n, accepted=[int(x) for x in a[1:1 + n]], bonus=int(a[1 + SS_MAX_TREE]),
+                argmax=[int(x) for x in a[2 + SS_MAX_TREE:2 + SS_MAX_TREE + T]],
+                status=int(a[2 + 2 * SS_MAX_TREE]))

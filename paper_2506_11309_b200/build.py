@@ -41,8 +41,8 @@ def _deps_mtime(src: str) -> float:
     return max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in hdrs])
 
 
-def _compile(src: str, obj: str, verbose: bool) -> str:
-    cmd = [nvcc()] + ARCH + FLAGS + ["-c", src, "-o", obj]
+def _compile(src: str, obj: str, verbose: bool, defines=()) -> str:
+    cmd = [nvcc()] + ARCH + FLAGS + [f"-D{d}" for d in defines] + ["-c", src, "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -51,7 +51,13 @@ def _compile(src: str, obj: str, verbose: bool) -> str:
     return r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str = "") -> str:
+    """variant != "": experiment build (extra -D defines) into build_<variant>/ and
+    lib/libswiftspec_<variant>.so; the product library is always the plain one."""
+    global BUILD, LIB
+    if variant:
+        BUILD = os.path.join(HERE, "build_" + variant)
+        LIB = os.path.join(LIBDIR, f"libswiftspec_{variant}.so")
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
@@ -65,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     logs = []
     if todo:
         with cf.ThreadPoolExecutor(max_workers=min(8, len(todo))) as ex:
-            futs = [ex.submit(_compile, s, o, verbose) for s, o in todo]
+            futs = [ex.submit(_compile, s, o, verbose, defines) for s, o in todo]
             for f in futs:
                 logs.append(f.result())
     if todo or force or not os.path.exists(LIB):
@@ -82,5 +88,7 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--variant", default="")
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.defines, a.variant))

@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
   constexpr int QS = D + 8;  // padded Q row stride (elements)
   constexpr int TILE_ELEMS = kKvTile * D;
   uint16_t* Qs = reinterpret_cast<uint16_t*>(smem);
-  uint16_t* Ks = Qs + ROWS * QS;  // [2][64*D]
+  uint16_t* Ks = Qs + 2 * ROWS * QS;  // [2][64*D] after the Q hi / lo planes
   uint16_t* Vs = Ks + 2 * TILE_ELEMS;
 
   const int split = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
@@ -34,6 +34,8 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   DevState* st = a.st;
+  pdl_wait();
+  pdl_trigger();
   const int L = st->L, T = st->T;
   const int G = a.G;
   const int Mrows = G * T;
@@ -53,20 +55,23 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
     bulk_g2s_nohint(Ks, a.kc + head_base + (size_t)t0 * TILE_ELEMS, TILE_ELEMS * 2, &full[0]);
     bulk_g2s_nohint(Vs, a.vc + head_base + (size_t)t0 * TILE_ELEMS, TILE_ELEMS * 2, &full[0]);
   }
-  // Q rows [m0, m0 + ROWS) of this kv head (post-RoPE, from the QKV epilogue)
+  // Q rows [m0, m0 + ROWS) of this kv head (post-RoPE, from the QKV epilogue),
+  // as bf16 hi and lo planes: q = hi + lo carries ~16 mantissa bits, so the
+  // QK^T product is not limited by a bf16 rounding of q.
   const uint16_t* qsrc = a.qbuf + ((size_t)kvh * (G * SS_MAX_TREE) + m0) * D;
+  const size_t qplane = (size_t)a.Hkv_l * G * SS_MAX_TREE * D;
   for (int i = threadIdx.x; i < ROWS * (D / 8); i += NW * 32) {
     int r = i / (D / 8), c = i % (D / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (m0 + r < Mrows) v = *reinterpret_cast<const uint4*>(qsrc + (size_t)r * D + c * 8);
+    uint4 v = make_uint4(0, 0, 0, 0), w = make_uint4(0, 0, 0, 0);
+    if (m0 + r < Mrows) {
+      v = *reinterpret_cast<const uint4*>(qsrc + (size_t)r * D + c * 8);
+      w = *reinterpret_cast<const uint4*>(qsrc + qplane + (size_t)r * D + c * 8);
+    }
     *reinterpret_cast<uint4*>(Qs + r * QS + c * 8) = v;
+    *reinterpret_cast<uint4*>(Qs + (ROWS + r) * QS + c * 8) = w;
   }
   __syncthreads();
-
-  uint32_t qf[D / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < D / 16; ++kk)
-    ldmatrix_x4(qf[kk], Qs + (warp * 16 + (lane & 15)) * QS + kk * 16 + (lane >> 4) * 8);
+  const uint16_t* qrow = Qs + (warp * 16 + (lane & 15)) * QS + (lane >> 4) * 8;
 
   const int rowA = m0 + warp * 16 + gq, rowB = rowA + 8;
   const int tokA = min(rowA / G, SS_MAX_TREE - 1), tokB = min(rowB / G, SS_MAX_TREE - 1);
@@ -83,6 +88,7 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
     const int b = (it - t0) & 1;
     const uint32_t phase = ((it - t0) >> 1) & 1;
     if (threadIdx.x == 0 && it + 1 < t1) {
+      fence_proxy_async_smem();  // ldmatrix reads of this buffer (previous tile) before the TMA overwrite
       mbar_expect_tx(&full[b ^ 1], 2 * TILE_ELEMS * 2);
       bulk_g2s_nohint(Ks + (b ^ 1) * TILE_ELEMS, a.kc + head_base + (size_t)(it + 1) * TILE_ELEMS, TILE_ELEMS * 2,
                       &full[b ^ 1]);
@@ -98,14 +104,19 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
     for (int n = 0; n < 8; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t qh[4], ql[4];
+      ldmatrix_x4(qh, qrow + kk * 16);
+      ldmatrix_x4(ql, qrow + ROWS * QS + kk * 16);
 #pragma unroll
       for (int np = 0; np < 4; ++np) {
         const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
         const int ch = kk * 2 + ((lane >> 3) & 1);
         uint32_t kb[4];
         ldmatrix_x4(kb, Kt + key * D + ((ch ^ (key & 7)) << 3));
-        mma_bf16_16816(sc[2 * np], qf[kk], kb[0], kb[1]);
-        mma_bf16_16816(sc[2 * np + 1], qf[kk], kb[2], kb[3]);
+        mma_bf16_16816(sc[2 * np], qh, kb[0], kb[1]);
+        mma_bf16_16816(sc[2 * np + 1], qh, kb[2], kb[3]);
+        mma_bf16_16816(sc[2 * np], ql, kb[0], kb[1]);
+        mma_bf16_16816(sc[2 * np + 1], ql, kb[2], kb[3]);
       }
     }
     // mask (prefix always visible; tree rows by ancestor bit; beyond L+T never)
@@ -132,15 +143,19 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
     const float uA = (mnA == -INFINITY) ? 0.f : mnA, uB = (mnB == -INFINITY) ? 0.f : mnB;
     const float alA = exp2f(mA - uA), alB = exp2f(mB - uB);
     float sumA = 0.f, sumB = 0.f;
-    uint32_t pa[4][4];
+    // probabilities as bf16 hi + lo (V is bf16 in the cache)
+    uint32_t pa[4][4], pl[4][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
       float p0 = exp2f(sc[n][0] - uA), p1 = exp2f(sc[n][1] - uA);
       float p2 = exp2f(sc[n][2] - uB), p3 = exp2f(sc[n][3] - uB);
       sumA += p0 + p1;
       sumB += p2 + p3;
-      pa[n >> 1][(n & 1) * 2 + 0] = pack_bf16x2(p0, p1);
-      pa[n >> 1][(n & 1) * 2 + 1] = pack_bf16x2(p2, p3);
+      uint32_t h01 = pack_bf16x2(p0, p1), h23 = pack_bf16x2(p2, p3);
+      pa[n >> 1][(n & 1) * 2 + 0] = h01;
+      pa[n >> 1][(n & 1) * 2 + 1] = h23;
+      pl[n >> 1][(n & 1) * 2 + 0] = pack_bf16x2(p0 - bf16_lo(h01), p1 - bf16_hi(h01));
+      pl[n >> 1][(n & 1) * 2 + 1] = pack_bf16x2(p2 - bf16_lo(h23), p3 - bf16_hi(h23));
     }
     sumA += __shfl_xor_sync(0xffffffffu, sumA, 1);
     sumA += __shfl_xor_sync(0xffffffffu, sumA, 2);
@@ -164,6 +179,8 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
         ldmatrix_x4_trans(vb, Vt + key * D + ((ch ^ (key & 7)) << 3));
         mma_bf16_16816(o[2 * dp], pa[kk], vb[0], vb[1]);
         mma_bf16_16816(o[2 * dp + 1], pa[kk], vb[2], vb[3]);
+        mma_bf16_16816(o[2 * dp], pl[kk], vb[0], vb[1]);
+        mma_bf16_16816(o[2 * dp + 1], pl[kk], vb[2], vb[3]);
       }
     }
     __syncthreads();  // buffer b is refilled two iterations later
@@ -185,40 +202,74 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
       *reinterpret_cast<float2*>(ml + rb * 2) = make_float2(mB, lB);
     }
   }
-  // ---- meet the other splits of this (kv head, row chunk)
+  // ---- meet the other splits of this (kv head, row chunk): every thread
+  // fences its partial stores, one thread arrives and spins on the flag.
+  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     atomicAdd(&a.bar[grp * 2], 1);
     while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) {
     }
     __threadfence();
   }
   __syncthreads();
-  // ---- merge a slice of the rows across the S splits (log-sum-exp, R11)
-  const int r_lo = split * ROWS / S, r_hi = (split + 1) * ROWS / S;
-  const float* wsg = a.ws + ((size_t)grp * S * 256) * D;
-  const float* mlg = a.ml + ((size_t)grp * S * 256) * 2;
-  for (int i = threadIdx.x; i < (r_hi - r_lo) * (D / 2); i += NW * 32) {
-    const int r = r_lo + i / (D / 2), dp = i % (D / 2);
-    const int m = m0 + r;
-    if (m >= Mrows) continue;
-    float mstar = -INFINITY;
-    for (int s2 = 0; s2 < S; ++s2) mstar = fmaxf(mstar, __ldcg(mlg + ((size_t)s2 * 256 + r) * 2));
-    float l = 0.f, v0 = 0.f, v1 = 0.f;
-    for (int s2 = 0; s2 < S; ++s2) {
-      float ms = __ldcg(mlg + ((size_t)s2 * 256 + r) * 2);
-      if (ms == -INFINITY) continue;
-      float w = exp2f(ms - mstar);
-      l += w * __ldcg(mlg + ((size_t)s2 * 256 + r) * 2 + 1);
-      float2 ov = __ldcg(reinterpret_cast<const float2*>(wsg + ((size_t)s2 * 256 + r) * D + 2 * dp));
-      v0 += w * ov.x;
-      v1 += w * ov.y;
+  __threadfence();
+  // ---- merge a slice of the rows across the S splits (log-sum-exp, R11).
+  // Items = (row, 4-float chunk); the CTA's items are a contiguous slice.  The
+  // per-(row, split) weights exp2(m_s - m*) / l* go through shared memory, and
+  // every thread issues its S partial loads back to back (no serial L2 chain).
+  {
+    float* s_w = reinterpret_cast<float*>(Ks);  // reuse the K/V ring: [rows_here][S]
+    const int n_items = ROWS * (D / 4);
+    const int i_lo = (int)((long)split * n_items / S), i_hi = (int)((long)(split + 1) * n_items / S);
+    const int r_first = i_lo / (D / 4), r_last = (i_hi - 1) / (D / 4);
+    const int nr = (i_hi > i_lo) ? r_last - r_first + 1 : 0;
+    const float* wsg = a.ws + ((size_t)grp * S * 256) * D;
+    const float* mlg = a.ml + ((size_t)grp * S * 256) * 2;
+    for (int i = threadIdx.x; i < nr * S; i += NW * 32) {
+      int rr = i / S, s2 = i % S;
+      float2 v = __ldcg(reinterpret_cast<const float2*>(mlg + ((size_t)s2 * 256 + r_first + rr) * 2));
+      s_w[i] = v.x;
+      s_w[nr * S + i] = v.y;
     }
-    const float inv = 1.f / l;
-    const int t = m / G, hq = kvh * G + (m % G);
-    const int k = hq * D + 2 * dp;
-    *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k, a.NT)) = pack_half2(v0 * inv, v1 * inv);
+    __syncthreads();
+    for (int rr = warp; rr < nr; rr += NW) {  // one warp per row: m*, l*, weights
+      float mx = -INFINITY;
+      for (int s2 = lane; s2 < S; s2 += 32) mx = fmaxf(mx, s_w[rr * S + s2]);
+      mx = warp_max(mx);
+      float l = 0.f;
+      for (int s2 = lane; s2 < S; s2 += 32) {
+        float ms = s_w[rr * S + s2];
+        float w = (ms == -INFINITY) ? 0.f : exp2f(ms - mx);
+        l += w * s_w[nr * S + rr * S + s2];
+        s_w[rr * S + s2] = w;
+      }
+      l = warp_sum(l);
+      __syncwarp();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      for (int s2 = lane; s2 < S; s2 += 32) s_w[rr * S + s2] *= inv;
+    }
+    __syncthreads();
+    for (int it = i_lo + threadIdx.x; it < i_hi; it += NW * 32) {
+      const int r = it / (D / 4), c4 = it % (D / 4);
+      const int m = m0 + r;
+      if (m >= Mrows) continue;
+      const float* wr = s_w + (r - r_first) * S;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+      for (int s2 = 0; s2 < S; ++s2) {
+        const float w = wr[s2];
+        const float4 ov = __ldcg(reinterpret_cast<const float4*>(wsg + ((size_t)s2 * 256 + r) * D + 4 * c4));
+        acc.x += w * ov.x;
+        acc.y += w * ov.y;
+        acc.z += w * ov.z;
+        acc.w += w * ov.w;
+      }
+      const int t = m / G, hq = kvh * G + (m % G);
+      const int k = hq * D + 4 * c4;
+      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k, a.NT)) = pack_half2(acc.x, acc.y);
+      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k + 2, a.NT)) = pack_half2(acc.z, acc.w);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -232,7 +283,7 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
 
 template <int D, int NW>
 static size_t attn_smem() {
-  return (size_t)NW * 16 * (D + 8) * 2 + 4 * (size_t)kKvTile * D * 2;
+  return 2 * (size_t)NW * 16 * (D + 8) * 2 + 4 * (size_t)kKvTile * D * 2;
 }
 
 template <int D, int NW>
@@ -283,11 +334,11 @@ static int launch_d(const AttnArgs& a0, int max_ctas, cudaStream_t st) {
   a.zchunks = Z;
   dim3 grid(S, a.Hkv_l, Z);
   switch (nw) {
-    case 1: attn_kernel<D, 1><<<grid, 32, attn_smem<D, 1>(), st>>>(a); break;
-    case 2: attn_kernel<D, 2><<<grid, 64, attn_smem<D, 2>(), st>>>(a); break;
-    case 4: attn_kernel<D, 4><<<grid, 128, attn_smem<D, 4>(), st>>>(a); break;
-    case 8: attn_kernel<D, 8><<<grid, 256, attn_smem<D, 8>(), st>>>(a); break;
-    default: attn_kernel<D, 16><<<grid, 512, attn_smem<D, 16>(), st>>>(a); break;
+    case 1: launch_pdl(attn_kernel<D, 1>, grid, dim3(32), attn_smem<D, 1>(), st, a); break;
+    case 2: launch_pdl(attn_kernel<D, 2>, grid, dim3(64), attn_smem<D, 2>(), st, a); break;
+    case 4: launch_pdl(attn_kernel<D, 4>, grid, dim3(128), attn_smem<D, 4>(), st, a); break;
+    case 8: launch_pdl(attn_kernel<D, 8>, grid, dim3(256), attn_smem<D, 8>(), st, a); break;
+    default: launch_pdl(attn_kernel<D, 16>, grid, dim3(512), attn_smem<D, 16>(), st, a); break;
   }
   return 1;
 }

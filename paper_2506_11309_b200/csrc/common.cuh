@@ -31,14 +31,16 @@ constexpr int kKvTile = 64;          // keys per attention tile
 // Activation "fragment order" (B operand of mma.m16n8k16, col layout).  W4
 // GEMM inputs are fp16 (exact integer weights (q - z) in fp16, DESIGN.md
 // "Precision"); the LM-head input is split bf16 hi/lo in 2*NT n-tiles.
-// element (token tt, k) of a [T][K] activation lives at
-//   ((k/16 * NT + tt/8) * 32 + lane) * 8 + word * 4 + half * 2   bytes,
-//   lane = (tt%8)*4 + ((k%16)%8)/2, word = (k%16)/8, half = k%2.
+// Element (token tt, k) of a [T][K] activation lives at
+//   (((k/32 * NT + tt/8) * 32 + lane) * 16 + ((k/16)%2) * 8 + word * 4 + half * 2  bytes,
+//   lane = (tt%8)*4 + ((k%16)%8)/2, word = (k%16)/8, half = k%2,
+// so one LDS.128 per lane yields the B fragments of two consecutive k16 steps.
 SS_DEV uint32_t act_frag_offset(int tt, int k, int NT) {
   int kk = k & 15;
   int lane = ((tt & 7) << 2) | ((kk & 7) >> 1);
   int word = kk >> 3;
-  return ((uint32_t)(((k >> 4) * NT + (tt >> 3)) * 32 + lane) << 3) + (word << 2) + ((k & 1) << 1);
+  return ((uint32_t)(((k >> 5) * NT + (tt >> 3)) * 32 + lane) << 4) + (((k >> 4) & 1) << 3) + (word << 2) +
+         ((k & 1) << 1);
 }
 
 // Swizzled KV cache row layout: 64-row blocks, 16-byte chunk index XORed
@@ -96,6 +98,15 @@ SS_DEV uint64_t policy_evict_last() {
   return p;
 }
 
+// Programmatic dependent launch (PDL): the next kernel in the stream may start
+// its prologue while this one drains; it must wait before reading our outputs.
+SS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Order this thread's (and, after a barrier, the CTA's) generic-proxy shared
+// memory accesses before subsequent async-proxy (TMA / bulk copy) accesses.
+SS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 SS_DEV void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -124,15 +135,26 @@ SS_DEV void red_add_v2(float* p, float a, float b) {
   asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
-// int4 nibble word -> 4 x f16x2 holding (1024 + q): lop3 with the 0x6400
-// exponent (1024.0 in fp16, ulp 1).  Nibble positions (0,4) -> r0, (1,5) ->
-// r1, (2,6) -> r2, (3,7) -> r3.
+// int4 nibble word -> the 4 f16x2 A-fragment registers of one m16n8k16 step.
+// Nibble e_p sits at bits [4p, 4p+4); (e0,e4) -> r0, (e1,e5) -> r1, (e2,e6)
+// -> r2, (e3,e7) -> r3.  lop3 with the fp16 exponent 0x6400 (1024, ulp 1)
+// turns a nibble at bits 0-3 of a half into 1024 + e and one at bits 4-7
+// into 1024 + 16 e; the second pair needs w >> 8, done as mul.hi on the FMA
+// pipe so the ALU pipe only runs the four lop3.  r1/r3 carry the factor 16,
+// which the zero-point fma removes exactly (see gemm.cu).
 SS_DEV void dequant8(uint32_t w, uint32_t* r) {
-  const uint32_t mask = 0x000F000Fu, magic = 0x64006400u;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[0]) : "r"(w), "r"(mask), "r"(magic));
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[1]) : "r"(w >> 4), "r"(mask), "r"(magic));
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[2]) : "r"(w >> 8), "r"(mask), "r"(magic));
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[3]) : "r"(w >> 12), "r"(mask), "r"(magic));
+  const uint32_t lo = 0x000F000Fu, hi = 0x00F000F0u, magic = 0x64006400u;
+  uint32_t w8;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(w8) : "r"(w), "r"(0x01000000u));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[0]) : "r"(w), "r"(lo), "r"(magic));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[1]) : "r"(w), "r"(hi), "r"(magic));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[2]) : "r"(w8), "r"(lo), "r"(magic));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[3]) : "r"(w8), "r"(hi), "r"(magic));
+}
+SS_DEV uint32_t f16x2_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
 }
 SS_DEV uint32_t f16x2_sub(uint32_t a, uint32_t b) {
   uint32_t r;

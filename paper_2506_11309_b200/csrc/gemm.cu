@@ -31,7 +31,12 @@ struct GemmCfg {
   static constexpr int ANT = WFMT == 0 ? NT : 2 * NT;  // LM head: bf16 hi + lo tiles
   static constexpr int ABYTES = (KS / 16) * ANT * 256;
   static constexpr int UBYTES = WBYTES + ABYTES;
-  static constexpr int STAGES = (UBYTES * 4 <= 104 * 1024) ? 4 : ((UBYTES * 6 <= 200 * 1024) ? 6 : 4);
+  // NT <= 2: 3 stages (~63-76 KB) -> 3 CTAs / SM; larger NT: 4 stages, 1-2 CTAs / SM
+#ifdef SS_EXP_STAGES
+  static constexpr int STAGES = SS_EXP_STAGES;
+#else
+  static constexpr int STAGES = (UBYTES <= 26 * 1024) ? 3 : 4;
+#endif
   static constexpr int SMEM = STAGES * UBYTES + 1024;
   static constexpr int THREADS = 288;  // 8 consumer warps + 1 producer warp
 };
@@ -56,9 +61,11 @@ __device__ void epi_qkv(const EpiArgs& e, int tg, const float* acc, int T) {
       v = (j < half) ? (v * cs.x - pv * cs.y) : (v * cs.x + pv * cs.y);
     }
     uint16_t b = f32_to_bf16_bits(v);
-    if (row < nq) {
+    if (row < nq) {  // q as bf16 hi + lo planes (attention.cu)
       int hq = row / d, kvh = hq / e.G, jj = hq - kvh * e.G;
-      e.qbuf[((size_t)kvh * (e.G * SS_MAX_TREE) + t * e.G + jj) * d + j] = b;
+      size_t qi = ((size_t)kvh * (e.G * SS_MAX_TREE) + t * e.G + jj) * d + j;
+      e.qbuf[qi] = b;
+      e.qbuf[qi + (size_t)e.Hkv_l * e.G * SS_MAX_TREE * d] = f32_to_bf16_bits(v - bf16_bits_to_f32(b));
     } else {
       int kvh = (row < nq + nk) ? (row - nq) / d : (row - nq - nk) / d;
       uint16_t* c = (row < nq + nk) ? e.kc : e.vc;
@@ -229,22 +236,44 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
+#ifdef SS_EXP_ALLARRIVE
+      mbar_init(&empty[s], 256);
+#else
       mbar_init(&empty[s], 8);
+#endif
     }
     fence_mbar_init();
     s_ndone = 0;
   }
   __syncthreads();
-  const int T = g.epi.st->T;
 
   if (warp == 8) {
-    // ---------------- producer: TMA bulk copies into the stage ring
+    // ---------------- producer: TMA bulk copies into the stage ring.  The
+    // weights do not depend on earlier kernels, so the first STAGES units'
+    // weights are requested before the PDL wait (overlapping the previous
+    // kernel's tail); activations only after it.
     if (lane == 0) {
       uint64_t pol = policy_evict_first();
-      int s = 0;
-      uint32_t ph = 0;
-      for (long u = u0; u < u1; ++u) {
+      const long npre = min((long)C::STAGES, u1 - u0);
+      for (long i = 0; i < npre; ++i) {
+        uint8_t* dst = smem + i * C::UBYTES;
+        mbar_expect_tx(&full[i], C::UBYTES);
+        bulk_g2s(dst, g.W + (size_t)(u0 + i) * C::WBYTES, C::WBYTES, &full[i], pol);
+      }
+      pdl_wait();
+      for (long i = 0; i < npre; ++i) {
+        int ks = (int)((u0 + i) % g.S);
+        bulk_g2s_nohint(smem + i * C::UBYTES + C::WBYTES, g.act + (size_t)ks * C::ABYTES, C::ABYTES, &full[i]);
+      }
+      int s = (int)(npre % C::STAGES);
+      uint32_t ph = (npre == C::STAGES) ? 1u : 0u;
+      for (long u = u0 + npre; u < u1; ++u) {
         mbar_wait(&empty[s], ph ^ 1);
+        // the consumers' generic-proxy reads of this stage must be ordered
+        // before the async-proxy (TMA) overwrite: without this fence a stage
+        // can be refilled under a slow reader (observed as whole-tile-group
+        // errors at 3-4 CTAs/SM).
+        fence_proxy_async_smem();
         uint8_t* dst = smem + s * C::UBYTES;
         mbar_expect_tx(&full[s], C::UBYTES);
         bulk_g2s(dst, g.W + (size_t)u * C::WBYTES, C::WBYTES, &full[s], pol);
@@ -255,6 +284,9 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
     }
     return;  // producer warp does not take part in epilogues
   }
+  pdl_wait();
+  pdl_trigger();
+  const int T = g.epi.st->T;
 
   // ---------------- consumers
   const int gq = lane >> 2, tq = lane & 3;
@@ -271,17 +303,20 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
     for (; u < tg_end; ++u) {
       mbar_wait(&full[s], ph);
       const uint8_t* stw = smem + s * C::UBYTES;
-      const uint2* sta = reinterpret_cast<const uint2*>(stw + C::WBYTES);
       if constexpr (WFMT == 0) {
         const uint4* wl = reinterpret_cast<const uint4*>(stw) + warp * 128;
         const uint16_t* sc = reinterpret_cast<const uint16_t*>(stw + kW4Bytes) + warp * 32;
         const uint2* zp = reinterpret_cast<const uint2*>(stw + kW4Bytes + 512) + warp * 2;
+        const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
 #pragma unroll
         for (int grp = 0; grp < 2; ++grp) {
           uint2 zz = zp[grp];
           uint64_t z64 = ((uint64_t)zz.y << 32) | zz.x;
           uint32_t z0 = (uint32_t)(z64 >> (4 * gq)) & 15u, z8 = (uint32_t)(z64 >> (4 * (gq + 8))) & 15u;
-          uint32_t zz0 = (0x6400u + z0) * 0x10001u, zz8 = (0x6400u + z8) * 0x10001u;
+          // rows g: subtract fp16(1024 + z); rows g+8: (1024 + 16 q) / 16 - fp16(64 + z)
+          const uint32_t zA = (0x6400u + z0) * 0x10001u;
+          const uint32_t zB = (0xD400u + (z8 << 4)) * 0x10001u;  // -(64 + z) in fp16
+          const uint32_t sixteenth = 0x2C002C00u;                 // 1/16 in fp16
           float cg[NT][4];
 #pragma unroll
           for (int n = 0; n < NT; ++n) cg[n][0] = cg[n][1] = cg[n][2] = cg[n][3] = 0.f;
@@ -291,18 +326,27 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
             uint4 wv = wl[kb * 32 + lane];
             uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t a[4];
-              dequant8(wa[j], a);
-              a[0] = f16x2_sub(a[0], zz0);
-              a[1] = f16x2_sub(a[1], zz8);
-              a[2] = f16x2_sub(a[2], zz0);
-              a[3] = f16x2_sub(a[3], zz8);
-              const int kstep = kb * 4 + j;
+            for (int jp = 0; jp < 2; ++jp) {
+              uint4 bb[NT];
 #pragma unroll
-              for (int n = 0; n < NT; ++n) {
-                uint2 b = sta[(kstep * NT + n) * 32 + lane];
-                mma_f16_16816(cg[n], a, b.x, b.y);
+              for (int n = 0; n < NT; ++n) bb[n] = sa[((kb * 2 + jp) * NT + n) * 32 + lane];
+#pragma unroll
+              for (int js = 0; js < 2; ++js) {
+                uint32_t a[4];
+#ifdef SS_EXP_NODEQ
+                a[0] = wa[jp * 2 + js]; a[1] = a[0] ^ 0x1111u; a[2] = a[0] ^ 0x2222u; a[3] = a[0] ^ 0x3333u;
+#else
+                dequant8(wa[jp * 2 + js], a);
+#endif
+#ifndef SS_EXP_NOZERO
+                a[0] = f16x2_sub(a[0], zA);
+                a[1] = f16x2_fma(a[1], sixteenth, zB);
+                a[2] = f16x2_sub(a[2], zA);
+                a[3] = f16x2_fma(a[3], sixteenth, zB);
+#endif
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+                  mma_f16_16816(cg[n], a, js ? bb[n].z : bb[n].x, js ? bb[n].w : bb[n].y);
               }
             }
           }
@@ -317,21 +361,29 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
         }
       } else {
         const uint4* wl = reinterpret_cast<const uint4*>(stw) + warp * 128;
+        const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 wv = wl[j * 32 + lane];
-          uint32_t a[4] = {wv.x, wv.y, wv.z, wv.w};
+        for (int jp = 0; jp < 2; ++jp) {
 #pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            uint2 bh = sta[(j * 2 * NT + n) * 32 + lane];
-            uint2 bl = sta[(j * 2 * NT + NT + n) * 32 + lane];
-            mma_bf16_16816(acc[n], a, bh.x, bh.y);
-            mma_bf16_16816(acc[n], a, bl.x, bl.y);
+          for (int js = 0; js < 2; ++js) {
+            uint4 wv = wl[(jp * 2 + js) * 32 + lane];
+            uint32_t a[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              uint4 bh = sa[(jp * 2 * NT + n) * 32 + lane];
+              uint4 bl = sa[(jp * 2 * NT + NT + n) * 32 + lane];
+              mma_bf16_16816(acc[n], a, js ? bh.z : bh.x, js ? bh.w : bh.y);
+              mma_bf16_16816(acc[n], a, js ? bl.z : bl.x, js ? bl.w : bl.y);
+            }
           }
         }
       }
+#ifdef SS_EXP_ALLARRIVE
+      mbar_arrive(&empty[s]);
+#else
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+#endif
       if (++s == C::STAGES) { s = 0; ph ^= 1; }
     }
     // ---- flush this tile-group's partial
@@ -345,9 +397,12 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
         acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
       }
     }
+    // every thread's reductions must be performed (device scope) before the
+    // arrival is counted: a fence by thread 0 alone does not cover the other
+    // threads' in-flight red.global ops.
+    __threadfence();
     named_bar_sync(1, 256);
     if (threadIdx.x == 0) {
-      __threadfence();
       int old = atomicAdd(&g.counters[tg], nst);
       s_last = (old + nst == g.S);
       if (s_last) __threadfence();
@@ -371,9 +426,9 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
       for (int i = threadIdx.x; i < 128 * NT * 8; i += 256) accw[i] = 0.f;
       if (threadIdx.x == 0) g.counters[tg] = 0;
       if constexpr (EPI == EPI_ARGMAX) {
+        __threadfence();  // this CTA's argmax atomics (all threads) before the arrival
         named_bar_sync(1, 256);
         if (threadIdx.x == 0) {
-          __threadfence();
           int old = atomicAdd(&g.epi.st->lm_done, 1);
           if (old == g.n_tg - 1) {
             __threadfence();
@@ -407,9 +462,11 @@ static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
     attr_set = true;
   }
   long U = (long)g.n_tg * g.S;
-  int grid = (int)std::min<long>(U, (long)g.n_sm * occ);
+  static const int occ_cap = getenv("SS_GEMM_OCC") ? atoi(getenv("SS_GEMM_OCC")) : 0;  // debugging aid
+  int o = (occ_cap > 0 && occ_cap < occ) ? occ_cap : occ;
+  int grid = (int)std::min<long>(U, (long)g.n_sm * o);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  k<<<grid, C::THREADS, C::SMEM, st>>>(g);
+  launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, g);
   return 1;
 }
 

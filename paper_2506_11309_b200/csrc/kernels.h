@@ -3,11 +3,33 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <algorithm>
+#include <utility>
+#include <cstdlib>
 #include "internal.h"
 
 namespace ss {
 
 enum { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_ARGMAX = 3 };
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while its predecessor drains; kernels call pdl_wait() before consuming
+// their predecessors' outputs.  Works under stream capture (graph edges).
+template <typename... ExpT, typename... ActT>
+inline cudaError_t launch_pdl(void (*k)(ExpT...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              ActT&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  static const bool no_pdl = getenv("SS_NO_PDL") != nullptr;  // debugging aid
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<ActT>(args)...);
+}
 
 struct EpiArgs {
   int kind = 0;

@@ -15,6 +15,20 @@ namespace ss {
 // ancestor-or-self bitmasks.  CTA t < T gathers E[token] (P:501 bf16
 // embedding) into the fp32 residual and writes RMSNorm(x) * g (layer 0 attn
 // norm) into the fragment-ordered activation; slots t >= T are zeroed.
+constexpr int kNormSplit = 4;   // CTAs per token for the row kernels
+constexpr int kMaxVec = 8;      // h <= 256 threads * 4 * kMaxVec = 8192
+
+// Block reduction of one float across 256 threads (result in every thread).
+SS_DEV float block_sum_256(float v, float* s_red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r += s_red[i];
+  return r;
+}
+
 __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int32_t* tokens,
                                                          const int32_t* parents, int T_in, const uint16_t* E,
                                                          int V, int h, float* x, const uint16_t* gain,
@@ -22,6 +36,8 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
   __shared__ int s_tok[SS_MAX_TREE], s_par[SS_MAX_TREE];
   __shared__ int s_bad;
   __shared__ float s_red[8];
+  pdl_wait();
+  pdl_trigger();
   const int tid = threadIdx.x;
   const int T = min(max(T_in, 1), SS_MAX_TREE);
   if (tid == 0) s_bad = (T_in < 1 || T_in > SS_MAX_TREE) ? 1 : 0;
@@ -35,8 +51,8 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     s_tok[tid] = (tk < 0 || tk >= V) ? 0 : tk;
   }
   __syncthreads();
-  const int t = blockIdx.x;
-  if (t == 0 && tid < SS_MAX_TREE) {
+  const int t = blockIdx.x, part = blockIdx.y;
+  if (t == 0 && part == 0 && tid < SS_MAX_TREE) {
     if (tid < T) {
       unsigned long long anc = 0;
       int dep = -1;
@@ -64,43 +80,50 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
       st->epoch = e;
     }
   }
-  if (t >= T) {  // padded token slot: zero its activation column
-    for (int k = 2 * tid; k < h; k += 512) *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = 0u;
+  const int nv = h / 4;  // 4-element vectors per row
+  if (t >= T) {          // padded token slot: zero its activation column
+    for (int f = tid; f < nv; f += 256)
+      if ((f % kNormSplit) == part) {
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f, NT)) = 0u;
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f + 2, NT)) = 0u;
+      }
     return;
   }
-  const uint16_t* e = E + (size_t)s_tok[t] * h;
-  float* xr = x + (size_t)t * h;
+  const uint2* e = reinterpret_cast<const uint2*>(E + (size_t)s_tok[t] * h);
+  float4 v[kMaxVec];
   float ss = 0.f;
-  for (int k = 2 * tid; k < h; k += 512) {
-    uint32_t w = *reinterpret_cast<const uint32_t*>(e + k);
-    float a = bf16_lo(w), b = bf16_hi(w);
-    xr[k] = a;
-    xr[k + 1] = b;
-    ss += a * a + b * b;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    int f = tid + 256 * i;
+    if (f < nv) {
+      uint2 w = e[f];
+      v[i] = make_float4(bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y));
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
   }
-  ss = warp_sum(ss);
-  if ((tid & 31) == 0) s_red[tid >> 5] = ss;
-  __syncthreads();
-  if (tid < 32) {
-    float v = tid < 8 ? s_red[tid] : 0.f;
-    v = warp_sum(v);
-    if (tid == 0) s_red[0] = v;
-  }
-  __syncthreads();
-  const float r = rsqrtf(s_red[0] / (float)h + eps);
-  for (int k = 2 * tid; k < h; k += 512) {
-    uint32_t gw = *reinterpret_cast<const uint32_t*>(gain + k);
-    float a = xr[k] * r * bf16_lo(gw), b = xr[k + 1] * r * bf16_hi(gw);
-    *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = pack_half2(a, b);
+  ss = block_sum_256(ss, s_red);
+  const float r = rsqrtf(ss / (float)h + eps);
+  float4* xr = reinterpret_cast<float4*>(x + (size_t)t * h);
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    int f = tid + 256 * i;
+    if (f < nv && (f % kNormSplit) == part) {
+      xr[f] = v[i];
+      uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f, NT)) =
+          pack_half2(v[i].x * r * bf16_lo(gw.x), v[i].y * r * bf16_hi(gw.x));
+      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f + 2, NT)) =
+          pack_half2(v[i].z * r * bf16_lo(gw.y), v[i].w * r * bf16_hi(gw.y));
+    }
   }
 }
 
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
                        cudaStream_t st) {
   const uint16_t* g0 = s->layers[0].attn_norm;
-  embed_meta_kernel<<<8 * NT, 256, 0, st>>>(s->dstate, tokens, parents, T, s->embed, s->cfg.vocab,
-                                            s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
-                                            2 * s->cfg.n_layers + 2);
+  launch_pdl(embed_meta_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, s->dstate, tokens, parents, T,
+             (const uint16_t*)s->embed, s->cfg.vocab, s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
+             2 * s->cfg.n_layers + 2);
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -118,45 +141,49 @@ __global__ void __launch_bounds__(256) prep_norm_kernel(const DevState* st, cons
                                                         const uint16_t* gain, uint8_t* act, int NT, float eps,
                                                         int split) {
   __shared__ float s_red[8];
-  const int t = blockIdx.x, tid = threadIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  const int t = blockIdx.x, part = blockIdx.y, tid = threadIdx.x;
   if (t >= st->T) return;
-  const float* xr = x + (size_t)t * h;
+  const int nv = h / 4;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)t * h);
+  float4 v[kMaxVec];
   float ss = 0.f;
-  for (int k = 4 * tid; k < h; k += 1024) {
-    float4 v = *reinterpret_cast<const float4*>(xr + k);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    int f = tid + 256 * i;
+    if (f < nv) {
+      v[i] = __ldcg(xr + f);
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
   }
-  ss = warp_sum(ss);
-  if ((tid & 31) == 0) s_red[tid >> 5] = ss;
-  __syncthreads();
-  if (tid < 32) {
-    float v = tid < 8 ? s_red[tid] : 0.f;
-    v = warp_sum(v);
-    if (tid == 0) s_red[0] = v;
-  }
-  __syncthreads();
-  const float r = rsqrtf(s_red[0] / (float)h + eps);
-  for (int k = 4 * tid; k < h; k += 1024) {
-    float4 v = *reinterpret_cast<const float4*>(xr + k);
-    uint2 gw = *reinterpret_cast<const uint2*>(gain + k);
-    float a0 = v.x * r * bf16_lo(gw.x), a1 = v.y * r * bf16_hi(gw.x);
-    float a2 = v.z * r * bf16_lo(gw.y), a3 = v.w * r * bf16_hi(gw.y);
-    if (!split) {
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = pack_half2(a0, a1);
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, NT)) = pack_half2(a2, a3);
-    } else {
-      // 2*NT n-tiles: token t in tile t/8 (hi) and NT + t/8 (lo)
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, 2 * NT)) = split_pack(a0, a1, 0);
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, 2 * NT)) = split_pack(a2, a3, 0);
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k, 2 * NT)) = split_pack(a0, a1, 1);
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k + 2, 2 * NT)) = split_pack(a2, a3, 1);
+  ss = block_sum_256(ss, s_red);
+  const float r = rsqrtf(ss / (float)h + eps);
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    int f = tid + 256 * i;
+    if (f < nv && (f % kNormSplit) == part) {
+      const int k = 4 * f;
+      uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
+      float a0 = v[i].x * r * bf16_lo(gw.x), a1 = v[i].y * r * bf16_hi(gw.x);
+      float a2 = v[i].z * r * bf16_lo(gw.y), a3 = v[i].w * r * bf16_hi(gw.y);
+      if (!split) {
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = pack_half2(a0, a1);
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, NT)) = pack_half2(a2, a3);
+      } else {
+        // 2*NT n-tiles: token t in tile t/8 (hi) and NT + t/8 (lo)
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, 2 * NT)) = split_pack(a0, a1, 0);
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, 2 * NT)) = split_pack(a2, a3, 0);
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k, 2 * NT)) = split_pack(a0, a1, 1);
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k + 2, 2 * NT)) = split_pack(a2, a3, 1);
+      }
     }
   }
 }
 
 void launch_prep_norm(ss_shard* s, const uint16_t* gain, int NT, int split, cudaStream_t st) {
-  prep_norm_kernel<<<8 * NT, 256, 0, st>>>(s->dstate, s->x, s->cfg.hidden, gain, split ? s->act_lm : s->act_h, NT,
-                                           s->cfg.rms_eps, split);
+  launch_pdl(prep_norm_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, (const DevState*)s->dstate,
+             (const float*)s->x, s->cfg.hidden, gain, split ? s->act_lm : s->act_h, NT, s->cfg.rms_eps, split);
 }
 
 // ---------------------------------------------------------------- a12 commit
@@ -167,6 +194,8 @@ void launch_prep_norm(ss_shard* s, const uint16_t* gain, int NT, int split, cuda
 // advances L by n (root + accepted, never the bonus: R9).
 __global__ void __launch_bounds__(256) commit_kernel(DevState* st, uint16_t* kc, uint16_t* vc, int Hkv_l, int d,
                                                      int max_ctx_pad, int from_result) {
+  pdl_wait();
+  pdl_trigger();
   const int kvh = blockIdx.x, layer = blockIdx.y;
   int n;
   const int* chain;
@@ -206,9 +235,9 @@ __global__ void __launch_bounds__(256) commit_kernel(DevState* st, uint16_t* kc,
       *reinterpret_cast<uint4*>(vc + off) = buf[1][i];
     }
   }
+  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     int old = atomicAdd(&st->commit_done, 1);
     if (old == (int)(gridDim.x * gridDim.y) - 1) {
       st->commit_done = 0;
@@ -220,8 +249,8 @@ __global__ void __launch_bounds__(256) commit_kernel(DevState* st, uint16_t* kc,
 
 void launch_commit(ss_shard* s, int from_result, cudaStream_t st) {
   dim3 grid(s->Hkv_l, s->cfg.n_layers);
-  commit_kernel<<<grid, 256, 0, st>>>(s->dstate, s->kcache, s->vcache, s->Hkv_l, s->cfg.head_dim,
-                                      s->max_ctx_pad, from_result);
+  launch_pdl(commit_kernel, grid, dim3(256), 0, st, s->dstate, s->kcache, s->vcache, s->Hkv_l, s->cfg.head_dim,
+             s->max_ctx_pad, from_result);
 }
 
 // ---------------------------------------------------------------- RoPE table

@@ -192,6 +192,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   if (c.hidden % kW4KS) FAIL(SS_EINVAL, "hidden must be a multiple of 256");
   if ((c.n_heads / tp_size * c.head_dim) % kW4KS) FAIL(SS_EINVAL, "n_heads*head_dim/tp must be a multiple of 256");
   if ((c.intermediate / tp_size) % kW4KS) FAIL(SS_EINVAL, "intermediate/tp must be a multiple of 256");
+  if (c.hidden > 8192) FAIL(SS_EINVAL, "hidden must be <= 8192");
   if (c.max_tree < 1 || c.max_tree > SS_MAX_TREE) FAIL(SS_EINVAL, "max_tree must be in [1, 64]");
   if (c.max_ctx < c.max_tree) FAIL(SS_EINVAL, "max_ctx too small");
   int G = c.n_heads / c.n_kv_heads;
@@ -262,7 +263,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   A(s->act_o, (size_t)s->Hq_l * d * 128);
   A(s->act_d, (size_t)s->I_l * 128);
   A(s->act_lm, (size_t)h * 256);
-  A(s->qbuf, (size_t)s->Hkv_l * G * SS_MAX_TREE * d * 2);
+  A(s->qbuf, (size_t)2 * s->Hkv_l * G * SS_MAX_TREE * d * 2);  // bf16 hi + lo planes
   A(s->attn_ws, (size_t)s->Hkv_l * 2 * 64 * 256 * d * 4);
   A(s->attn_ml, (size_t)s->Hkv_l * 2 * 64 * 256 * 2 * 4);
   A(s->attn_bar, (size_t)s->Hkv_l * 2 * 2 * 4);

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libswiftspec.so")
+LIB_PATH = os.path.join(HERE, "lib", os.environ.get("SWIFTSPEC_LIB", "libswiftspec.so"))
 
 SS_MAX_TREE = 64
 STATUS = {0: "SS_OK", -1: "SS_EINVAL", -2: "SS_ECAPACITY", -3: "SS_ECONSISTENCY", -4: "SS_ECUDA",

@@ -117,7 +117,7 @@ typedef enum {
 
 /* Create the shard of TP rank tp_rank (0 <= tp_rank < tp_size, tp_size in
  * {1,2,4,8}) on CUDA device `device`: allocates weights, the KV cache
- * [n_layers][n_kv_heads/tp][max_ctx][head_dim] (bf16), workspaces and the
+ * [n_layers][n_kv_heads/tp][max_ctx][head_dim] (fp16), workspaces and the
  * peer receive buffers.  *out receives the handle (owned by the caller, free
  * with ss_destroy).  Errors: SS_EINVAL (shape rules above), SS_ECUDA. */
 ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
@@ -159,13 +159,16 @@ ss_status ss_synth_weights(ss_shard* s, uint64_t seed);
 
 /* Committed prefix rows [0, len) of one layer: k, v host uint16 bf16 bits
  * [len][n_kv_heads][head_dim] (FULL heads; the shard keeps its own).  Keys are
- * post-RoPE as cached.  Sets L = len when called for the last layer. */
+ * post-RoPE as cached.  Stored as fp16 (SS_EINVAL if a value exceeds the fp16
+ * range).  Sets L = len when called for the last layer. */
 ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k, const void* v, int32_t len);
 /* Device-side synthetic prefix for all layers (synth.gen_prefix_kv), L = len. */
 ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len);
-/* Read committed rows [row0, row0+n) of layer `layer` back to host, full-head
- * canonical layout of this shard's heads: [n][n_kv_heads/tp][head_dim] bf16. */
-ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, void* k_out, void* v_out);
+/* Read cache rows [row0, row0+n) of layer `layer` back to host as float32,
+ * layout [n][n_kv_heads/tp][head_dim] (this shard's heads).  The cache stores
+ * K/V as fp16 (exact for the bf16 prefix inputs).
+ * Synchronises the device. */
+ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, float* k_out, float* v_out);
 /* Set the committed length (truncate; cannot grow beyond rows ever written). */
 ss_status ss_set_committed_len(ss_shard* s, int32_t L);
 /* Committed length L (synchronises with the device if the last commit was

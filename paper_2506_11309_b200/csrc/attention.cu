@@ -1,41 +1,62 @@
 // attention.cu -- tree-masked GQA attention.
 //
 // Every tree node attends to the committed prefix [0, L) plus its
-// ancestors-or-self among the tree rows [L, L+T) (square mask P:321, bitmask
-// per node).  One CTA = (kv head, key split, row chunk); the rows are the
-// G query heads x T nodes that share the kv head (GQA), so K/V tiles are
-// read from HBM once per kv head.  K/V tiles (64 keys, pre-swizzled in the
-// cache layout) arrive via the TMA bulk engine into a double-buffered ring;
-// QK^T and PV run on mma.sync with ldmatrix; online softmax in fp32 (R11).
-// The split partials are combined inside the same kernel: CTAs of one kv head
-// meet at a flag counter (the paper's intra-GPU LL aggregation, "without
-// explicit synchronization across thread blocks or extra kernel launches")
-// and each CTA then merges a slice of the rows, writing the bf16 result
-// straight into the O-projection's fragment-ordered input.
+// ancestors-or-self among the tree rows [L, L+T) (square mask P:321, one
+// ancestor bitmask per node).  One CTA = (kv head, key split, row chunk).
+// The rows are the G query heads x T nodes that share the kv head (GQA), so
+// each K/V tile is read from HBM once per kv head.  Warps are laid out as
+// (16-row block) x (key slice of every 64-key tile), so a CTA keeps 8 warps
+// busy even for the 64 rows of a T=8 tree.  K/V tiles (pre-swizzled in the
+// cache layout) arrive through the TMA bulk engine into a double-buffered
+// ring; prefix tiles are requested before the PDL wait because they do not
+// depend on the QKV kernel.  QK^T and PV run on mma.sync (fp16, fp32
+// accumulate); online softmax in fp32 (R11).
+//
+// The split partials are merged inside the same kernel ("the
+// threadblocks aggregate the sum ... without explicit synchronization across
+// thread blocks or extra kernel launches"): the CTAs of one kv head meet at a
+// flag counter and each then merges a slice of the rows by log-sum-exp,
+// writing fp16 straight into the O-projection's fragment-ordered input.
 #include "common.cuh"
 #include "internal.h"
 #include "kernels.h"
 
 namespace ss {
 
-template <int D, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
+template <int D, int RB>
+struct AttnCfg {
+  static constexpr int KS = (8 / RB) < 1 ? 1 : ((8 / RB) > 4 ? 4 : (8 / RB));  // key slices
+  static constexpr int WARPS = RB * KS;
+  static constexpr int ROWS = RB * 16;
+  static constexpr int KEYS = kKvTile / KS;   // keys per warp per tile (64, 32 or 16)
+  static constexpr int NTK = KEYS / 8;        // score n-tiles per warp
+  static constexpr int TILE_ELEMS = kKvTile * D;
+  static constexpr int NBUF = 4;              // K/V tiles in flight (a CTA's whole range at L=4K)
+  static constexpr size_t SMEM = (size_t)ROWS * D * 2 + 2 * NBUF * (size_t)TILE_ELEMS * 2;
+};
+
+template <int D, int RB>
+__global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(AttnArgs a) {
+  using C = AttnCfg<D, RB>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[2];
-  constexpr int ROWS = NW * 16;
-  constexpr int QS = D + 8;  // padded Q row stride (elements)
-  constexpr int TILE_ELEMS = kKvTile * D;
-  uint16_t* Qs = reinterpret_cast<uint16_t*>(smem);
-  uint16_t* Ks = Qs + 2 * ROWS * QS;  // [2][64*D] after the Q hi / lo planes
-  uint16_t* Vs = Ks + 2 * TILE_ELEMS;
+  constexpr int NBUF = C::NBUF;
+  __shared__ __align__(8) uint64_t full[NBUF];
+  __shared__ __align__(8) uint64_t qbar;
+  constexpr int ROWS = C::ROWS, TILE_ELEMS = C::TILE_ELEMS, NTHR = C::WARPS * 32;
+  uint16_t* Qs = reinterpret_cast<uint16_t*>(smem);  // [ROWS][D] fp16, swizzled
+  uint16_t* Ks = Qs + ROWS * D;                      // [NBUF][64][D]
+  uint16_t* Vs = Ks + NBUF * TILE_ELEMS;
 
   const int split = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
   const int S = gridDim.x, Z = gridDim.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = warp % RB, ks = warp / RB;
   const int gq = lane >> 2, tq = lane & 3;
   DevState* st = a.st;
-  pdl_wait();
-  pdl_trigger();
+  // L (committed by an earlier step) and T (written by this step's ingest
+  // kernel, which completed before the QKV kernel could trigger our launch)
+  // are stable here; only the tree rows [L, L+T) and q come from the QKV
+  // kernel this launch depends on.
   const int L = st->L, T = st->T;
   const int G = a.G;
   const int Mrows = G * T;
@@ -45,39 +66,46 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
   const size_t head_base = ((size_t)a.layer * a.Hkv_l + kvh) * a.max_ctx_pad * D;
 
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int i = 0; i < NBUF; ++i) mbar_init(&full[i], 1);
+    mbar_init(&qbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0 && t0 < t1) {
-    mbar_expect_tx(&full[0], 2 * TILE_ELEMS * 2);
-    bulk_g2s_nohint(Ks, a.kc + head_base + (size_t)t0 * TILE_ELEMS, TILE_ELEMS * 2, &full[0]);
-    bulk_g2s_nohint(Vs, a.vc + head_base + (size_t)t0 * TILE_ELEMS, TILE_ELEMS * 2, &full[0]);
-  }
-  // Q rows [m0, m0 + ROWS) of this kv head (post-RoPE, from the QKV epilogue),
-  // as bf16 hi and lo planes: q = hi + lo carries ~16 mantissa bits, so the
-  // QK^T product is not limited by a bf16 rounding of q.
-  const uint16_t* qsrc = a.qbuf + ((size_t)kvh * (G * SS_MAX_TREE) + m0) * D;
-  const size_t qplane = (size_t)a.Hkv_l * G * SS_MAX_TREE * D;
-  for (int i = threadIdx.x; i < ROWS * (D / 8); i += NW * 32) {
-    int r = i / (D / 8), c = i % (D / 8);
-    uint4 v = make_uint4(0, 0, 0, 0), w = make_uint4(0, 0, 0, 0);
-    if (m0 + r < Mrows) {
-      v = *reinterpret_cast<const uint4*>(qsrc + (size_t)r * D + c * 8);
-      w = *reinterpret_cast<const uint4*>(qsrc + qplane + (size_t)r * D + c * 8);
+  int issued = 0;
+  if (threadIdx.x == 0) {  // prefix tiles: independent of the QKV kernel
+    for (int i = 0; i < NBUF && t0 + i < t1; ++i) {
+      const int tile = t0 + i;
+      if ((tile + 1) * kKvTile > L) break;
+      mbar_expect_tx(&full[i], 2 * TILE_ELEMS * 2);
+      bulk_g2s_nohint(Ks + i * TILE_ELEMS, a.kc + head_base + (size_t)tile * TILE_ELEMS, TILE_ELEMS * 2, &full[i]);
+      bulk_g2s_nohint(Vs + i * TILE_ELEMS, a.vc + head_base + (size_t)tile * TILE_ELEMS, TILE_ELEMS * 2, &full[i]);
+      ++issued;
     }
-    *reinterpret_cast<uint4*>(Qs + r * QS + c * 8) = v;
-    *reinterpret_cast<uint4*>(Qs + (ROWS + r) * QS + c * 8) = w;
   }
-  __syncthreads();
-  const uint16_t* qrow = Qs + (warp * 16 + (lane & 15)) * QS + (lane >> 4) * 8;
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    for (int i = issued; i < NBUF && t0 + i < t1; ++i) {
+      const int tile = t0 + i;
+      mbar_expect_tx(&full[i], 2 * TILE_ELEMS * 2);
+      bulk_g2s_nohint(Ks + i * TILE_ELEMS, a.kc + head_base + (size_t)tile * TILE_ELEMS, TILE_ELEMS * 2, &full[i]);
+      bulk_g2s_nohint(Vs + i * TILE_ELEMS, a.vc + head_base + (size_t)tile * TILE_ELEMS, TILE_ELEMS * 2, &full[i]);
+    }
+    // q rows [m0, m0 + ROWS) of this kv head (fp16, swizzled by the QKV
+    // epilogue).  Rows >= G*T are stale but finite and masked below.
+    mbar_expect_tx(&qbar, ROWS * D * 2);
+    bulk_g2s_nohint(Qs, a.qbuf + ((size_t)kvh * (G * SS_MAX_TREE) + m0) * D, ROWS * D * 2, &qbar);
+  }
+  mbar_wait(&qbar, 0);
+  const int qr = rb * 16 + (lane & 15);
+  const uint16_t* qrow = Qs + qr * D;
 
-  const int rowA = m0 + warp * 16 + gq, rowB = rowA + 8;
+  const int rowA = m0 + rb * 16 + gq, rowB = rowA + 8;
   const int tokA = min(rowA / G, SS_MAX_TREE - 1), tokB = min(rowB / G, SS_MAX_TREE - 1);
   const unsigned long long ancA = st->anc[tokA], ancB = st->anc[tokB];
   const bool okA = rowA < Mrows, okB = rowB < Mrows;
   const float sl2 = rsqrtf((float)D) * 1.4426950408889634f;
+  const int kofs = ks * C::KEYS;  // this warp's key slice inside each tile
 
   float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
   float o[D / 8][4];
@@ -85,52 +113,41 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
   for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
 
   for (int it = t0; it < t1; ++it) {
-    const int b = (it - t0) & 1;
-    const uint32_t phase = ((it - t0) >> 1) & 1;
-    if (threadIdx.x == 0 && it + 1 < t1) {
-      fence_proxy_async_smem();  // ldmatrix reads of this buffer (previous tile) before the TMA overwrite
-      mbar_expect_tx(&full[b ^ 1], 2 * TILE_ELEMS * 2);
-      bulk_g2s_nohint(Ks + (b ^ 1) * TILE_ELEMS, a.kc + head_base + (size_t)(it + 1) * TILE_ELEMS, TILE_ELEMS * 2,
-                      &full[b ^ 1]);
-      bulk_g2s_nohint(Vs + (b ^ 1) * TILE_ELEMS, a.vc + head_base + (size_t)(it + 1) * TILE_ELEMS, TILE_ELEMS * 2,
-                      &full[b ^ 1]);
-    }
+    const int b = (it - t0) % NBUF;
+    const uint32_t phase = ((it - t0) / NBUF) & 1;
     mbar_wait(&full[b], phase);
     const uint16_t* Kt = Ks + b * TILE_ELEMS;
     const uint16_t* Vt = Vs + b * TILE_ELEMS;
 
-    float sc[8][4];
+    float sc[C::NTK][4];
 #pragma unroll
-    for (int n = 0; n < 8; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+    for (int n = 0; n < C::NTK; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
-      uint32_t qh[4], ql[4];
-      ldmatrix_x4(qh, qrow + kk * 16);
-      ldmatrix_x4(ql, qrow + ROWS * QS + kk * 16);
+      uint32_t qa[4];
+      ldmatrix_x4(qa, qrow + (((kk * 2 + (lane >> 4)) ^ (qr & 7)) << 3));
 #pragma unroll
-      for (int np = 0; np < 4; ++np) {
-        const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+      for (int np = 0; np < C::NTK / 2; ++np) {
+        const int key = kofs + np * 16 + (lane & 7) + ((lane >> 4) << 3);
         const int ch = kk * 2 + ((lane >> 3) & 1);
         uint32_t kb[4];
         ldmatrix_x4(kb, Kt + key * D + ((ch ^ (key & 7)) << 3));
-        mma_bf16_16816(sc[2 * np], qh, kb[0], kb[1]);
-        mma_bf16_16816(sc[2 * np + 1], qh, kb[2], kb[3]);
-        mma_bf16_16816(sc[2 * np], ql, kb[0], kb[1]);
-        mma_bf16_16816(sc[2 * np + 1], ql, kb[2], kb[3]);
+        mma_f16_16816(sc[2 * np], qa, kb[0], kb[1]);
+        mma_f16_16816(sc[2 * np + 1], qa, kb[2], kb[3]);
       }
     }
-    // mask (prefix always visible; tree rows by ancestor bit; beyond L+T never)
-    const int kbase = it * kKvTile;
+    // mask: prefix always visible; tree rows by ancestor bit; beyond L+T never
+    const int kbase = it * kKvTile + kofs;
     float mxA = -INFINITY, mxB = -INFINITY;
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
+    for (int n = 0; n < C::NTK; ++n) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int key = kbase + n * 8 + 2 * tq + (e & 1);
         const unsigned long long anc = (e < 2) ? ancA : ancB;
         const bool ok = (e < 2) ? okA : okB;
-        bool vis = ok && (key < L || (key < L + T && ((anc >> (key - L)) & 1ull)));
-        float v = vis ? sc[n][e] * sl2 : -INFINITY;
+        const bool vis = ok && (key < L || (key < L + T && ((anc >> (key - L)) & 1ull)));
+        const float v = vis ? sc[n][e] * sl2 : -INFINITY;
         sc[n][e] = v;
         if (e < 2) mxA = fmaxf(mxA, v); else mxB = fmaxf(mxB, v);
       }
@@ -143,19 +160,15 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
     const float uA = (mnA == -INFINITY) ? 0.f : mnA, uB = (mnB == -INFINITY) ? 0.f : mnB;
     const float alA = exp2f(mA - uA), alB = exp2f(mB - uB);
     float sumA = 0.f, sumB = 0.f;
-    // probabilities as bf16 hi + lo (V is bf16 in the cache)
-    uint32_t pa[4][4], pl[4][4];
+    uint32_t pa[C::NTK / 2][4];
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      float p0 = exp2f(sc[n][0] - uA), p1 = exp2f(sc[n][1] - uA);
-      float p2 = exp2f(sc[n][2] - uB), p3 = exp2f(sc[n][3] - uB);
+    for (int n = 0; n < C::NTK; ++n) {
+      const float p0 = exp2f(sc[n][0] - uA), p1 = exp2f(sc[n][1] - uA);
+      const float p2 = exp2f(sc[n][2] - uB), p3 = exp2f(sc[n][3] - uB);
       sumA += p0 + p1;
       sumB += p2 + p3;
-      uint32_t h01 = pack_bf16x2(p0, p1), h23 = pack_bf16x2(p2, p3);
-      pa[n >> 1][(n & 1) * 2 + 0] = h01;
-      pa[n >> 1][(n & 1) * 2 + 1] = h23;
-      pl[n >> 1][(n & 1) * 2 + 0] = pack_bf16x2(p0 - bf16_lo(h01), p1 - bf16_hi(h01));
-      pl[n >> 1][(n & 1) * 2 + 1] = pack_bf16x2(p2 - bf16_lo(h23), p3 - bf16_hi(h23));
+      pa[n >> 1][(n & 1) * 2 + 0] = pack_half2(p0, p1);
+      pa[n >> 1][(n & 1) * 2 + 1] = pack_half2(p2, p3);
     }
     sumA += __shfl_xor_sync(0xffffffffu, sumA, 1);
     sumA += __shfl_xor_sync(0xffffffffu, sumA, 2);
@@ -170,36 +183,46 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
       o[n][0] *= alA; o[n][1] *= alA; o[n][2] *= alB; o[n][3] *= alB;
     }
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
+    for (int kk = 0; kk < C::NTK / 2; ++kk) {
 #pragma unroll
       for (int dp = 0; dp < D / 16; ++dp) {
-        const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int key = kofs + kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
         const int ch = dp * 2 + (lane >> 4);
         uint32_t vb[4];
         ldmatrix_x4_trans(vb, Vt + key * D + ((ch ^ (key & 7)) << 3));
-        mma_bf16_16816(o[2 * dp], pa[kk], vb[0], vb[1]);
-        mma_bf16_16816(o[2 * dp + 1], pa[kk], vb[2], vb[3]);
-        mma_bf16_16816(o[2 * dp], pl[kk], vb[0], vb[1]);
-        mma_bf16_16816(o[2 * dp + 1], pl[kk], vb[2], vb[3]);
+        mma_f16_16816(o[2 * dp], pa[kk], vb[0], vb[1]);
+        mma_f16_16816(o[2 * dp + 1], pa[kk], vb[2], vb[3]);
       }
     }
-    __syncthreads();  // buffer b is refilled two iterations later
+    if (it + NBUF < t1) {
+      __syncthreads();  // every warp is done with buffer b: refill it with tile it + NBUF
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();  // the ldmatrix reads above before the TMA overwrite
+        mbar_expect_tx(&full[b], 2 * TILE_ELEMS * 2);
+        bulk_g2s_nohint(Ks + b * TILE_ELEMS, a.kc + head_base + (size_t)(it + NBUF) * TILE_ELEMS, TILE_ELEMS * 2,
+                        &full[b]);
+        bulk_g2s_nohint(Vs + b * TILE_ELEMS, a.vc + head_base + (size_t)(it + NBUF) * TILE_ELEMS, TILE_ELEMS * 2,
+                        &full[b]);
+      }
+    }
   }
 
-  // ---- partials to the workspace
+  // ---- partial (split, key slice) -> workspace
   const int grp = kvh * Z + z;
-  float* ws = a.ws + (((size_t)grp * S + split) * 256) * D;
-  float* ml = a.ml + (((size_t)grp * S + split) * 256) * 2;
+  const int P = S * C::KS;  // partials per (kv head, row chunk)
+  const int pidx = split * C::KS + ks;
   {
-    const int ra = warp * 16 + gq, rb = ra + 8;
+    float* ws = a.ws + (((size_t)grp * P + pidx) * 256) * D;
+    float* ml = a.ml + (((size_t)grp * P + pidx) * 256) * 2;
+    const int ra = rb * 16 + gq, rbb = ra + 8;
 #pragma unroll
     for (int n = 0; n < D / 8; ++n) {
       *reinterpret_cast<float2*>(ws + (size_t)ra * D + n * 8 + 2 * tq) = make_float2(o[n][0], o[n][1]);
-      *reinterpret_cast<float2*>(ws + (size_t)rb * D + n * 8 + 2 * tq) = make_float2(o[n][2], o[n][3]);
+      *reinterpret_cast<float2*>(ws + (size_t)rbb * D + n * 8 + 2 * tq) = make_float2(o[n][2], o[n][3]);
     }
     if (tq == 0) {
       *reinterpret_cast<float2*>(ml + ra * 2) = make_float2(mA, lA);
-      *reinterpret_cast<float2*>(ml + rb * 2) = make_float2(mB, lB);
+      *reinterpret_cast<float2*>(ml + rbb * 2) = make_float2(mB, lB);
     }
   }
   // ---- meet the other splits of this (kv head, row chunk): every thread
@@ -214,52 +237,52 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
   }
   __syncthreads();
   __threadfence();
-  // ---- merge a slice of the rows across the S splits (log-sum-exp, R11).
+  // ---- merge a slice of the rows across the P partials (log-sum-exp, R11).
   // Items = (row, 4-float chunk); the CTA's items are a contiguous slice.  The
-  // per-(row, split) weights exp2(m_s - m*) / l* go through shared memory, and
-  // every thread issues its S partial loads back to back (no serial L2 chain).
+  // per-(row, partial) weights exp2(m_p - m*) / l* go through shared memory and
+  // every thread issues its P loads back to back (no serial L2 chain).
   {
-    float* s_w = reinterpret_cast<float*>(Ks);  // reuse the K/V ring: [rows_here][S]
+    float* s_w = reinterpret_cast<float*>(Ks);  // reuse the K/V ring: [rows_here][P] x 2
     const int n_items = ROWS * (D / 4);
     const int i_lo = (int)((long)split * n_items / S), i_hi = (int)((long)(split + 1) * n_items / S);
     const int r_first = i_lo / (D / 4), r_last = (i_hi - 1) / (D / 4);
     const int nr = (i_hi > i_lo) ? r_last - r_first + 1 : 0;
-    const float* wsg = a.ws + ((size_t)grp * S * 256) * D;
-    const float* mlg = a.ml + ((size_t)grp * S * 256) * 2;
-    for (int i = threadIdx.x; i < nr * S; i += NW * 32) {
-      int rr = i / S, s2 = i % S;
-      float2 v = __ldcg(reinterpret_cast<const float2*>(mlg + ((size_t)s2 * 256 + r_first + rr) * 2));
+    const float* wsg = a.ws + ((size_t)grp * P * 256) * D;
+    const float* mlg = a.ml + ((size_t)grp * P * 256) * 2;
+    for (int i = threadIdx.x; i < nr * P; i += NTHR) {
+      const int rr = i / P, p2 = i % P;
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(mlg + ((size_t)p2 * 256 + r_first + rr) * 2));
       s_w[i] = v.x;
-      s_w[nr * S + i] = v.y;
+      s_w[nr * P + i] = v.y;
     }
     __syncthreads();
-    for (int rr = warp; rr < nr; rr += NW) {  // one warp per row: m*, l*, weights
+    for (int rr = warp; rr < nr; rr += C::WARPS) {  // one warp per row: m*, l*, weights
       float mx = -INFINITY;
-      for (int s2 = lane; s2 < S; s2 += 32) mx = fmaxf(mx, s_w[rr * S + s2]);
+      for (int p2 = lane; p2 < P; p2 += 32) mx = fmaxf(mx, s_w[rr * P + p2]);
       mx = warp_max(mx);
       float l = 0.f;
-      for (int s2 = lane; s2 < S; s2 += 32) {
-        float ms = s_w[rr * S + s2];
-        float w = (ms == -INFINITY) ? 0.f : exp2f(ms - mx);
-        l += w * s_w[nr * S + rr * S + s2];
-        s_w[rr * S + s2] = w;
+      for (int p2 = lane; p2 < P; p2 += 32) {
+        const float ms = s_w[rr * P + p2];
+        const float w = (ms == -INFINITY) ? 0.f : exp2f(ms - mx);
+        l += w * s_w[nr * P + rr * P + p2];
+        s_w[rr * P + p2] = w;
       }
       l = warp_sum(l);
       __syncwarp();
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      for (int s2 = lane; s2 < S; s2 += 32) s_w[rr * S + s2] *= inv;
+      for (int p2 = lane; p2 < P; p2 += 32) s_w[rr * P + p2] *= inv;
     }
     __syncthreads();
-    for (int it = i_lo + threadIdx.x; it < i_hi; it += NW * 32) {
-      const int r = it / (D / 4), c4 = it % (D / 4);
+    for (int itm = i_lo + threadIdx.x; itm < i_hi; itm += NTHR) {
+      const int r = itm / (D / 4), c4 = itm % (D / 4);
       const int m = m0 + r;
       if (m >= Mrows) continue;
-      const float* wr = s_w + (r - r_first) * S;
+      const float* wr = s_w + (r - r_first) * P;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-      for (int s2 = 0; s2 < S; ++s2) {
-        const float w = wr[s2];
-        const float4 ov = __ldcg(reinterpret_cast<const float4*>(wsg + ((size_t)s2 * 256 + r) * D + 4 * c4));
+      for (int p2 = 0; p2 < P; ++p2) {
+        const float w = wr[p2];
+        const float4 ov = __ldcg(reinterpret_cast<const float4*>(wsg + ((size_t)p2 * 256 + r) * D + 4 * c4));
         acc.x += w * ov.x;
         acc.y += w * ov.y;
         acc.z += w * ov.z;
@@ -267,8 +290,11 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
       }
       const int t = m / G, hq = kvh * G + (m % G);
       const int k = hq * D + 4 * c4;
-      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k, a.NT)) = pack_half2(acc.x, acc.y);
-      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k + 2, a.NT)) = pack_half2(acc.z, acc.w);
+      const uint32_t p01 = pack_half2(acc.x, acc.y), p23 = pack_half2(acc.z, acc.w);
+      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k, a.NT)) = p01;
+      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k + 2, a.NT)) = p23;
+      // group sum X of the O-projection input (slots zeroed by the QKV kernel)
+      atomicAdd(reinterpret_cast<float*>(a.act_out + act_xsum_offset(t, k >> 7, a.NT)), half2_sum(p01) + half2_sum(p23));
     }
   }
   __syncthreads();
@@ -281,66 +307,54 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_kernel(AttnArgs a) {
   }
 }
 
-template <int D, int NW>
-static size_t attn_smem() {
-  return 2 * (size_t)NW * 16 * (D + 8) * 2 + 4 * (size_t)kKvTile * D * 2;
-}
-
-template <int D, int NW>
+template <int D, int RB>
 static int occ_of() {
   static int occ = -1;
+  using C = AttnCfg<D, RB>;
   if (occ < 0) {
-    cudaFuncSetAttribute(attn_kernel<D, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem<D, NW>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_kernel<D, NW>, NW * 32, attn_smem<D, NW>());
+    cudaFuncSetAttribute(attn_kernel<D, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_kernel<D, RB>, C::WARPS * 32, C::SMEM);
     if (occ < 1) occ = 1;
   }
   return occ;
 }
 
-static int nw_for(int G, int NT) {
+static int rb_for(int G, int NT) {
   int rb = (G * NT * 8 + 15) / 16;
-  int nw = 1;
-  while (nw < rb && nw < 16) nw <<= 1;
-  return nw;
+  int r = 1;
+  while (r < rb && r < 16) r <<= 1;
+  return r;
 }
 
-template <int D>
-static int occ_dispatch(int nw) {
-  switch (nw) {
-    case 1: return occ_of<D, 1>();
-    case 2: return occ_of<D, 2>();
-    case 4: return occ_of<D, 4>();
-    case 8: return occ_of<D, 8>();
-    default: return occ_of<D, 16>();
-  }
-}
-
-template <int D>
-static int launch_d(const AttnArgs& a0, int max_ctas, cudaStream_t st) {
-  AttnArgs a = a0;
-  int nw = nw_for(a.G, a.NT);
-  int rows = a.G * a.NT * 8;
-  int Z = (rows + nw * 16 - 1) / (nw * 16);
+template <int D, int RB>
+static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
+  using C = AttnCfg<D, RB>;
+  const int rows = a.G * a.NT * 8;
+  const int Z = (rows + C::ROWS - 1) / C::ROWS;
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-  int cap = n_sm * occ_dispatch<D>(nw);
+  int cap = n_sm * occ_of<D, RB>();
   if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
   int S = cap / (a.Hkv_l * Z);
-  int max_tiles = (a.max_ctx_pad + kKvTile - 1) / kKvTile;
+  const int max_tiles = (a.max_ctx_pad + kKvTile - 1) / kKvTile;
   if (S > max_tiles) S = max_tiles;
-  if (S > 64) S = 64;
+  if (S * C::KS > 64) S = 64 / C::KS;  // workspace holds 64 partials per row chunk
   if (S < 1) S = 1;
   a.splits = S;
   a.zchunks = Z;
-  dim3 grid(S, a.Hkv_l, Z);
-  switch (nw) {
-    case 1: launch_pdl(attn_kernel<D, 1>, grid, dim3(32), attn_smem<D, 1>(), st, a); break;
-    case 2: launch_pdl(attn_kernel<D, 2>, grid, dim3(64), attn_smem<D, 2>(), st, a); break;
-    case 4: launch_pdl(attn_kernel<D, 4>, grid, dim3(128), attn_smem<D, 4>(), st, a); break;
-    case 8: launch_pdl(attn_kernel<D, 8>, grid, dim3(256), attn_smem<D, 8>(), st, a); break;
-    default: launch_pdl(attn_kernel<D, 16>, grid, dim3(512), attn_smem<D, 16>(), st, a); break;
-  }
+  launch_pdl(attn_kernel<D, RB>, dim3(S, a.Hkv_l, Z), dim3(C::WARPS * 32), C::SMEM, st, a);
   return 1;
+}
+
+template <int D>
+static int launch_d(const AttnArgs& a, int max_ctas, cudaStream_t st) {
+  switch (rb_for(a.G, a.NT)) {
+    case 1: return launch_rb<D, 1>(a, max_ctas, st);
+    case 2: return launch_rb<D, 2>(a, max_ctas, st);
+    case 4: return launch_rb<D, 4>(a, max_ctas, st);
+    case 8: return launch_rb<D, 8>(a, max_ctas, st);
+    default: return launch_rb<D, 16>(a, max_ctas, st);
+  }
 }
 
 int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st) {

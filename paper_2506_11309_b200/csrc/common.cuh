@@ -29,18 +29,27 @@ constexpr int kBFUnitBytes = 16384;
 constexpr int kKvTile = 64;          // keys per attention tile
 
 // Activation "fragment order" (B operand of mma.m16n8k16, col layout).  W4
-// GEMM inputs are fp16 (exact integer weights (q - z) in fp16, DESIGN.md
-// "Precision"); the LM-head input is split bf16 hi/lo in 2*NT n-tiles.
-// Element (token tt, k) of a [T][K] activation lives at
-//   (((k/32 * NT + tt/8) * 32 + lane) * 16 + ((k/16)%2) * 8 + word * 4 + half * 2  bytes,
+// GEMM inputs are fp16; the LM-head input is split bf16 hi/lo in 2*NT n-tiles.
+// Inside one 32-deep k block, element (token tt, k) sits at
+//   ((k/32 * NT + tt/8) * 32 + lane) * 16 + ((k/16)%2) * 8 + word * 4 + half * 2  bytes,
 //   lane = (tt%8)*4 + ((k%16)%8)/2, word = (k%16)/8, half = k%2,
 // so one LDS.128 per lane yields the B fragments of two consecutive k16 steps.
-SS_DEV uint32_t act_frag_offset(int tt, int k, int NT) {
+SS_DEV uint32_t frag_offset(int tt, int k, int NT) {
   int kk = k & 15;
   int lane = ((tt & 7) << 2) | ((kk & 7) >> 1);
   int word = kk >> 3;
   return ((uint32_t)(((k >> 5) * NT + (tt >> 3)) * 32 + lane) << 4) + (((k >> 4) & 1) << 3) + (word << 2) +
          ((k & 1) << 1);
+}
+// W4 GEMM input: one chunk per 256-deep K stage = the fp16 fragments (NT*4 KB)
+// followed by X[2 groups][8*NT] fp32, the per-(128-group, token) sums of the
+// fp16 values (the zero-point correction of gemm.cu).
+SS_DEV constexpr uint32_t w4_act_stage_bytes(int NT) { return (uint32_t)NT * 4096u + (uint32_t)NT * 64u; }
+SS_DEV uint32_t act_frag_offset(int tt, int k, int NT) {
+  return (uint32_t)(k >> 8) * w4_act_stage_bytes(NT) + frag_offset(tt, k & 255, NT);
+}
+SS_DEV uint32_t act_xsum_offset(int tt, int g, int NT) {
+  return (uint32_t)(g >> 1) * w4_act_stage_bytes(NT) + (uint32_t)NT * 4096u + (uint32_t)(((g & 1) * 8 * NT + tt) * 4);
 }
 
 // Swizzled KV cache row layout: 64-row blocks, 16-byte chunk index XORed
@@ -106,6 +115,10 @@ SS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::
 // Order this thread's (and, after a barrier, the CTA's) generic-proxy shared
 // memory accesses before subsequent async-proxy (TMA / bulk copy) accesses.
 SS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Release/acquire fence at GPU scope (lighter than __threadfence's fence.sc,
+// which also invalidates L1).
+SS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 SS_DEV void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -183,6 +196,16 @@ SS_DEV float bf16_bits_to_f32(uint16_t b) { return __uint_as_float(((uint32_t)b)
 SS_DEV uint16_t f32_to_bf16_bits(float f) {
   __nv_bfloat16 h = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&h);
+}
+
+SS_DEV uint16_t f32_to_f16_bits(float f) {
+  __half h = __float2half_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+
+SS_DEV float half2_sum(uint32_t p) {
+  const __half2 h = *reinterpret_cast<const __half2*>(&p);
+  return __low2float(h) + __high2float(h);
 }
 
 SS_DEV float warp_sum(float v) {

@@ -29,16 +29,25 @@ struct GemmCfg {
   static constexpr int KS = WFMT == 0 ? kW4KS : kBFKS;
   static constexpr int WBYTES = WFMT == 0 ? kW4UnitBytes : kBFUnitBytes;
   static constexpr int ANT = WFMT == 0 ? NT : 2 * NT;  // LM head: bf16 hi + lo tiles
-  static constexpr int ABYTES = (KS / 16) * ANT * 256;
+  // W4: fragments + X (group sums, 2 groups x 8NT fp32); LM head: fragments only
+  static constexpr int ABYTES = (KS / 16) * ANT * 256 + (WFMT == 0 ? NT * 64 : 0);
   static constexpr int UBYTES = WBYTES + ABYTES;
   // NT <= 2: 3 stages (~63-76 KB) -> 3 CTAs / SM; larger NT: 4 stages, 1-2 CTAs / SM
+#ifdef SS_EXP_NCW
+  static constexpr int NCW = SS_EXP_NCW;
+#else
+  static constexpr int NCW = 8;  // consumer warps: one per 16-row tile (measured best at T <= 16)
+#endif
+  // ring depth: NT <= 2 -> 3 stages (~63-76 KB, 3 CTAs/SM); larger NT -> 4
 #ifdef SS_EXP_STAGES
   static constexpr int STAGES = SS_EXP_STAGES;
 #else
   static constexpr int STAGES = (UBYTES <= 26 * 1024) ? 3 : 4;
 #endif
   static constexpr int SMEM = STAGES * UBYTES + 1024;
-  static constexpr int THREADS = 288;  // 8 consumer warps + 1 producer warp
+  static constexpr int KPARTS = NCW / 8;
+  static constexpr int NACC = NT <= 2 ? 2 : 1;     // independent accumulator sets per warp
+  static constexpr int THREADS = 32 * (NCW + 1);  // + 1 producer warp
 };
 
 // ---------------------------------------------------------------- epilogues
@@ -60,12 +69,11 @@ __device__ void epi_qkv(const EpiArgs& e, int tg, const float* acc, int T) {
       float2 cs = e.rope_cs[(size_t)pos * half + (j % half)];
       v = (j < half) ? (v * cs.x - pv * cs.y) : (v * cs.x + pv * cs.y);
     }
-    uint16_t b = f32_to_bf16_bits(v);
-    if (row < nq) {  // q as bf16 hi + lo planes (attention.cu)
+    const uint16_t b = f32_to_f16_bits(v);  // q and the KV cache are fp16
+    if (row < nq) {
       int hq = row / d, kvh = hq / e.G, jj = hq - kvh * e.G;
-      size_t qi = ((size_t)kvh * (e.G * SS_MAX_TREE) + t * e.G + jj) * d + j;
-      e.qbuf[qi] = b;
-      e.qbuf[qi + (size_t)e.Hkv_l * e.G * SS_MAX_TREE * d] = f32_to_bf16_bits(v - bf16_bits_to_f32(b));
+      const int m = t * e.G + jj;  // attention row; 16-byte chunks swizzled by m % 8
+      e.qbuf[((size_t)kvh * (e.G * SS_MAX_TREE) + m) * d + ((((j >> 3) ^ (m & 7))) << 3) + (j & 7)] = b;
     } else {
       int kvh = (row < nq + nk) ? (row - nq) / d : (row - nq - nk) / d;
       uint16_t* c = (row < nq + nk) ? e.kc : e.vc;
@@ -78,17 +86,23 @@ __device__ void epi_qkv(const EpiArgs& e, int tg, const float* acc, int T) {
 template <int NT>
 __device__ void epi_swiglu(const EpiArgs& e, int tg, const float* acc, int T) {
   const int TP = NT * 8;
-  // tile-group rows: [0,64) gate, [64,128) up for intermediate columns tg*64..+64
-  for (int idx = threadIdx.x; idx < 32 * T; idx += 256) {
-    int cp = idx / T, t = idx - cp * T;
-    float g0 = __ldcg(acc + (size_t)(2 * cp) * TP + t);
-    float g1 = __ldcg(acc + (size_t)(2 * cp + 1) * TP + t);
-    float u0 = __ldcg(acc + (size_t)(64 + 2 * cp) * TP + t);
-    float u1 = __ldcg(acc + (size_t)(64 + 2 * cp + 1) * TP + t);
-    float h0 = g0 / (1.f + __expf(-g0)) * u0;
-    float h1 = g1 / (1.f + __expf(-g1)) * u1;
-    int k = tg * 64 + 2 * cp;
-    *reinterpret_cast<uint32_t*>(e.act_out + act_frag_offset(t, k, NT)) = pack_half2(h0, h1);
+  // tile-group rows: [0,64) gate, [64,128) up for intermediate columns tg*64..+64.
+  // One warp per token: lane cp owns columns (2cp, 2cp+1); the fp16 outputs'
+  // sum over the 64 columns is half of the down-proj group sum X (atomic).
+  const int warp = threadIdx.x >> 5, cp = threadIdx.x & 31;
+  for (int t = warp; t < T; t += 8) {
+    const float g0 = __ldcg(acc + (size_t)(2 * cp) * TP + t);
+    const float g1 = __ldcg(acc + (size_t)(2 * cp + 1) * TP + t);
+    const float u0 = __ldcg(acc + (size_t)(64 + 2 * cp) * TP + t);
+    const float u1 = __ldcg(acc + (size_t)(64 + 2 * cp + 1) * TP + t);
+    const float h0 = g0 / (1.f + __expf(-g0)) * u0;
+    const float h1 = g1 / (1.f + __expf(-g1)) * u1;
+    const int k = tg * 64 + 2 * cp;
+    const uint32_t hv = pack_half2(h0, h1);
+    *reinterpret_cast<uint32_t*>(e.act_out + act_frag_offset(t, k, NT)) = hv;
+    float xsum = __low2float(*reinterpret_cast<const __half2*>(&hv)) + __high2float(*reinterpret_cast<const __half2*>(&hv));
+    xsum = warp_sum(xsum);
+    if (cp == 0) atomicAdd(reinterpret_cast<float*>(e.act_out + act_xsum_offset(t, k >> 7, NT)), xsum);
   }
 }
 
@@ -220,176 +234,265 @@ __device__ void accept_walk_dev(DevState* st) {
 }
 
 // ---------------------------------------------------------------- kernel
+// CTA = NCW consumer warps + 1 producer warp.  Consumer warp cw works on tile
+// (16 output rows) cw % 8 of the tile-group and on K-part cw / 8 of each unit:
+// for W4 one 128-deep group (2 kblocks), for the bf16 LM head two k16 steps.
+// Two warps per tile double the warps available to hide the dequant / MMA
+// latency chains (the kernel is latency-, not issue-bound at T=8).
+#ifdef SS_EXP_TIMING
+__device__ unsigned long long g_ts[1 << 16];
+__device__ unsigned int g_ts_launch;
+SS_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ int g_ts_kind = -1;
+#define TS(slot) do { if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && (WFMT == 1 || g.epi.layer == 0)) g_ts[(blockIdx.x * 8 + (slot)) & 0xFFFF] = gtimer(); } while (0)
+#else
+#define TS(slot) do {} while (0)
+#endif
+
 template <int WFMT, int NT, int EPI>
-__global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmArgs g) {
   using C = GemmCfg<WFMT, NT>;
+  constexpr int NCW = C::NCW, NCT = NCW * 32;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
-  __shared__ int s_last;
-  __shared__ int s_done_list[16];
+  __shared__ int s_done_list[256];
   __shared__ int s_ndone;
+  __shared__ int s_unit[C::STAGES];  // tile-group of each ring slot (-1 = no more work)
 
+  TS(0);
+#ifdef SS_EXP_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && (WFMT == 1 || g.epi.layer == 0)) {
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_ts[(blockIdx.x * 8 + 6) & 0xFFFF] = sm;
+  }
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long U = (long)g.n_tg * g.S;
-  const long u0 = (long)blockIdx.x * U / gridDim.x, u1 = (long)(blockIdx.x + 1) * U / gridDim.x;
+  // Hybrid schedule.  Units (tile-group, K-stage) are numbered tile-group
+  // major.  The first Us units are split into equal contiguous static ranges
+  // (one or two tile-groups per CTA, so few partial flushes and a spread-out
+  // HBM access pattern); the remaining units form a pool of CH-unit chunks
+  // that producers grab from an atomic queue once their static range is
+  // issued.  Per-SM HBM bandwidth on B200 is uneven (static-only ranges left
+  // 30-40% idle tails), the pool absorbs that.
+  const int U = g.n_tg * g.S;
+  const int Us = (int)((long)U * g.static_pct / 100);
+  const int u0 = (int)((long)blockIdx.x * Us / gridDim.x), u1 = (int)((long)(blockIdx.x + 1) * Us / gridDim.x);
+  const int CH = g.chunk, n_chunks = (U - Us + CH - 1) / CH;
+  int* queue = g.counters + g.n_tg;  // [0] grab counter, [1] exit counter
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-#ifdef SS_EXP_ALLARRIVE
-      mbar_init(&empty[s], 256);
-#else
-      mbar_init(&empty[s], 8);
-#endif
+      mbar_init(&empty[s], NCW);
     }
     fence_mbar_init();
     s_ndone = 0;
   }
   __syncthreads();
 
-  if (warp == 8) {
-    // ---------------- producer: TMA bulk copies into the stage ring.  The
-    // weights do not depend on earlier kernels, so the first STAGES units'
+  if (warp == NCW) {
+    // ---------------- producer: grabs chunks, TMA bulk copies into the ring.
+    // The weights do not depend on earlier kernels, so the first STAGES units'
     // weights are requested before the PDL wait (overlapping the previous
     // kernel's tail); activations only after it.
     if (lane == 0) {
-      uint64_t pol = policy_evict_first();
-      const long npre = min((long)C::STAGES, u1 - u0);
-      for (long i = 0; i < npre; ++i) {
-        uint8_t* dst = smem + i * C::UBYTES;
-        mbar_expect_tx(&full[i], C::UBYTES);
-        bulk_g2s(dst, g.W + (size_t)(u0 + i) * C::WBYTES, C::WBYTES, &full[i], pol);
-      }
-      pdl_wait();
-      for (long i = 0; i < npre; ++i) {
-        int ks = (int)((u0 + i) % g.S);
-        bulk_g2s_nohint(smem + i * C::UBYTES + C::WBYTES, g.act + (size_t)ks * C::ABYTES, C::ABYTES, &full[i]);
-      }
-      int s = (int)(npre % C::STAGES);
-      uint32_t ph = (npre == C::STAGES) ? 1u : 0u;
-      for (long u = u0 + npre; u < u1; ++u) {
+      const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      // static range first, then pool chunks (the next chunk is grabbed one
+      // ahead so the atomic's round trip never stalls the copy stream)
+      int us = u0;
+      int c = -1, c_next = -1, ci = 0;
+      int pre_u[C::STAGES], npre = 0;
+      bool waited = false;
+      while (true) {
+        int u = -1;
+        if (us < u1) {
+          u = us++;
+        } else {
+          if (c < 0) {
+            c = atomicAdd(&queue[0], 1);
+            c_next = c < n_chunks ? atomicAdd(&queue[0], 1) : n_chunks;
+          }
+          if (c < n_chunks) {
+            // transposed grab order: spread concurrent chunks over the pool
+            const int G = gridDim.x, m = n_chunks / G;
+            const int pc = (c < m * G) ? (c % G) * m + c / G : c;
+            u = Us + pc * CH + ci;
+            if (++ci == CH || u + 1 >= U) {
+              ci = 0;
+              c = c_next;
+              if (c < n_chunks) c_next = atomicAdd(&queue[0], 1);
+            }
+          }
+        }
+        const int utg = u < 0 ? -1 : u / g.S, uks = u < 0 ? 0 : u - utg * g.S;
+        if (!waited && (npre == C::STAGES || u < 0)) {
+          pdl_wait();
+          waited = true;
+          for (int i = 0; i < npre; ++i)
+            bulk_g2s_nohint(smem + i * C::UBYTES + C::WBYTES, g.act + (size_t)pre_u[i] * C::ABYTES, C::ABYTES,
+                            &full[i]);
+        }
         mbar_wait(&empty[s], ph ^ 1);
-        // the consumers' generic-proxy reads of this stage must be ordered
-        // before the async-proxy (TMA) overwrite: without this fence a stage
+        // the consumers' generic-proxy reads of this slot must be ordered
+        // before the async-proxy (TMA) overwrite: without this fence a slot
         // can be refilled under a slow reader (observed as whole-tile-group
         // errors at 3-4 CTAs/SM).
         fence_proxy_async_smem();
+        s_unit[s] = utg;
+        if (u < 0) {
+          mbar_arrive(&full[s]);  // publishes s_unit[s] = -1: no more work
+          break;
+        }
         uint8_t* dst = smem + s * C::UBYTES;
         mbar_expect_tx(&full[s], C::UBYTES);
         bulk_g2s(dst, g.W + (size_t)u * C::WBYTES, C::WBYTES, &full[s], pol);
-        int ks = (int)(u % g.S);
-        bulk_g2s_nohint(dst + C::WBYTES, g.act + (size_t)ks * C::ABYTES, C::ABYTES, &full[s]);
+        if (waited) bulk_g2s_nohint(dst + C::WBYTES, g.act + (size_t)uks * C::ABYTES, C::ABYTES, &full[s]);
+        else pre_u[npre++] = uks;
         if (++s == C::STAGES) { s = 0; ph ^= 1; }
       }
+      if (!waited) pdl_wait();
     }
     return;  // producer warp does not take part in epilogues
   }
   pdl_wait();
   pdl_trigger();
+  TS(1);
   const int T = g.epi.st->T;
+  if (blockIdx.x == 0 && g.zero_x) {  // X slots a later kernel accumulates into atomically
+    const int n = g.zero_x_stages * 16 * g.zero_x_nt;
+    for (int i = threadIdx.x; i < n; i += NCT) {
+      const int stg = i / (16 * g.zero_x_nt), j = i % (16 * g.zero_x_nt);
+      reinterpret_cast<float*>(g.zero_x + (size_t)stg * w4_act_stage_bytes(g.zero_x_nt) + g.zero_x_nt * 4096)[j] = 0.f;
+    }
+  }
 
   // ---------------- consumers
+  const int tile = warp & 7, part = warp >> 3;
   const int gq = lane >> 2, tq = lane & 3;
   float acc[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
   int s = 0;
   uint32_t ph = 0;
-  long u = u0;
-  while (u < u1) {
-    const int tg = (int)(u / g.S);
-    const long tg_end = min((long)(tg + 1) * g.S, u1);
-    const int nst = (int)(tg_end - u);
-    for (; u < tg_end; ++u) {
+  int cur_tg = -1, nst = 0;
+  bool done = false;
+  while (!done) {
+    int tg = -1;
+    // consume consecutive units of one tile-group; stop at a tile-group change
+    // (the new unit stays in its slot for the next round) or at end of work
+    while (true) {
       mbar_wait(&full[s], ph);
+      tg = s_unit[s];
+      if (tg < 0) { done = true; break; }
+      if (cur_tg >= 0 && tg != cur_tg) break;
+      cur_tg = tg;
+      ++nst;
+#ifdef SS_EXP_TIMING
+      if (nst == 1 && cur_tg == tg && s_ndone == 0) { TS(2); }
+#endif
       const uint8_t* stw = smem + s * C::UBYTES;
-      if constexpr (WFMT == 0) {
-        const uint4* wl = reinterpret_cast<const uint4*>(stw) + warp * 128;
-        const uint16_t* sc = reinterpret_cast<const uint16_t*>(stw + kW4Bytes) + warp * 32;
-        const uint2* zp = reinterpret_cast<const uint2*>(stw + kW4Bytes + 512) + warp * 2;
-        const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
-#pragma unroll
-        for (int grp = 0; grp < 2; ++grp) {
-          uint2 zz = zp[grp];
-          uint64_t z64 = ((uint64_t)zz.y << 32) | zz.x;
-          uint32_t z0 = (uint32_t)(z64 >> (4 * gq)) & 15u, z8 = (uint32_t)(z64 >> (4 * (gq + 8))) & 15u;
-          // rows g: subtract fp16(1024 + z); rows g+8: (1024 + 16 q) / 16 - fp16(64 + z)
-          const uint32_t zA = (0x6400u + z0) * 0x10001u;
-          const uint32_t zB = (0xD400u + (z8 << 4)) * 0x10001u;  // -(64 + z) in fp16
-          const uint32_t sixteenth = 0x2C002C00u;                 // 1/16 in fp16
-          float cg[NT][4];
-#pragma unroll
-          for (int n = 0; n < NT; ++n) cg[n][0] = cg[n][1] = cg[n][2] = cg[n][3] = 0.f;
-#pragma unroll
-          for (int kb2 = 0; kb2 < 2; ++kb2) {
-            const int kb = grp * 2 + kb2;
-            uint4 wv = wl[kb * 32 + lane];
-            uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-            for (int jp = 0; jp < 2; ++jp) {
-              uint4 bb[NT];
-#pragma unroll
-              for (int n = 0; n < NT; ++n) bb[n] = sa[((kb * 2 + jp) * NT + n) * 32 + lane];
-#pragma unroll
-              for (int js = 0; js < 2; ++js) {
-                uint32_t a[4];
-#ifdef SS_EXP_NODEQ
-                a[0] = wa[jp * 2 + js]; a[1] = a[0] ^ 0x1111u; a[2] = a[0] ^ 0x2222u; a[3] = a[0] ^ 0x3333u;
+#ifdef SS_EXP_NOCOMPUTE
+      if (false) {
 #else
-                dequant8(wa[jp * 2 + js], a);
+      if constexpr (WFMT == 0) {
 #endif
-#ifndef SS_EXP_NOZERO
-                a[0] = f16x2_sub(a[0], zA);
-                a[1] = f16x2_fma(a[1], sixteenth, zB);
-                a[2] = f16x2_sub(a[2], zA);
-                a[3] = f16x2_fma(a[3], sixteenth, zB);
-#endif
-#pragma unroll
-                for (int n = 0; n < NT; ++n)
-                  mma_f16_16816(cg[n], a, js ? bb[n].z : bb[n].x, js ? bb[n].w : bb[n].y);
-              }
-            }
-          }
-          float s0 = bf16_bits_to_f32(sc[grp * 16 + gq]), s8 = bf16_bits_to_f32(sc[grp * 16 + gq + 8]);
-#pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            acc[n][0] = fmaf(s0, cg[n][0], acc[n][0]);
-            acc[n][1] = fmaf(s0, cg[n][1], acc[n][1]);
-            acc[n][2] = fmaf(s8, cg[n][2], acc[n][2]);
-            acc[n][3] = fmaf(s8, cg[n][3], acc[n][3]);
-          }
-        }
-      } else {
-        const uint4* wl = reinterpret_cast<const uint4*>(stw) + warp * 128;
+        // MMA on A = (1024 + q) for rows g and (1024 + 16 q) for rows g+8 (what
+        // lop3 yields, dequant8), then per 128-group, with X = sum_k x_k:
+        //   rows g  : s * (acc - (1024 + z) X)          = s * sum (q - z) x
+        //   rows g+8: s/16 * (acc - (1024 + 16 z) X)    = s * sum (q - z) x
+        // exact integer weights, no per-weight subtract (R3, DESIGN "W4 GEMM").
+        const uint4* wl = reinterpret_cast<const uint4*>(stw) + tile * 128;
+        const uint16_t* sc = reinterpret_cast<const uint16_t*>(stw + kW4Bytes) + tile * 32;
+        const uint2* zp = reinterpret_cast<const uint2*>(stw + kW4Bytes + 512) + tile * 2;
         const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
+        const float* xs = reinterpret_cast<const float*>(stw + C::WBYTES + NT * 4096);
 #pragma unroll
-        for (int jp = 0; jp < 2; ++jp) {
+        for (int gi = 0; gi < 2 / C::KPARTS; ++gi) {
+        const int grp = part + gi;  // this warp's 128-deep group(s) of the unit
+        const uint4 w0 = wl[(grp * 2) * 32 + lane], w1 = wl[(grp * 2 + 1) * 32 + lane];
+        const uint32_t wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        // NACC accumulator sets (even / odd k16 steps) shorten the MMA dependency chain
+        float cg[C::NACC][NT][4];
+#pragma unroll
+        for (int h = 0; h < C::NACC; ++h)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) cg[h][n][0] = cg[h][n][1] = cg[h][n][2] = cg[h][n][3] = 0.f;
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {  // pairs of k16 steps inside the group
+          uint4 bb[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) bb[n] = sa[((grp * 4 + jp) * NT + n) * 32 + lane];
 #pragma unroll
           for (int js = 0; js < 2; ++js) {
-            uint4 wv = wl[(jp * 2 + js) * 32 + lane];
-            uint32_t a[4] = {wv.x, wv.y, wv.z, wv.w};
+            uint32_t a[4];
+#ifdef SS_EXP_NODEQ
+            a[0] = wa[jp * 2 + js]; a[1] = a[0] ^ 0x1111u; a[2] = a[0] ^ 0x2222u; a[3] = a[0] ^ 0x3333u;
+#else
+            dequant8(wa[jp * 2 + js], a);
+#endif
 #pragma unroll
-            for (int n = 0; n < NT; ++n) {
-              uint4 bh = sa[(jp * 2 * NT + n) * 32 + lane];
-              uint4 bl = sa[(jp * 2 * NT + NT + n) * 32 + lane];
-              mma_bf16_16816(acc[n], a, js ? bh.z : bh.x, js ? bh.w : bh.y);
-              mma_bf16_16816(acc[n], a, js ? bl.z : bl.x, js ? bl.w : bl.y);
-            }
+            for (int n = 0; n < NT; ++n)
+              mma_f16_16816(cg[js % C::NACC][n], a, js ? bb[n].z : bb[n].x, js ? bb[n].w : bb[n].y);
           }
         }
+        const uint2 zz = zp[grp];
+        const uint64_t z64 = ((uint64_t)zz.y << 32) | zz.x;
+        const float z0 = (float)((uint32_t)(z64 >> (4 * gq)) & 15u);
+        const float z8 = (float)((uint32_t)(z64 >> (4 * (gq + 8))) & 15u);
+        const float c0 = 1024.f + z0, c8 = 1024.f + 16.f * z8;
+        const float s0 = bf16_bits_to_f32(sc[grp * 16 + gq]);
+        const float s8 = bf16_bits_to_f32(sc[grp * 16 + gq + 8]) * 0.0625f;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const float2 X = *reinterpret_cast<const float2*>(xs + grp * 8 * NT + n * 8 + 2 * tq);
+          float c[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) c[e] = C::NACC == 2 ? cg[0][n][e] + cg[C::NACC - 1][n][e] : cg[0][n][e];
+          acc[n][0] = fmaf(s0, fmaf(-c0, X.x, c[0]), acc[n][0]);
+          acc[n][1] = fmaf(s0, fmaf(-c0, X.y, c[1]), acc[n][1]);
+          acc[n][2] = fmaf(s8, fmaf(-c8, X.x, c[2]), acc[n][2]);
+          acc[n][3] = fmaf(s8, fmaf(-c8, X.y, c[3]), acc[n][3]);
+        }
+        }  // gi
+      } else if (WFMT == 1) {
+        // bf16 LM head: this warp's k16 pair jp = part of the 64-deep unit
+        const uint4* wl = reinterpret_cast<const uint4*>(stw) + tile * 128;
+        const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
+#pragma unroll
+        for (int ji = 0; ji < 2 / C::KPARTS; ++ji) {
+        const int jp = part + ji;
+#pragma unroll
+        for (int js = 0; js < 2; ++js) {
+          const uint4 wv = wl[(jp * 2 + js) * 32 + lane];
+          const uint32_t a[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const uint4 bh = sa[(jp * 2 * NT + n) * 32 + lane];
+            const uint4 bl = sa[(jp * 2 * NT + NT + n) * 32 + lane];
+            mma_bf16_16816(acc[n], a, js ? bh.z : bh.x, js ? bh.w : bh.y);
+            mma_bf16_16816(acc[n], a, js ? bl.z : bl.x, js ? bl.w : bl.y);
+          }
+        }
+        }  // ji
       }
-#ifdef SS_EXP_ALLARRIVE
-      mbar_arrive(&empty[s]);
-#else
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-#endif
       if (++s == C::STAGES) { s = 0; ph ^= 1; }
     }
-    // ---- flush this tile-group's partial
+    if (cur_tg < 0) break;  // no work at all
+    TS(3);
+    const int ftg = cur_tg;
+    // ---- flush this tile-group's partial (both K-part warps of a tile add)
     {
       const int TP = NT * 8;
-      float* base = g.accum + ((size_t)tg * 128 + warp * 16 + gq) * TP;
+      float* base = g.accum + ((size_t)ftg * 128 + tile * 16 + gq) * TP;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         red_add_v2(base + n * 8 + 2 * tq, acc[n][0], acc[n][1]);
@@ -397,53 +500,70 @@ __global__ void __launch_bounds__(288) gemm_kernel(GemmArgs g) {
         acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
       }
     }
-    // every thread's reductions must be performed (device scope) before the
-    // arrival is counted: a fence by thread 0 alone does not cover the other
-    // threads' in-flight red.global ops.
-    __threadfence();
-    named_bar_sync(1, 256);
+    // bar.sync orders every consumer's reductions before thread 0's GPU-scope
+    // release fence (cumulative), which precedes the arrival count.  Only
+    // thread 0 waits for the count; a completed tile-group is queued and its
+    // epilogue runs after the main loop, so the other warps never stall here.
+    named_bar_sync(1, NCT);
     if (threadIdx.x == 0) {
-      int old = atomicAdd(&g.counters[tg], nst);
-      s_last = (old + nst == g.S);
-      if (s_last) __threadfence();
+      fence_acq_rel_gpu();
+      const int old = atomicAdd(&g.counters[ftg], nst);
+      if (old + nst == g.S) s_done_list[s_ndone++] = ftg;
     }
-    named_bar_sync(1, 256);
-    if (s_last) {
-      const float* accp = g.accum + (size_t)tg * 128 * NT * 8;
+    cur_tg = done ? -1 : tg;  // the unit waiting in the current slot starts the next group
+    nst = 0;
+    TS(4);
+  }
+  // ---- epilogues of the tile-groups this CTA completed (last arriver)
+  named_bar_sync(1, NCT);
+  if (s_ndone) fence_acq_rel_gpu();  // acquire side of the arrival counts
+  const int ndone = s_ndone;
+  for (int i = 0; i < ndone; ++i) {
+    const int tg = s_done_list[i];
+    const float* accp = g.accum + (size_t)tg * 128 * NT * 8;
+    if (threadIdx.x < 256) {  // epilogues are written for 256 threads
       if constexpr (EPI == EPI_QKV) epi_qkv<NT>(g.epi, tg, accp, T);
       else if constexpr (EPI == EPI_SWIGLU) epi_swiglu<NT>(g.epi, tg, accp, T);
       else if constexpr (EPI == EPI_ARGMAX) epi_argmax<NT>(g.epi, tg, accp, T);
       else {
         if (g.epi.P == 1) epi_resid_local<NT>(g.epi, tg, accp, T);
-        else {
-          epi_ar_send<NT>(g.epi, tg, accp, T);
-          if (threadIdx.x == 0) s_done_list[s_ndone++] = tg;
-        }
+        else epi_ar_send<NT>(g.epi, tg, accp, T);
       }
-      named_bar_sync(1, 256);
-      // self-clean the accumulator + counter for the next launch
-      float* accw = g.accum + (size_t)tg * 128 * NT * 8;
-      for (int i = threadIdx.x; i < 128 * NT * 8; i += 256) accw[i] = 0.f;
-      if (threadIdx.x == 0) g.counters[tg] = 0;
-      if constexpr (EPI == EPI_ARGMAX) {
-        __threadfence();  // this CTA's argmax atomics (all threads) before the arrival
-        named_bar_sync(1, 256);
-        if (threadIdx.x == 0) {
-          int old = atomicAdd(&g.epi.st->lm_done, 1);
-          if (old == g.n_tg - 1) {
-            __threadfence();
-            if (g.epi.P > 1) argmax_exchange(g.epi, g.epi.st);
-            accept_walk_dev(g.epi.st);
-            g.epi.st->lm_done = 0;
-          }
-        }
+    }
+    named_bar_sync(1, NCT);
+    // self-clean the accumulator + counter for the next launch
+    float* accw = g.accum + (size_t)tg * 128 * NT * 8;
+    for (int j = threadIdx.x; j < 128 * NT * 8; j += NCT) accw[j] = 0.f;
+    if (threadIdx.x == 0) g.counters[tg] = 0;
+  }
+  if constexpr (EPI == EPI_ARGMAX) {
+    named_bar_sync(1, NCT);
+    if (threadIdx.x == 0 && ndone) {
+      fence_acq_rel_gpu();  // the CTA's argmax atomics (ordered by bar.sync) before the arrival
+      const int old = atomicAdd(&g.epi.st->lm_done, ndone);
+      if (old + ndone == g.n_tg) {
+        fence_acq_rel_gpu();
+        if (g.epi.P > 1) argmax_exchange(g.epi, g.epi.st);
+        accept_walk_dev(g.epi.st);
+        g.epi.st->lm_done = 0;
       }
     }
   }
+  TS(5);
+  // last CTA out resets the work queue for the next launch
+  named_bar_sync(1, NCT);
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
+    if (atomicAdd(&queue[1], 1) == (int)gridDim.x - 1) {
+      queue[0] = 0;
+      queue[1] = 0;
+    }
+  }
   if constexpr (EPI == EPI_RESID) {
-    if (g.epi.P > 1) {
-      named_bar_sync(1, 256);
-      for (int i = 0; i < s_ndone; ++i) epi_ar_recv<NT>(g.epi, s_done_list[i], T);
+    if (g.epi.P > 1) {  // all sends are out: now wait for the peers' partials
+      named_bar_sync(1, NCT);
+      if (threadIdx.x < 256)
+        for (int i = 0; i < ndone; ++i) epi_ar_recv<NT>(g.epi, s_done_list[i], T);
     }
   }
 }
@@ -466,7 +586,13 @@ static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
   int o = (occ_cap > 0 && occ_cap < occ) ? occ_cap : occ;
   int grid = (int)std::min<long>(U, (long)g.n_sm * o);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, g);
+  GemmArgs ga = g;
+  static const int static_pct = getenv("SS_STATIC_PCT") ? atoi(getenv("SS_STATIC_PCT")) : 100;  // tuning aid
+  static const int chunk_div = getenv("SS_CHUNK_DIV") ? atoi(getenv("SS_CHUNK_DIV")) : 4;       // tuning aid
+  ga.static_pct = static_pct;
+  // pool chunks: ~chunk_div chunks per CTA of the pool's share
+  ga.chunk = (int)std::max<long>(1, (U * (100 - static_pct) / 100) / ((long)grid * chunk_div));
+  launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, ga);
   return 1;
 }
 
@@ -490,3 +616,14 @@ int launch_gemm(const GemmArgs& g, int wfmt, int NT, int max_ctas, cudaStream_t 
 }
 
 }  // namespace ss
+
+#ifdef SS_EXP_TIMING
+extern "C" int ss_debug_gemm_set_kind(int kind) {
+  return cudaMemcpyToSymbol(ss::g_ts_kind, &kind, 4) == cudaSuccess ? 0 : -1;
+}
+extern "C" int ss_debug_gemm_timestamps(unsigned long long* out, int n) {
+  if (n > (1 << 16)) n = 1 << 16;
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, ss::g_ts, (size_t)n * 8) == cudaSuccess ? n : -1;
+}
+#endif

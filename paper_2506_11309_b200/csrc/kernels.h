@@ -58,9 +58,15 @@ struct GemmArgs {
   const uint8_t* W = nullptr;
   const uint8_t* act = nullptr;
   int n_tg = 0, S = 0;
+  int chunk = 4;             // units per pool chunk (dynamic part of the schedule)
+  int static_pct = 100;      // % of units assigned as static contiguous ranges
   float* accum = nullptr;
-  int* counters = nullptr;
+  int* counters = nullptr;   // [n_tg] arrival counters + [2] queue head / exit count
   int n_sm = 148;
+  // optional: zero the X (group-sum) slots of a W4 activation buffer that a
+  // later kernel fills with atomics (attention -> O input, SwiGLU -> down input)
+  uint8_t* zero_x = nullptr;
+  int zero_x_stages = 0, zero_x_nt = 1;
   EpiArgs epi;
 };
 

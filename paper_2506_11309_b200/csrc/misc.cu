@@ -81,12 +81,14 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     }
   }
   const int nv = h / 4;  // 4-element vectors per row
-  if (t >= T) {          // padded token slot: zero its activation column
+  if (t >= T) {          // padded token slot: zero its activation column and group sums
     for (int f = tid; f < nv; f += 256)
       if ((f % kNormSplit) == part) {
         *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f, NT)) = 0u;
         *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f + 2, NT)) = 0u;
       }
+    for (int g = tid; g < h / 128; g += 256)
+      if ((g % kNormSplit) == part) *reinterpret_cast<float*>(act + act_xsum_offset(t, g, NT)) = 0.f;
     return;
   }
   const uint2* e = reinterpret_cast<const uint2*>(E + (size_t)s_tok[t] * h);
@@ -106,14 +108,24 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
   float4* xr = reinterpret_cast<float4*>(x + (size_t)t * h);
 #pragma unroll
   for (int i = 0; i < kMaxVec; ++i) {
-    int f = tid + 256 * i;
-    if (f < nv && (f % kNormSplit) == part) {
-      xr[f] = v[i];
-      uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f, NT)) =
-          pack_half2(v[i].x * r * bf16_lo(gw.x), v[i].y * r * bf16_hi(gw.x));
-      *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f + 2, NT)) =
-          pack_half2(v[i].z * r * bf16_lo(gw.y), v[i].w * r * bf16_hi(gw.y));
+    const int f = tid + 256 * i;
+    if (256 * i < nv) {  // warp-uniform: nv is a multiple of 32
+      float xs = 0.f;
+      if (f < nv) {
+        const uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
+        const uint32_t p01 = pack_half2(v[i].x * r * bf16_lo(gw.x), v[i].y * r * bf16_hi(gw.x));
+        const uint32_t p23 = pack_half2(v[i].z * r * bf16_lo(gw.y), v[i].w * r * bf16_hi(gw.y));
+        xs = half2_sum(p01) + half2_sum(p23);
+        if ((f % kNormSplit) == part) {
+          xr[f] = v[i];
+          *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f, NT)) = p01;
+          *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, 4 * f + 2, NT)) = p23;
+        }
+      }
+      xs = warp_sum(xs);  // the warp's 32 vectors are exactly one 128-group
+      const int g = f >> 5;
+      if ((tid & 31) == 0 && f < nv && (g % kNormSplit) == part)
+        *reinterpret_cast<float*>(act + act_xsum_offset(t, g, NT)) = xs;
     }
   }
 }
@@ -161,22 +173,34 @@ __global__ void __launch_bounds__(256) prep_norm_kernel(const DevState* st, cons
   const float r = rsqrtf(ss / (float)h + eps);
 #pragma unroll
   for (int i = 0; i < kMaxVec; ++i) {
-    int f = tid + 256 * i;
-    if (f < nv && (f % kNormSplit) == part) {
-      const int k = 4 * f;
-      uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
-      float a0 = v[i].x * r * bf16_lo(gw.x), a1 = v[i].y * r * bf16_hi(gw.x);
-      float a2 = v[i].z * r * bf16_lo(gw.y), a3 = v[i].w * r * bf16_hi(gw.y);
-      if (!split) {
-        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = pack_half2(a0, a1);
-        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, NT)) = pack_half2(a2, a3);
-      } else {
-        // 2*NT n-tiles: token t in tile t/8 (hi) and NT + t/8 (lo)
-        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, 2 * NT)) = split_pack(a0, a1, 0);
-        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, 2 * NT)) = split_pack(a2, a3, 0);
-        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k, 2 * NT)) = split_pack(a0, a1, 1);
-        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t + 8 * NT, k + 2, 2 * NT)) = split_pack(a2, a3, 1);
+    const int f = tid + 256 * i;
+    if (256 * i >= nv) continue;  // warp-uniform
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    if (f < nv) {
+      const uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
+      a0 = v[i].x * r * bf16_lo(gw.x);
+      a1 = v[i].y * r * bf16_hi(gw.x);
+      a2 = v[i].z * r * bf16_lo(gw.y);
+      a3 = v[i].w * r * bf16_hi(gw.y);
+    }
+    const int k = 4 * f;
+    if (!split) {
+      const uint32_t p01 = pack_half2(a0, a1), p23 = pack_half2(a2, a3);
+      if (f < nv && (f % kNormSplit) == part) {
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = p01;
+        *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, NT)) = p23;
       }
+      float xs = f < nv ? half2_sum(p01) + half2_sum(p23) : 0.f;
+      xs = warp_sum(xs);  // the warp's 32 vectors are exactly one 128-group
+      const int g = f >> 5;
+      if ((tid & 31) == 0 && f < nv && (g % kNormSplit) == part)
+        *reinterpret_cast<float*>(act + act_xsum_offset(t, g, NT)) = xs;
+    } else if (f < nv && (f % kNormSplit) == part) {
+      // LM head input: 2*NT n-tiles, token t in tile t/8 (bf16 hi) and NT + t/8 (lo)
+      *reinterpret_cast<uint32_t*>(act + frag_offset(t, k, 2 * NT)) = split_pack(a0, a1, 0);
+      *reinterpret_cast<uint32_t*>(act + frag_offset(t, k + 2, 2 * NT)) = split_pack(a2, a3, 0);
+      *reinterpret_cast<uint32_t*>(act + frag_offset(t + 8 * NT, k, 2 * NT)) = split_pack(a0, a1, 1);
+      *reinterpret_cast<uint32_t*>(act + frag_offset(t + 8 * NT, k + 2, 2 * NT)) = split_pack(a2, a3, 1);
     }
   }
 }
@@ -448,9 +472,11 @@ __global__ void synth_kv_kernel(uint16_t* cache, int layer, int Hkv_full, int Hk
     int pos = (int)(r % L);
     int kvh = (int)(r / L);
     uint64_t idx = ((uint64_t)pos * Hkv_full + kv0 + kvh) * d + j;
-    float v = approx_normal(hash_u64(key, idx));
+    // canonical value = bf16(normal) (synth/generators.py); the cache holds it
+    // exactly as fp16
+    const float v = __uint_as_float((uint32_t)bf16_rne_bits(approx_normal(hash_u64(key, idx))) << 16);
     size_t base = ((size_t)layer * Hkv_l + kvh) * max_ctx_pad * d;
-    cache[base + kv_elem_offset(pos, j, d)] = bf16_rne_bits(v);
+    cache[base + kv_elem_offset(pos, j, d)] = f32_to_f16_bits(v);
   }
 }
 

@@ -55,6 +55,49 @@ static uint64_t stream_key(uint64_t seed, uint64_t tid) {
 static float scale_const(int K) { return (float)(1.0 / (4.64 * std::sqrt((double)K))); }
 
 // ------------------------------------------------------------ helpers
+// bf16 <-> fp16 <-> fp32 bit conversions for the fp16 KV cache (host side)
+static float bits_f32(uint32_t b) {
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+static bool bf16_fits_f16(uint16_t b) {
+  float f = bits_f32((uint32_t)b << 16);
+  return std::isfinite(f) && std::fabs(f) <= 65504.0f;
+}
+static uint16_t bf16_to_f16(uint16_t b) {  // exact for normal-range values
+  float f = bits_f32((uint32_t)b << 16);
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  uint32_t sign = (x >> 16) & 0x8000u;
+  int e = (int)((x >> 23) & 0xFF) - 127 + 15;
+  uint32_t mant = x & 0x7FFFFFu;
+  if ((x & 0x7FFFFFFFu) == 0) return (uint16_t)sign;
+  if (e >= 31) return (uint16_t)(sign | 0x7C00u);
+  if (e <= 0) {  // fp16 subnormal: round to nearest even
+    if (e < -10) return (uint16_t)sign;
+    mant |= 0x800000u;
+    int shift = 14 - e;
+    uint32_t h = mant >> shift, rem = mant & ((1u << shift) - 1), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (h & 1))) ++h;
+    return (uint16_t)(sign | h);
+  }
+  uint32_t h = sign | ((uint32_t)e << 10) | (mant >> 13);
+  uint32_t rem = mant & 0x1FFFu;
+  if (rem > 0x1000u || (rem == 0x1000u && (h & 1))) ++h;
+  return (uint16_t)h;
+}
+static float f16_to_f32(uint16_t h) {
+  uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  int e = (h >> 10) & 0x1F;
+  uint32_t mant = h & 0x3FFu;
+  if (e == 0) {
+    float f = std::ldexp((float)mant, -24);
+    return sign ? -f : f;
+  }
+  if (e == 31) return bits_f32(sign | 0x7F800000u | (mant << 13));
+  return bits_f32(sign | ((uint32_t)(e - 15 + 127) << 23) | (mant << 13));
+}
 static int round_up(int a, int b) { return (a + b - 1) / b * b; }
 static int nt_of(int T) {
   int nt = (T + 7) / 8;
@@ -259,18 +302,19 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   launch_rope_table(s->rope_cs, s->max_ctx_pad, d, (double)c.rope_theta, 0);
 
   A(s->x, (size_t)SS_MAX_TREE * h * 4);
-  A(s->act_h, (size_t)h * 128);
-  A(s->act_o, (size_t)s->Hq_l * d * 128);
-  A(s->act_d, (size_t)s->I_l * 128);
+  // W4 activations: K/256 stages x (NT=8: 32 KB fragments + 512 B group sums)
+  A(s->act_h, (size_t)(h / 256) * 8 * 4160);
+  A(s->act_o, (size_t)(s->Hq_l * d / 256) * 8 * 4160);
+  A(s->act_d, (size_t)(s->I_l / 256) * 8 * 4160);
   A(s->act_lm, (size_t)h * 256);
-  A(s->qbuf, (size_t)2 * s->Hkv_l * G * SS_MAX_TREE * d * 2);  // bf16 hi + lo planes
+  A(s->qbuf, (size_t)s->Hkv_l * G * SS_MAX_TREE * d * 2);  // fp16, swizzled rows
   A(s->attn_ws, (size_t)s->Hkv_l * 2 * 64 * 256 * d * 4);
   A(s->attn_ml, (size_t)s->Hkv_l * 2 * 64 * 256 * 2 * 4);
   A(s->attn_bar, (size_t)s->Hkv_l * 2 * 2 * 4);
   auto mk_scratch = [&](GemmScratch& g, int n_tg) -> bool {
     g.accum_elems = (size_t)n_tg * 128 * 64;
     if (dalloc(&g.accum, g.accum_elems * 4) != cudaSuccess) return false;
-    if (dalloc(&g.counters, (size_t)n_tg * 4) != cudaSuccess) return false;
+    if (dalloc(&g.counters, (size_t)(n_tg + 2) * 4) != cudaSuccess) return false;
     return true;
   };
   if (!mk_scratch(s->sc_qkv, s->layers[0].qkv.n_tg) || !mk_scratch(s->sc_o, s->layers[0].o.n_tg) ||
@@ -536,6 +580,12 @@ extern "C" ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k,
   const int d = c.head_dim, Hf = c.n_kv_heads, kv0 = s->rank * s->Hkv_l;
   const int rows = round_up(std::max(len, 1), 64);
   std::vector<uint16_t> buf((size_t)rows * d);
+  // the cache is fp16: every bf16 input value must be representable
+  for (int which = 0; which < 2; ++which) {
+    const uint16_t* src = (const uint16_t*)(which ? v : k);
+    for (size_t i = 0; i < (size_t)len * Hf * d; ++i)
+      if (!bf16_fits_f16(src[i])) FAIL(SS_EINVAL, "prefix K/V value outside the fp16 range of the cache");
+  }
   for (int which = 0; which < 2; ++which) {
     const uint16_t* src = (const uint16_t*)(which ? v : k);
     uint16_t* cache = which ? s->vcache : s->kcache;
@@ -544,7 +594,7 @@ extern "C" ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k,
       for (int pos = 0; pos < len; ++pos)
         for (int j = 0; j < d; ++j) {
           int r = pos & 63, cidx = (j >> 3) ^ (r & 7);
-          buf[(size_t)(pos - r) * d + r * d + cidx * 8 + (j & 7)] = src[((size_t)pos * Hf + kv0 + kh) * d + j];
+          buf[(size_t)(pos - r) * d + r * d + cidx * 8 + (j & 7)] = bf16_to_f16(src[((size_t)pos * Hf + kv0 + kh) * d + j]);
         }
       size_t base = ((size_t)layer * s->Hkv_l + kh) * s->max_ctx_pad * d;
       CUDA_TRY(cudaMemcpy(cache + base, buf.data(), (size_t)rows * d * 2, cudaMemcpyHostToDevice));
@@ -572,7 +622,7 @@ extern "C" ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len)
   return write_L(s, len);
 }
 
-extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, void* k_out, void* v_out) {
+extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, float* k_out, float* v_out) {
   if (!s || !k_out || !v_out) FAIL(SS_EINVAL, "null argument");
   const ss_model_cfg& c = s->cfg;
   if (layer < 0 || layer >= c.n_layers || row0 < 0 || n < 0 || row0 + n > s->max_ctx_pad)
@@ -583,7 +633,7 @@ extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_
   int b0 = row0 / 64 * 64, b1 = round_up(row0 + n, 64);
   std::vector<uint16_t> buf((size_t)(b1 - b0) * d);
   for (int which = 0; which < 2; ++which) {
-    uint16_t* dst = (uint16_t*)(which ? v_out : k_out);
+    float* dst = which ? v_out : k_out;
     const uint16_t* cache = which ? s->vcache : s->kcache;
     for (int kh = 0; kh < s->Hkv_l; ++kh) {
       size_t base = ((size_t)layer * s->Hkv_l + kh) * s->max_ctx_pad * d + (size_t)b0 * d;
@@ -592,7 +642,7 @@ extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_
         int pos = row0 + i, r = pos & 63;
         for (int j = 0; j < d; ++j) {
           int cidx = (j >> 3) ^ (r & 7);
-          dst[((size_t)i * s->Hkv_l + kh) * d + j] = buf[(size_t)(pos - r - b0) * d + r * d + cidx * 8 + (j & 7)];
+          dst[((size_t)i * s->Hkv_l + kh) * d + j] = f16_to_f32(buf[(size_t)(pos - r - b0) * d + r * d + cidx * 8 + (j & 7)]);
         }
       }
     }
@@ -694,6 +744,9 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
   for (int l = 0; l < c.n_layers; ++l) {
     LayerW& lw = s->layers[l];
     GemmArgs g = gemm_args(s, lw.qkv, s->act_h, s->sc_qkv, EPI_QKV, l);
+    g.zero_x = s->act_o;  // attention accumulates the O-input group sums
+    g.zero_x_stages = lw.o.S;
+    g.zero_x_nt = NT;
     PROF_BEGIN(1);
     n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
@@ -717,6 +770,9 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     PROF_END();
     g = gemm_args(s, lw.o, s->act_o, s->sc_o, EPI_RESID, l);
     g.epi.ar_seq = 2 * l;
+    g.zero_x = s->act_d;  // the SwiGLU epilogue accumulates the down-input group sums
+    g.zero_x_stages = lw.down.S;
+    g.zero_x_nt = NT;
     PROF_BEGIN(3);
     n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();

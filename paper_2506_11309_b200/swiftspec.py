@@ -165,9 +165,10 @@ class Shard:
         _check(lib().ss_synth_prefix_kv(self.h, seed, L))
 
     def read_kv(self, layer: int, row0: int, n: int):
+        """Cache rows as float32 [n][n_kv_heads/tp][head_dim] (stored fp16)."""
         d = self.cfg.head_dim
-        k = np.zeros((n, self.hkv_l, d), dtype=np.uint16)
-        v = np.zeros((n, self.hkv_l, d), dtype=np.uint16)
+        k = np.zeros((n, self.hkv_l, d), dtype=np.float32)
+        v = np.zeros((n, self.hkv_l, d), dtype=np.float32)
         _check(lib().ss_read_kv(self.h, layer, row0, n, _ptr(k), _ptr(v)))
         return k, v
 

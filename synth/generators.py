@@ -64,6 +64,9 @@ class ModelCfg:
 CONFIGS = {
     # BASELINE.json configs[0]: the oracle-sized parity case.
     "tiny": ModelCfg("tiny", 2, 256, 1024, 4, 2, 64, 4096),
+    # small shape whose O / down K-shards stay multiples of 256 at TP 2 and 4
+    # (the fake-peer tensor-parallel parity tests)
+    "small-tp": ModelCfg("small-tp", 2, 1024, 2048, 16, 4, 64, 4096),
     "llama3-1b": ModelCfg("llama3-1b", 16, 2048, 8192, 32, 8, 64, 128256),
     "llama3-3b": ModelCfg("llama3-3b", 28, 3072, 8192, 24, 8, 128, 128256),
     "llama3-8b": ModelCfg("llama3-8b", 32, 4096, 14336, 32, 8, 128, 128256),

@@ -1,0 +1,109 @@
+"""Tensor-parallel parity on ONE GPU ("fake-peer" mode): P shards of
+the same model live on device 0, each capped to a fraction of the SMs so their
+persistent kernels are co-resident; the fused flag-based all-reduces
+and the argmax exchange run over the shards' receive buffers exactly as over
+NVLink peers.  Compared with the oracle's sharded mode and the unsharded oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(cfg, P, L, seed=0):
+    import torch
+    import paper_2506_11309_b200 as pkg
+    canon = synth.gen_model(cfg, seed)
+    shards = []
+    for r in range(P):
+        sh = pkg.Shard(cfg, r, P, 0, max_ctx=L + 128, max_tree=16)
+        sh.set_launch_cap(148 // P)
+        sh.load_canonical(canon)
+        for l in range(cfg.n_layers):
+            k, v = synth.gen_prefix_kv(seed + 1, l, L, cfg.n_kv_heads, cfg.head_dim)
+            sh.set_prefix_kv(l, k, v)
+        shards.append(sh)
+    pkg.Shard.import_local_peers(shards)
+    m = O.OracleModel(cfg, canon)
+    kv = O.KVCache(cfg, L + 128)
+    for l in range(cfg.n_layers):
+        k, v = synth.gen_prefix_kv(seed + 1, l, L, cfg.n_kv_heads, cfg.head_dim)
+        kv.set_prefix(l, k, v)
+    kv.L = L
+    return shards, m, kv
+
+
+def _run(shards, tokens, parents, auto_commit=False):
+    """Launch the step on every shard on its own stream, then wait for all."""
+    import torch
+    from paper_2506_11309_b200 import swiftspec as ssp
+    T = len(tokens)
+    outs = []
+    streams = [torch.cuda.Stream() for _ in shards]
+    bufs = []
+    for sh, st in zip(shards, streams):
+        dt = torch.tensor(tokens, dtype=torch.int32, device="cuda")
+        dp = torch.tensor(parents, dtype=torch.int32, device="cuda")
+        res = torch.zeros(ssp.result_nbytes() // 4, dtype=torch.int32, device="cuda")
+        lg = torch.zeros((T, sh.v_l), dtype=torch.float32, device="cuda")
+        bufs.append((dt, dp, res, lg))
+        torch.cuda.synchronize()
+    for sh, st, (dt, dp, res, lg) in zip(shards, streams, bufs):
+        sh.verify_dev(dt, dp, T, d_result=res, d_logits=lg, auto_commit=auto_commit, stream=st)
+    torch.cuda.synchronize()
+    for (dt, dp, res, lg) in bufs:
+        outs.append((ssp.parse_result(res.cpu().numpy(), T), lg.cpu().numpy()))
+    return outs
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_fakepeer_tp_parity(P):
+    cfg = synth.CONFIGS["small-tp"]
+    L = 64
+    shards, m, kv = _setup(cfg, P, L)
+    rng = np.random.default_rng(P)
+    for kind in ("paperlike", "chain"):
+        tokens, parents = (synth.tree_paperlike if kind == "paperlike" else synth.tree_chain)(8, cfg.vocab, rng)
+        outs = _run(shards, tokens, parents)
+        ro = O.verify_sharded(cfg, m, kv, tokens, parents, P)
+        logits = np.concatenate([lg for _, lg in outs], axis=1)
+        err = np.abs(logits - ro["logits"])
+        assert np.all(err <= 2e-2 + 1e-2 * np.abs(ro["logits"])), err.max()
+        # every rank walks the same path from the same all-gathered argmax
+        res0 = outs[0][0]
+        for res, _ in outs[1:]:
+            assert res["argmax"] == res0["argmax"] and res["accepted"] == res0["accepted"]
+            assert res["bonus"] == res0["bonus"]
+        for i in range(len(tokens)):
+            a, b = res0["argmax"][i], int(ro["argmax"][i])
+            assert a == b or abs(ro["logits"][i][a] - ro["logits"][i][b]) < 2e-2
+        acc, bonus = O.accept_walk(tokens, parents, res0["argmax"])
+        assert res0["accepted"] == acc and res0["bonus"] == bonus
+        # each rank holds its own kv heads of the tree rows
+        hk = cfg.n_kv_heads // P
+        for r, sh in enumerate(shards):
+            for l in range(cfg.n_layers):
+                k, v = sh.read_kv(l, L, len(tokens))
+                np.testing.assert_allclose(k, ro["tree_k"][l][:, r * hk:(r + 1) * hk], atol=2e-2, rtol=1e-2)
+    for sh in shards:
+        sh.close()
+
+
+def test_fakepeer_tp_autocommit_many_steps():
+    """Repeated steps exercise the LL flag epochs and both all-reduce buffer
+    parities; the committed length advances identically on every rank."""
+    cfg = synth.CONFIGS["small-tp"]
+    L = 64
+    shards, m, kv = _setup(cfg, 2, L)
+    rng = np.random.default_rng(7)
+    total = 0
+    for step in range(6):
+        tokens, parents = synth.tree_random(8, cfg.vocab, rng)
+        outs = _run(shards, tokens, parents, auto_commit=True)
+        assert outs[0][0]["accepted"] == outs[1][0]["accepted"]
+        total += outs[0][0]["n_accepted"]
+        assert [sh.L for sh in shards] == [L + total] * 2
+    for sh in shards:
+        sh.close()

@@ -219,6 +219,38 @@ int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_commit);
 ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
                           float* ms, int32_t* count, void* stream);
 
+/* ---- a13: asynchronous draft -> target handoff ---------------------------
+ * P:44 / P:228-234 / Alg. 1: the draft group sends the next tree,
+ * the target group verifies it and sends back the verified tokens (or STOP),
+ * with no host round trip.  Messages are 16-byte LL lines (data1, flag1,
+ * data2, flag2; Alg. 2, R15) whose flags all equal the message
+ * sequence number (1, 2, ...; 0 is the idle value), written with one
+ * st.volatile.v4 into peer-mapped memory (NVLink) or local memory.
+ *   inbox  (owned by the target shard): line 0 = (T, seq), line 1+i =
+ *          (token_i, parent_i);
+ *   outbox (owned by the draft side):   line 1+k = (accepted[k], token),
+ *          then line 0 = (n_accepted | stop << 31, bonus_token).
+ * Sequence numbers are consecutive per shard, starting at 1. */
+
+/* Device pointer of this shard's inbox ((1 + SS_MAX_TREE) lines x 16 B, a
+ * separate cudaMalloc the draft side may map with cudaIpc). */
+ss_status ss_mailbox_inbox(ss_shard* s, void** dev_ptr);
+/* Where the verified path is posted (a device pointer valid in this shard's
+ * context, e.g. a peer-mapped draft buffer of (1 + SS_MAX_TREE) lines); only
+ * tp_rank 0 posts.  eos_token >= 0 sets the STOP bit when the bonus equals it. */
+ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eos_token);
+/* One verify step whose tree comes from the inbox (the kernels poll for
+ * message mbox_seq + 1) and whose result is posted to the outbox after the
+ * accept walk.  Asynchronous on `stream`; with auto_commit the accepted path
+ * is committed in the same launch sequence.  Errors as ss_verify_tree_dev. */
+ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream);
+/* Draft-side helpers: post a tree into an inbox / wait for a verified path in
+ * an outbox and copy it to dev_out = [n, bonus, stop, (node, token) x n]
+ * (int32, device).  Both enqueue one small kernel on `stream`. */
+ss_status ss_mailbox_post_tree(void* inbox_dev, const int32_t* tokens, const int32_t* parents, int32_t T,
+                               uint32_t seq, void* stream);
+ss_status ss_mailbox_recv_result(const void* outbox_dev, uint32_t seq, int32_t* dev_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -357,6 +357,21 @@ static int launch_d(const AttnArgs& a, int max_ctas, cudaStream_t st) {
   }
 }
 
+template <int D>
+static void warm_d() {
+  cudaFuncAttributes at;
+  cudaFuncGetAttributes(&at, attn_kernel<D, 1>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 2>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 4>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 8>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 16>);
+}
+// see warm_misc_kernels (misc.cu)
+void warm_attention_kernels() {
+  warm_d<64>();
+  warm_d<128>();
+}
+
 int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st) {
   return a.d == 64 ? launch_d<64>(a, max_ctas, st) : launch_d<128>(a, max_ctas, st);
 }

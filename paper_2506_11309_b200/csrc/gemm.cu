@@ -231,6 +231,19 @@ __device__ void accept_walk_dev(DevState* st) {
   res.n_accepted = n;
   res.status = st->status;
   st->have_verify = 1;
+  // a13: post the verified path to the draft group's outbox (Alg. 1
+  // "Send the verified tokens"; P:293 STOP at the end of generation): lines
+  // 1..n = (node index, token), then line 0 = (n | stop << 31, bonus).
+  if (st->mbox_mode) {
+    const uint32_t seq = st->mbox_cur;
+    if (st->mbox_post && st->mbox_out) {
+      for (int k = 0; k < n; ++k)
+        ll_store(st->mbox_out + 1 + k, (uint32_t)res.accepted[k], (uint32_t)st->tokens[res.accepted[k]], seq);
+      const uint32_t stop = (st->eos >= 0 && res.bonus_token == st->eos) ? 1u : 0u;
+      ll_store(st->mbox_out, (uint32_t)n | (stop << 31), (uint32_t)res.bonus_token, seq);
+    }
+    st->mbox_seq = seq;
+  }
 }
 
 // ---------------------------------------------------------------- kernel
@@ -604,6 +617,22 @@ static int launch_nt(const GemmArgs& g, int NT, int max_ctas, cudaStream_t st) {
     case 4: return launch_t<WFMT, 4, EPI>(g, max_ctas, st);
     default: return launch_t<WFMT, 8, EPI>(g, max_ctas, st);
   }
+}
+
+template <int WFMT, int EPI>
+static void warm_nt() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, gemm_kernel<WFMT, 1, EPI>);
+  cudaFuncGetAttributes(&a, gemm_kernel<WFMT, 2, EPI>);
+  cudaFuncGetAttributes(&a, gemm_kernel<WFMT, 4, EPI>);
+  cudaFuncGetAttributes(&a, gemm_kernel<WFMT, 8, EPI>);
+}
+// see warm_misc_kernels (misc.cu): load every GEMM variant before any launch
+void warm_gemm_kernels() {
+  warm_nt<0, EPI_QKV>();
+  warm_nt<0, EPI_RESID>();
+  warm_nt<0, EPI_SWIGLU>();
+  warm_nt<1, EPI_ARGMAX>();
 }
 
 int launch_gemm(const GemmArgs& g, int wfmt, int NT, int max_ctas, cudaStream_t st) {

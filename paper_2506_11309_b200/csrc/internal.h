@@ -33,6 +33,14 @@ struct DevState {
   int32_t commit_done;       // commit CTAs finished (self-resetting)
   uint32_t epoch;            // LL flag epoch of the current step (TP)
   int32_t timeout;           // set when a peer poll exceeded its budget
+  // a13 mailbox handoff (LL lines over NVLink / local memory)
+  uint32_t mbox_seq;         // last message sequence number fully handled
+  uint32_t mbox_cur;         // sequence number of the tree being verified
+  int32_t mbox_mode;         // 1 while the current step came from the inbox
+  int32_t mbox_post;         // 1 on the rank that posts the verified path
+  int32_t eos;               // STOP when the bonus token equals eos (-1: never)
+  int32_t pad1;
+  uint4* mbox_out;           // draft group's outbox (peer-mapped), nullptr = none
 };
 
 // One packed linear (W4 format, see common.cuh) or bf16 matrix.
@@ -124,6 +132,9 @@ struct ss_shard {
   float* peer_recv[ss::kMaxPeers] = {nullptr};
   bool peers_ready = false;
   bool ipc_opened[ss::kMaxPeers] = {false};
+
+  // a13 mailbox: this shard's inbox (written by the draft group)
+  uint4* mbox_in = nullptr;
 
   // graphs: key = NT*4 + auto_commit*2 + logits
   std::map<int, ss::Graph> graphs;

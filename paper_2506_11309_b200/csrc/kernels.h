@@ -84,11 +84,19 @@ struct AttnArgs {
 };
 
 int launch_gemm(const GemmArgs& g, int wfmt, int NT, int max_ctas, cudaStream_t st);
+// force-load every kernel (lazy module loading vs cross-kernel flag waits)
+void warm_gemm_kernels();
+void warm_attention_kernels();
+void warm_misc_kernels();
 int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st);
 
 // embed + tree metadata (a0, a1) + first RMSNorm into the frag activation
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
-                       cudaStream_t st);
+                       cudaStream_t st, bool from_mailbox = false);
+// a13 mailbox helpers for the draft side (and tests)
+void launch_mailbox_post(void* inbox, const int32_t* tokens, const int32_t* parents, int T, uint32_t seq,
+                         cudaStream_t st);
+void launch_mailbox_recv(const void* outbox, uint32_t seq, int32_t* dev_out, cudaStream_t st);
 // RMSNorm of the residual into frag activations (a2 / a7 / final)
 void launch_prep_norm(ss_shard* s, const uint16_t* gain, int NT, int split, cudaStream_t st);
 // KV compaction + commit (a12); chain from the device result or commit list

@@ -29,21 +29,53 @@ SS_DEV float block_sum_256(float v, float* s_red) {
   return r;
 }
 
+// a13 inbox poll: spin on one LL line until its flag equals seq (bounded).
+SS_DEV bool ll_wait(const uint4* line, uint32_t seq, uint32_t& d1, uint32_t& d2) {
+  for (long spins = 0; spins < (1L << 26); ++spins)
+    if (ll_try_load(line, seq, d1, d2)) return true;
+  return false;
+}
+
 __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int32_t* tokens,
                                                          const int32_t* parents, int T_in, const uint16_t* E,
                                                          int V, int h, float* x, const uint16_t* gain,
-                                                         uint8_t* act, int NT, float eps, int epoch_stride) {
+                                                         uint8_t* act, int NT, float eps, int epoch_stride,
+                                                         const uint4* mbox_in) {
   __shared__ int s_tok[SS_MAX_TREE], s_par[SS_MAX_TREE];
   __shared__ int s_bad;
+  __shared__ int s_T;
   __shared__ float s_red[8];
   pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
+  // a13: the tree arrives in the inbox as LL lines ("sends a
+  // sub-graph ... to the target worker"): line 0 = (T, seq), line 1+i =
+  // (token_i, parent_i), every line flagged with the message sequence number.
+  uint32_t mtok = 0, mpar = 0;
+  if (mbox_in) {
+    const uint32_t seq = st->mbox_seq + 1;
+    if (tid == 0) {
+      uint32_t d1 = 0, d2 = 0;
+      s_T = ll_wait(mbox_in, seq, d1, d2) ? (int)d1 : 0;
+      if (blockIdx.x == 0 && blockIdx.y == 0) {
+        st->mbox_cur = seq;
+        st->mbox_mode = 1;
+        if (s_T == 0) st->timeout = 1;
+      }
+    }
+    __syncthreads();
+    T_in = s_T;
+    if (tid < min(max(T_in, 0), SS_MAX_TREE)) {
+      if (!ll_wait(mbox_in + 1 + tid, seq, mtok, mpar)) { mtok = 0; mpar = 0; }
+    }
+  } else if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    st->mbox_mode = 0;
+  }
   const int T = min(max(T_in, 1), SS_MAX_TREE);
   if (tid == 0) s_bad = (T_in < 1 || T_in > SS_MAX_TREE) ? 1 : 0;
   __syncthreads();
   if (tid < T) {
-    int p = parents[tid], tk = tokens[tid];
+    int p = mbox_in ? (int)mpar : parents[tid], tk = mbox_in ? (int)mtok : tokens[tid];
     bool bad = (tid == 0) ? (p != -1) : (p < 0 || p >= tid);
     bad = bad || tk < 0 || tk >= V;
     if (bad) atomicOr(&s_bad, 1);
@@ -131,11 +163,56 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
 }
 
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool from_mailbox) {
   const uint16_t* g0 = s->layers[0].attn_norm;
   launch_pdl(embed_meta_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, s->dstate, tokens, parents, T,
              (const uint16_t*)s->embed, s->cfg.vocab, s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
-             2 * s->cfg.n_layers + 2);
+             2 * s->cfg.n_layers + 2, from_mailbox ? (const uint4*)s->mbox_in : (const uint4*)nullptr);
+}
+
+// ---------------------------------------------------------------- a13 draft-side helpers
+// Post one tree into a target inbox as LL lines (the draft group's send,
+// Alg. 1 P:286 "Send it to the target worker to verify").
+struct MboxTree {
+  int32_t tokens[SS_MAX_TREE];
+  int32_t parents[SS_MAX_TREE];
+};
+__global__ void mailbox_post_kernel(uint4* inbox, MboxTree tree, int T, uint32_t seq) {
+  const int i = threadIdx.x;
+  if (i < T) ll_store(inbox + 1 + i, (uint32_t)tree.tokens[i], (uint32_t)tree.parents[i], seq);
+  if (i == 0) ll_store(inbox, (uint32_t)T, seq, seq);
+}
+void launch_mailbox_post(void* inbox, const int32_t* tokens, const int32_t* parents, int T, uint32_t seq,
+                         cudaStream_t st) {
+  MboxTree t{};
+  for (int i = 0; i < T && i < SS_MAX_TREE; ++i) {
+    t.tokens[i] = tokens[i];
+    t.parents[i] = parents[i];
+  }
+  mailbox_post_kernel<<<1, SS_MAX_TREE, 0, st>>>((uint4*)inbox, t, T, seq);
+}
+// Wait for the verified path with sequence number seq in an outbox and copy
+// it out: out[0] = n_accepted, out[1] = bonus, out[2] = stop, then n
+// (node index, token) pairs.
+__global__ void mailbox_recv_kernel(const uint4* outbox, uint32_t seq, int32_t* out) {
+  __shared__ int s_n;
+  uint32_t d1 = 0, d2 = 0;
+  if (threadIdx.x == 0) {
+    const bool ok = ll_wait(outbox, seq, d1, d2);
+    s_n = ok ? (int)(d1 & 0x7FFFFFFFu) : -1;
+    out[0] = s_n;
+    out[1] = (int)d2;
+    out[2] = (int)(d1 >> 31);
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i < s_n && ll_wait(outbox + 1 + i, seq, d1, d2)) {
+    out[3 + 2 * i] = (int)d1;
+    out[4 + 2 * i] = (int)d2;
+  }
+}
+void launch_mailbox_recv(const void* outbox, uint32_t seq, int32_t* dev_out, cudaStream_t st) {
+  mailbox_recv_kernel<<<1, SS_MAX_TREE, 0, st>>>((const uint4*)outbox, seq, dev_out);
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -485,4 +562,19 @@ void launch_synth_kv_key(uint16_t* cache, int layer, int Hkv_full, int Hkv_l, in
   synth_kv_kernel<<<148 * 8, 256, 0, st>>>(cache, layer, Hkv_full, Hkv_l, kv0, d, L, max_ctx_pad, key);
 }
 
+}  // namespace ss
+
+namespace ss {
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first
+// launch, which can wait for running kernels: a producer whose kernel is
+// loaded only after a consumer already spins on its flags would deadlock.
+// Every kernel that takes part in a cross-kernel wait is loaded up front.
+void warm_misc_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, embed_meta_kernel);
+  cudaFuncGetAttributes(&a, prep_norm_kernel);
+  cudaFuncGetAttributes(&a, commit_kernel);
+  cudaFuncGetAttributes(&a, mailbox_post_kernel);
+  cudaFuncGetAttributes(&a, mailbox_recv_kernel);
+}
 }  // namespace ss

@@ -242,6 +242,9 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   if (G * nt_of(c.max_tree) * 8 > 512) FAIL(SS_EINVAL, "(n_heads/n_kv_heads) * max_tree too large (<= 512 rows)");
 
   CUDA_TRY(cudaSetDevice(device));
+  warm_gemm_kernels();
+  warm_attention_kernels();
+  warm_misc_kernels();
   ss_shard* s = new ss_shard();
   s->cfg = c;
   s->rank = tp_rank;
@@ -334,12 +337,15 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   {
     DevState init{};
     init.epoch = 1;
+    init.eos = -1;
+    init.mbox_post = tp_rank == 0 ? 1 : 0;
     if (cudaMemcpy(s->dstate, &init, sizeof(DevState), cudaMemcpyHostToDevice) != cudaSuccess) {
       g_err = "init state copy failed";
       return fail(SS_ECUDA);
     }
   }
   // LL receive buffer: [P][n_tg_total][128 rows][32 lines] x 16 B (fp32 pairs + flags)
+  A(s->mbox_in, (size_t)(1 + SS_MAX_TREE) * 16);
   if (tp_size > 1) {
     s->recv_bytes = ((size_t)2 * tp_size * (h / 128) * 128 * 32 + (size_t)tp_size * 64) * 16;
     A(s->recv, s->recv_bytes);
@@ -371,7 +377,7 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
     if (s->ipc_opened[p] && s->peer_recv[p]) cudaIpcCloseMemHandle(s->peer_recv[p]);
   void* ptrs[] = {s->embed, s->final_norm, s->lm_head.d, s->kcache, s->vcache, s->rope_cs, s->x, s->act_h,
                   s->act_o, s->act_d, s->act_lm, s->qbuf, s->attn_ws, s->attn_ml, s->attn_bar, s->logits_dev, s->dstate,
-                  s->d_tree_in, s->recv, s->sc_qkv.accum, s->sc_qkv.counters, s->sc_o.accum, s->sc_o.counters,
+                  s->d_tree_in, s->recv, s->mbox_in, s->sc_qkv.accum, s->sc_qkv.counters, s->sc_o.accum, s->sc_o.counters,
                   s->sc_gu.accum, s->sc_gu.counters, s->sc_down.accum, s->sc_down.counters, s->sc_lm.accum,
                   s->sc_lm.counters};
   for (void* p : ptrs)
@@ -855,12 +861,12 @@ static ss_status check_ready(ss_shard* s, int T) {
 }
 
 static ss_status run_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int T, int auto_commit,
-                          int want_logits, cudaStream_t st) {
+                          int want_logits, cudaStream_t st, bool from_mailbox = false) {
   const int NT = nt_of(T);
   Graph* gr;
   ss_status r = get_graph(s, NT, auto_commit, want_logits, &gr);
   if (r != SS_OK) return r;
-  launch_embed_meta(s, d_tokens, d_parents, T, NT, st);
+  launch_embed_meta(s, d_tokens, d_parents, T, NT, st, from_mailbox);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaGraphLaunch(gr->exec, st));
   s->last_T = T;
@@ -1065,5 +1071,60 @@ extern "C" ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const
   s->L_known = false;
   s->L_upper += T;
   s->have_verify = false;
+  return SS_OK;
+}
+
+// ------------------------------------------------------------ a13 mailbox
+extern "C" ss_status ss_mailbox_inbox(ss_shard* s, void** dev_ptr) {
+  if (!s || !dev_ptr) FAIL(SS_EINVAL, "null argument");
+  *dev_ptr = s->mbox_in;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eos_token) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  uint4* p = (uint4*)outbox_dev;
+  CUDA_TRY(cudaMemcpy(&s->dstate->mbox_out, &p, sizeof(p), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(&s->dstate->eos, &eos_token, 4, cudaMemcpyHostToDevice));
+  return SS_OK;
+}
+
+extern "C" ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream) {
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  cudaSetDevice(s->device);
+  const int T = s->cfg.max_tree;  // the tree size arrives with the message
+  ss_status r = check_ready(s, T);
+  if (r != SS_OK) return r;
+  cudaStream_t st = (cudaStream_t)stream;
+  r = run_step(s, nullptr, nullptr, T, auto_commit ? 1 : 0, 0, st, true);
+  if (r != SS_OK) return r;
+  if (auto_commit) {
+    s->L_known = false;
+    s->L_upper += T;
+    s->have_verify = false;
+  } else {
+    s->have_verify = true;
+    s->last_T = T;
+  }
+  return SS_OK;
+}
+
+extern "C" ss_status ss_mailbox_post_tree(void* inbox_dev, const int32_t* tokens, const int32_t* parents, int32_t T,
+                                          uint32_t seq, void* stream) {
+  if (!inbox_dev || !tokens || !parents) FAIL(SS_EINVAL, "null argument");
+  if (T < 1 || T > SS_MAX_TREE) FAIL(SS_EINVAL, "T out of [1, 64]");
+  if (seq == 0) FAIL(SS_EINVAL, "sequence number 0 is reserved (idle lines)");
+  launch_mailbox_post(inbox_dev, tokens, parents, T, seq, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+extern "C" ss_status ss_mailbox_recv_result(const void* outbox_dev, uint32_t seq, int32_t* dev_out, void* stream) {
+  if (!outbox_dev || !dev_out) FAIL(SS_EINVAL, "null argument");
+  if (seq == 0) FAIL(SS_EINVAL, "sequence number 0 is reserved (idle lines)");
+  launch_mailbox_recv(outbox_dev, seq, dev_out, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }

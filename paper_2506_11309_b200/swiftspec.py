@@ -47,7 +47,8 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_set_launch_cap", "ss_destroy", "ss_last_error", "ss_load_weights", "ss_synth_weights",
            "ss_set_prefix_kv", "ss_synth_prefix_kv", "ss_read_kv", "ss_set_committed_len",
            "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
-           "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step"]
+           "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
+           "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result"]
 
 
 def lib():
@@ -81,6 +82,11 @@ def lib():
         "ss_commit_accepted": (i32, [vp, vp]),
         "ss_kernels_per_step": (i32, [vp, i32, i32]),
         "ss_profile_step": (i32, [vp, vp, vp, i32, vp, vp, vp]),
+        "ss_mailbox_inbox": (i32, [vp, C.POINTER(vp)]),
+        "ss_attach_mailbox": (i32, [vp, vp, i32]),
+        "ss_verify_tree_mailbox": (i32, [vp, i32, vp]),
+        "ss_mailbox_post_tree": (i32, [vp, vp, vp, i32, C.c_uint32, vp]),
+        "ss_mailbox_recv_result": (i32, [vp, C.c_uint32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -127,7 +133,10 @@ class Shard:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().ss_destroy(self.h)
+            try:
+                lib().ss_destroy(self.h)
+            except TypeError:  # interpreter shutdown: ctypes already torn down
+                pass
             self.h = None
 
     __del__ = close
@@ -224,6 +233,18 @@ class Shard:
                                      _stream_handle(stream)))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PROF_KINDS)}
 
+    # ---- a13 mailbox handoff
+    def mailbox_inbox(self) -> int:
+        ptr = C.c_void_p()
+        _check(lib().ss_mailbox_inbox(self.h, C.byref(ptr)))
+        return ptr.value
+
+    def attach_mailbox(self, outbox_ptr: int, eos: int = -1):
+        _check(lib().ss_attach_mailbox(self.h, outbox_ptr, eos))
+
+    def verify_mailbox(self, auto_commit: bool = True, stream=None):
+        _check(lib().ss_verify_tree_mailbox(self.h, 1 if auto_commit else 0, _stream_handle(stream)))
+
     # ---- tensor parallel peers
     def export_handle(self) -> bytes:
         buf = C.create_string_buffer(4096)
@@ -260,3 +281,13 @@ def parse_result(buf: np.ndarray, T: int) -> dict:
     return dict(n_accepted=n, accepted=[int(x) for x in a[1:1 + n]], bonus=int(a[1 + SS_MAX_TREE]),
                 argmax=[int(x) for x in a[2 + SS_MAX_TREE:2 + SS_MAX_TREE + T]],
                 status=int(a[2 + 2 * SS_MAX_TREE]))
+
+
+def mailbox_post_tree(inbox_ptr: int, tokens, parents, seq: int, stream=None):
+    t = np.ascontiguousarray(tokens, dtype=np.int32)
+    p = np.ascontiguousarray(parents, dtype=np.int32)
+    _check(lib().ss_mailbox_post_tree(inbox_ptr, _ptr(t), _ptr(p), len(t), seq, _stream_handle(stream)))
+
+
+def mailbox_recv_result(outbox_ptr: int, seq: int, dev_out_ptr: int, stream=None):
+    _check(lib().ss_mailbox_recv_result(outbox_ptr, seq, dev_out_ptr, _stream_handle(stream)))

@@ -15,8 +15,10 @@ namespace ss {
 // ---------------------------------------------------------------- layouts
 // W4 unit (tile-group of 128 output rows x one K-stage of 256):
 //   [warp 0..7][kblock 0..3][lane 0..31][4 x u32 nibble words] = 16384 B
-//   [warp][group 0..1][16 bf16 scales]                          =   512 B
-//   [warp][group 0..1][16 int4 zeros packed in 8 B]             =   128 B
+//   [warp][group 0..1][gq 0..7] bf16x2 (s[gq], s[gq+8])         =   512 B
+//   [warp][group 0..1][gq 0..7] byte   z[gq] | z[gq+8] << 4      =   128 B
+// (gq = lane / 4: one 32-bit and one 8-bit shared load give a lane the
+// scales and zeros of both of its rows)
 // BF16 unit (LM head; 128 rows x K-stage of 64):
 //   [warp][k16 step 0..3][lane][4 x u32 bf16x2]                 = 16384 B
 constexpr int kTG = 128;             // rows per tile-group (8 warps x 16)

@@ -107,11 +107,19 @@ __device__ void epi_swiglu(const EpiArgs& e, int tg, const float* acc, int T) {
 }
 
 template <int NT>
-__device__ void epi_resid_local(const EpiArgs& e, int tg, const float* acc, int T) {
+__device__ void epi_resid_local(const EpiArgs& e, int tg, const float* acc, int T, float* ss) {
   const int TP = NT * 8;
+  // warp = 32 columns of one token: the new residual's squares reduce per
+  // warp into the per-token sum the fused RMSNorm needs
   for (int idx = threadIdx.x; idx < 128 * T; idx += 256) {
-    int t = idx >> 7, r = idx & 127;
-    e.x[(size_t)t * e.h + tg * 128 + r] += __ldcg(acc + (size_t)r * TP + t);
+    const int t = idx >> 7, r = idx & 127;
+    float* xp = e.x + (size_t)t * e.h + tg * 128 + r;
+    const float nx = *xp + __ldcg(acc + (size_t)r * TP + t);
+    *xp = nx;
+    if (ss) {
+      const float q = warp_sum(nx * nx);
+      if ((threadIdx.x & 31) == 0) atomicAdd(ss + t, q);
+    }
   }
 }
 
@@ -136,11 +144,11 @@ __device__ void epi_ar_send(const EpiArgs& e, int tg, const float* acc, int T) {
 // tp > 1, phase 2 (after the CTA's compute loop): wait for every rank's
 // partial of the tile-group, sum in rank order (identical on all ranks), add.
 template <int NT>
-__device__ void epi_ar_recv(const EpiArgs& e, int tg, int T) {
+__device__ void epi_ar_recv(const EpiArgs& e, int tg, int T, float* ss) {
   const uint32_t flag = e.st->epoch + e.ar_seq;
   const int pairs = (T + 1) >> 1;
   for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
-    int r = idx / pairs, tp = idx - r * pairs;
+    const int tp = idx >> 7, r = idx & 127;  // warp = 32 rows of one token pair
     float s0 = 0.f, s1 = 0.f;
     for (int p = 0; p < e.P; ++p) {
       const uint4* src = reinterpret_cast<const uint4*>(e.recv) +
@@ -153,9 +161,57 @@ __device__ void epi_ar_recv(const EpiArgs& e, int tg, int T) {
       s0 += __uint_as_float(d1);
       s1 += __uint_as_float(d2);
     }
-    int t0 = 2 * tp;
-    e.x[(size_t)t0 * e.h + tg * 128 + r] += s0;
-    if (t0 + 1 < T) e.x[(size_t)(t0 + 1) * e.h + tg * 128 + r] += s1;
+    const int t0 = 2 * tp;
+    float* x0 = e.x + (size_t)t0 * e.h + tg * 128 + r;
+    const float n0 = *x0 + s0;
+    *x0 = n0;
+    float n1 = 0.f;
+    if (t0 + 1 < T) {
+      float* x1 = x0 + e.h;
+      n1 = *x1 + s1;
+      *x1 = n1;
+    }
+    if (ss) {
+      const float q0 = warp_sum(n0 * n0), q1 = warp_sum(n1 * n1);
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(ss + t0, q0);
+        if (t0 + 1 < T) atomicAdd(ss + t0 + 1, q1);
+      }
+    }
+  }
+}
+
+// Fused RMSNorm of the updated residual (R5) into the next GEMM's input,
+// after every tile-group of this launch has been added (grid barrier): each
+// warp normalises one (token, 128-group) item -- fp16 fragments + group sum X
+// for a W4 GEMM, or bf16 hi/lo fragments for the LM head (split).
+template <int NT>
+__device__ void norm_slice(const GemmArgs& g, int T, int ncw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = g.epi.h, ngr = h / 128;
+  for (int it = blockIdx.x + gridDim.x * warp; it < T * ngr; it += gridDim.x * ncw) {
+    const int t = it / ngr, grp = it - t * ngr;
+    const int k = grp * 128 + lane * 4;
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(g.epi.x + (size_t)t * h + k));
+    const uint2 gw = *reinterpret_cast<const uint2*>(g.norm_gain + k);
+    const float r = rsqrtf(__ldcg(g.ss + t) / (float)h + g.eps);
+    const float a0 = v.x * r * bf16_lo(gw.x), a1 = v.y * r * bf16_hi(gw.x);
+    const float a2 = v.z * r * bf16_lo(gw.y), a3 = v.w * r * bf16_hi(gw.y);
+    if (!g.norm_split) {
+      const uint32_t p01 = pack_half2(a0, a1), p23 = pack_half2(a2, a3);
+      *reinterpret_cast<uint32_t*>(g.norm_out + act_frag_offset(t, k, NT)) = p01;
+      *reinterpret_cast<uint32_t*>(g.norm_out + act_frag_offset(t, k + 2, NT)) = p23;
+      const float xs = warp_sum(half2_sum(p01) + half2_sum(p23));
+      if (lane == 0) *reinterpret_cast<float*>(g.norm_out + act_xsum_offset(t, grp, NT)) = xs;
+    } else {
+      uint32_t h01 = pack_bf16x2(a0, a1), h23 = pack_bf16x2(a2, a3);
+      *reinterpret_cast<uint32_t*>(g.norm_out + frag_offset(t, k, 2 * NT)) = h01;
+      *reinterpret_cast<uint32_t*>(g.norm_out + frag_offset(t, k + 2, 2 * NT)) = h23;
+      *reinterpret_cast<uint32_t*>(g.norm_out + frag_offset(t + 8 * NT, k, 2 * NT)) =
+          pack_bf16x2(a0 - bf16_lo(h01), a1 - bf16_hi(h01));
+      *reinterpret_cast<uint32_t*>(g.norm_out + frag_offset(t + 8 * NT, k + 2, 2 * NT)) =
+          pack_bf16x2(a2 - bf16_lo(h23), a3 - bf16_hi(h23));
+    }
   }
 }
 
@@ -365,7 +421,11 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
         }
         uint8_t* dst = smem + s * C::UBYTES;
         mbar_expect_tx(&full[s], C::UBYTES);
+#ifdef SS_EXP_L2W
+        bulk_g2s(dst, g.W + (size_t)(u % 64) * C::WBYTES, C::WBYTES, &full[s], pol);
+#else
         bulk_g2s(dst, g.W + (size_t)u * C::WBYTES, C::WBYTES, &full[s], pol);
+#endif
         if (waited) bulk_g2s_nohint(dst + C::WBYTES, g.act + (size_t)uks * C::ABYTES, C::ABYTES, &full[s]);
         else pre_u[npre++] = uks;
         if (++s == C::STAGES) { s = 0; ph ^= 1; }
@@ -422,8 +482,8 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
         //   rows g+8: s/16 * (acc - (1024 + 16 z) X)    = s * sum (q - z) x
         // exact integer weights, no per-weight subtract (R3, DESIGN "W4 GEMM").
         const uint4* wl = reinterpret_cast<const uint4*>(stw) + tile * 128;
-        const uint16_t* sc = reinterpret_cast<const uint16_t*>(stw + kW4Bytes) + tile * 32;
-        const uint2* zp = reinterpret_cast<const uint2*>(stw + kW4Bytes + 512) + tile * 2;
+        const uint32_t* sc = reinterpret_cast<const uint32_t*>(stw + kW4Bytes) + tile * 16;  // [grp][gq]
+        const uint8_t* zp = stw + kW4Bytes + 512 + tile * 16;                                  // [grp][gq]
         const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
         const float* xs = reinterpret_cast<const float*>(stw + C::WBYTES + NT * 4096);
 #pragma unroll
@@ -455,13 +515,13 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
               mma_f16_16816(cg[js % C::NACC][n], a, js ? bb[n].z : bb[n].x, js ? bb[n].w : bb[n].y);
           }
         }
-        const uint2 zz = zp[grp];
-        const uint64_t z64 = ((uint64_t)zz.y << 32) | zz.x;
-        const float z0 = (float)((uint32_t)(z64 >> (4 * gq)) & 15u);
-        const float z8 = (float)((uint32_t)(z64 >> (4 * (gq + 8))) & 15u);
-        const float c0 = 1024.f + z0, c8 = 1024.f + 16.f * z8;
-        const float s0 = bf16_bits_to_f32(sc[grp * 16 + gq]);
-        const float s8 = bf16_bits_to_f32(sc[grp * 16 + gq + 8]) * 0.0625f;
+        // c0 = 1024 + z, c8 = 1024 + 16 z built directly as fp32 bits (1024 = 0x44800000,
+        // one ulp = 2^-13 there); scales are the bf16 halves of one word
+        const uint32_t zb = zp[grp * 8 + gq], sp = sc[grp * 8 + gq];
+        const float c0 = __uint_as_float(0x44800000u | ((zb & 15u) << 13));
+        const float c8 = __uint_as_float(0x44800000u | ((zb >> 4) << 17));
+        const float s0 = __uint_as_float(sp << 16);
+        const float s8 = __uint_as_float(sp & 0xFFFF0000u) * 0.0625f;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const float2 X = *reinterpret_cast<const float2*>(xs + grp * 8 * NT + n * 8 + 2 * tq);
@@ -539,7 +599,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
       else if constexpr (EPI == EPI_SWIGLU) epi_swiglu<NT>(g.epi, tg, accp, T);
       else if constexpr (EPI == EPI_ARGMAX) epi_argmax<NT>(g.epi, tg, accp, T);
       else {
-        if (g.epi.P == 1) epi_resid_local<NT>(g.epi, tg, accp, T);
+        if (g.epi.P == 1) epi_resid_local<NT>(g.epi, tg, accp, T, g.norm_out ? g.ss : nullptr);
         else epi_ar_send<NT>(g.epi, tg, accp, T);
       }
     }
@@ -563,20 +623,36 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
     }
   }
   TS(5);
-  // last CTA out resets the work queue for the next launch
+  if constexpr (EPI == EPI_RESID) {
+    if (g.epi.P > 1) {  // all sends are out: now wait for the peers' partials
+      named_bar_sync(1, NCT);
+      if (threadIdx.x < 256)
+        for (int i = 0; i < ndone; ++i) epi_ar_recv<NT>(g.epi, s_done_list[i], T, g.norm_out ? g.ss : nullptr);
+    }
+    if (g.norm_out) {  // fused RMSNorm: wait for every CTA's residual updates
+      named_bar_sync(1, NCT);
+      if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();
+        atomicAdd(&g.nbar[0], 1);
+        while (*reinterpret_cast<volatile int*>(&g.nbar[0]) < (int)gridDim.x) {
+        }
+        fence_acq_rel_gpu();
+      }
+      named_bar_sync(1, NCT);
+      norm_slice<NT>(g, T, NCW);
+    }
+  }
+  // last CTA out resets the work queue (and the norm barrier / sums)
   named_bar_sync(1, NCT);
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
     if (atomicAdd(&queue[1], 1) == (int)gridDim.x - 1) {
       queue[0] = 0;
       queue[1] = 0;
-    }
-  }
-  if constexpr (EPI == EPI_RESID) {
-    if (g.epi.P > 1) {  // all sends are out: now wait for the peers' partials
-      named_bar_sync(1, NCT);
-      if (threadIdx.x < 256)
-        for (int i = 0; i < ndone; ++i) epi_ar_recv<NT>(g.epi, s_done_list[i], T);
+      if (g.norm_out) {
+        g.nbar[0] = 0;
+        for (int t = 0; t < SS_MAX_TREE; ++t) g.ss[t] = 0.f;
+      }
     }
   }
 }

@@ -66,7 +66,9 @@ struct CanonLinear {
 
 struct GemmScratch {
   float* accum = nullptr;    // [n_tg*128][8*NT_max] fp32, self-zeroing
-  int* counters = nullptr;   // [n_tg]
+  int* counters = nullptr;   // [n_tg + 2]
+  float* ss = nullptr;       // [64] fused-norm sums of squares
+  int* nbar = nullptr;       // fused-norm grid barrier
   size_t accum_elems = 0;
 };
 

@@ -67,6 +67,14 @@ struct GemmArgs {
   // later kernel fills with atomics (attention -> O input, SwiGLU -> down input)
   uint8_t* zero_x = nullptr;
   int zero_x_stages = 0, zero_x_nt = 1;
+  // optional fused RMSNorm of the updated residual (EPI_RESID): output into
+  // norm_out (fp16 + X, or bf16 hi/lo for the LM head when norm_split)
+  const uint16_t* norm_gain = nullptr;
+  uint8_t* norm_out = nullptr;
+  int norm_split = 0;
+  float eps = 1e-5f;
+  float* ss = nullptr;       // [64] per-token sum of squares (self-cleaning)
+  int* nbar = nullptr;       // grid barrier counter (self-cleaning)
   EpiArgs epi;
 };
 

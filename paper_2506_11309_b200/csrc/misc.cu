@@ -455,37 +455,35 @@ __global__ void synth_linear_kernel(uint8_t* dst, SynthLinArgs a) {
       }
       reinterpret_cast<uint32_t*>(ub)[w_in] = word;
     } else {
-      // metadata: 32 slots per unit = 8 warps x 2 groups x (16 scales + 16 zeros)
+      // metadata: 32 slots per unit = 8 warps x 2 groups x (scales, zeros),
+      // stored as lane-indexed (row gq, row gq+8) pairs (common.cuh)
       int slot = w_in - (int)words_per_unit;
       int warp = slot >> 2, grp = (slot >> 1) & 1, which = slot & 1;
       int g = s * 2 + grp;
-      if (which == 0) {
-        uint16_t* sc = reinterpret_cast<uint16_t*>(ub + kW4Bytes) + warp * 32 + grp * 16;
-        for (int i2 = 0; i2 < 16; ++i2) {
-          int row = tg * 128 + warp * 16 + i2;
-          int part, n, kk;
-          float sv = 0.f;
-          if (lin_map(a.m, row, g * 128, part, n, kk)) {
-            int gg = kk / 128;
+      uint16_t sv[16];
+      uint32_t zv[16];
+      for (int i2 = 0; i2 < 16; ++i2) {
+        int row = tg * 128 + warp * 16 + i2;
+        int part, n, kk;
+        sv[i2] = 0;
+        zv[i2] = 8;
+        if (lin_map(a.m, row, g * 128, part, n, kk)) {
+          int gg = kk / 128;
+          if (which == 0) {
             uint64_t hs = hash_u64(a.keys[part][2], (uint64_t)gg * a.N_full[part] + n);
             float u = __fmul_rn((float)(uint32_t)((hs >> 41) + (1u << 22)), 1.1920928955078125e-07f);
-            sv = __fmul_rn(u, a.scale_c[part]);
+            sv[i2] = bf16_rne_bits(__fmul_rn(u, a.scale_c[part]));
+          } else {
+            zv[i2] = 6u + (uint32_t)(hash_u64(a.keys[part][1], (uint64_t)gg * a.N_full[part] + n) & 3u);
           }
-          sc[i2] = bf16_rne_bits(sv);
         }
+      }
+      if (which == 0) {
+        uint32_t* sc = reinterpret_cast<uint32_t*>(ub + kW4Bytes) + (warp * 2 + grp) * 8;
+        for (int gq = 0; gq < 8; ++gq) sc[gq] = (uint32_t)sv[gq] | ((uint32_t)sv[gq + 8] << 16);
       } else {
-        uint64_t zw = 0;
-        for (int i2 = 0; i2 < 16; ++i2) {
-          int row = tg * 128 + warp * 16 + i2;
-          int part, n, kk;
-          uint32_t zv = 8;
-          if (lin_map(a.m, row, g * 128, part, n, kk)) {
-            int gg = kk / 128;
-            zv = 6u + (uint32_t)(hash_u64(a.keys[part][1], (uint64_t)gg * a.N_full[part] + n) & 3u);
-          }
-          zw |= (uint64_t)zv << (4 * i2);
-        }
-        reinterpret_cast<uint64_t*>(ub + kW4Bytes + 512)[warp * 2 + grp] = zw;
+        uint8_t* zb = ub + kW4Bytes + 512 + (warp * 2 + grp) * 8;
+        for (int gq = 0; gq < 8; ++gq) zb[gq] = (uint8_t)(zv[gq] | (zv[gq + 8] << 4));
       }
     }
   }

@@ -177,22 +177,26 @@ static void pack_w4_host(const PackedLinear& pl, const LinMap& m, const CanonLin
             }
       for (int warp = 0; warp < 8; ++warp)
         for (int grp = 0; grp < 2; ++grp) {
-          uint16_t* sc = reinterpret_cast<uint16_t*>(ub + kW4Bytes) + warp * 32 + grp * 16;
-          uint64_t zw = 0;
+          uint16_t sv[16];
+          uint32_t zv[16];
           for (int i = 0; i < 16; ++i) {
             int row = tg * 128 + warp * 16 + i;
             int part, n, kk;
-            uint16_t sv = 0;
-            uint32_t zv = 8;
+            sv[i] = 0;
+            zv[i] = 8;
             if (lin_map_h(m, row, (s * 2 + grp) * 128, part, n, kk)) {
               size_t gi = (size_t)(kk / 128) * Nfull[part] + n;
-              sv = parts[part]->s[gi];
-              zv = parts[part]->z[gi] & 15u;
+              sv[i] = parts[part]->s[gi];
+              zv[i] = parts[part]->z[gi] & 15u;
             }
-            sc[i] = sv;
-            zw |= (uint64_t)zv << (4 * i);
           }
-          reinterpret_cast<uint64_t*>(ub + kW4Bytes + 512)[warp * 2 + grp] = zw;
+          // lane-indexed pairs (rows gq, gq+8): see common.cuh
+          uint32_t* sc = reinterpret_cast<uint32_t*>(ub + kW4Bytes) + (warp * 2 + grp) * 8;
+          uint8_t* zb = ub + kW4Bytes + 512 + (warp * 2 + grp) * 8;
+          for (int gq = 0; gq < 8; ++gq) {
+            sc[gq] = (uint32_t)sv[gq] | ((uint32_t)sv[gq + 8] << 16);
+            zb[gq] = (uint8_t)(zv[gq] | (zv[gq + 8] << 4));
+          }
         }
     }
 }
@@ -318,6 +322,8 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
     g.accum_elems = (size_t)n_tg * 128 * 64;
     if (dalloc(&g.accum, g.accum_elems * 4) != cudaSuccess) return false;
     if (dalloc(&g.counters, (size_t)(n_tg + 2) * 4) != cudaSuccess) return false;
+    if (dalloc(&g.ss, (size_t)SS_MAX_TREE * 4) != cudaSuccess) return false;
+    if (dalloc(&g.nbar, 16) != cudaSuccess) return false;
     return true;
   };
   if (!mk_scratch(s->sc_qkv, s->layers[0].qkv.n_tg) || !mk_scratch(s->sc_o, s->layers[0].o.n_tg) ||
@@ -379,7 +385,7 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
                   s->act_o, s->act_d, s->act_lm, s->qbuf, s->attn_ws, s->attn_ml, s->attn_bar, s->logits_dev, s->dstate,
                   s->d_tree_in, s->recv, s->mbox_in, s->sc_qkv.accum, s->sc_qkv.counters, s->sc_o.accum, s->sc_o.counters,
                   s->sc_gu.accum, s->sc_gu.counters, s->sc_down.accum, s->sc_down.counters, s->sc_lm.accum,
-                  s->sc_lm.counters};
+                  s->sc_lm.counters, s->sc_o.ss, s->sc_o.nbar, s->sc_down.ss, s->sc_down.nbar};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->hstate) cudaFreeHost(s->hstate);
@@ -691,6 +697,9 @@ static GemmArgs gemm_args(ss_shard* s, const PackedLinear& pl, const uint8_t* ac
   g.S = pl.S;
   g.accum = sc.accum;
   g.counters = sc.counters;
+  g.ss = sc.ss;
+  g.nbar = sc.nbar;
+  g.eps = s->cfg.rms_eps;
   g.n_sm = s->n_sm;
   EpiArgs& e = g.epi;
   e.kind = kind;
@@ -779,27 +788,25 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.zero_x = s->act_d;  // the SwiGLU epilogue accumulates the down-input group sums
     g.zero_x_stages = lw.down.S;
     g.zero_x_nt = NT;
+    g.norm_gain = lw.mlp_norm;  // a7 fused: RMSNorm into the gate/up input
+    g.norm_out = s->act_h;
+    g.norm_split = 0;
     PROF_BEGIN(3);
     n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
-    PROF_BEGIN(4);
-    launch_prep_norm(s, lw.mlp_norm, NT, 0, st);
-    PROF_END();
-    ++n;
     g = gemm_args(s, lw.gu, s->act_h, s->sc_gu, EPI_SWIGLU, l);
     PROF_BEGIN(5);
     n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     g = gemm_args(s, lw.down, s->act_d, s->sc_down, EPI_RESID, l);
     g.epi.ar_seq = 2 * l + 1;
+    // a2 of the next layer (or the final norm before the LM head) fused
+    g.norm_gain = l + 1 < c.n_layers ? s->layers[l + 1].attn_norm : s->final_norm;
+    g.norm_out = l + 1 < c.n_layers ? s->act_h : s->act_lm;
+    g.norm_split = l + 1 < c.n_layers ? 0 : 1;
     PROF_BEGIN(6);
     n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
-    PROF_BEGIN(4);
-    launch_prep_norm(s, l + 1 < c.n_layers ? s->layers[l + 1].attn_norm : s->final_norm, NT,
-                     l + 1 < c.n_layers ? 0 : 1, st);
-    PROF_END();
-    ++n;
   }
   GemmArgs g = gemm_args(s, s->lm_head, s->act_lm, s->sc_lm, EPI_ARGMAX, 0);
   g.epi.logits = want_logits ? s->logits_dev : nullptr;

@@ -33,6 +33,8 @@ struct AttnCfg {
   static constexpr int TILE_ELEMS = kKvTile * D;
   static constexpr int NBUF = 4;              // K/V tiles in flight (a CTA's whole range at L=4K)
   static constexpr size_t SMEM = (size_t)ROWS * D * 2 + 2 * NBUF * (size_t)TILE_ELEMS * 2;
+  // the in-CTA key-slice merge reuses the K/V ring
+  static_assert((size_t)(KS - 1) * ROWS * (D + 2) * 4 <= 2 * NBUF * (size_t)TILE_ELEMS * 2, "merge buffer");
 };
 
 template <int D, int RB>
@@ -207,14 +209,57 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     }
   }
 
-  // ---- partial (split, key slice) -> workspace
+  // ---- merge the KS key-slice partials of each row inside the CTA (shared
+  // memory, reusing the K/V ring), so only one partial per split goes out
   const int grp = kvh * Z + z;
-  const int P = S * C::KS;  // partials per (kv head, row chunk)
-  const int pidx = split * C::KS + ks;
-  {
-    float* ws = a.ws + (((size_t)grp * P + pidx) * 256) * D;
-    float* ml = a.ml + (((size_t)grp * P + pidx) * 256) * 2;
-    const int ra = rb * 16 + gq, rbb = ra + 8;
+  const int P = S;  // partials per (kv head, row chunk)
+  const int ra = rb * 16 + gq, rbb = ra + 8;
+  if constexpr (C::KS > 1) {
+    __syncthreads();  // every warp is done with the K/V ring
+    float* so = reinterpret_cast<float*>(Ks);          // [KS-1][ROWS][D]
+    float* sml = so + (C::KS - 1) * ROWS * D;          // [KS-1][ROWS][2]
+    if (ks > 0) {
+      float* dst = so + (size_t)(ks - 1) * ROWS * D;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        *reinterpret_cast<float2*>(dst + ra * D + n * 8 + 2 * tq) = make_float2(o[n][0], o[n][1]);
+        *reinterpret_cast<float2*>(dst + rbb * D + n * 8 + 2 * tq) = make_float2(o[n][2], o[n][3]);
+      }
+      if (tq == 0) {
+        *reinterpret_cast<float2*>(sml + ((ks - 1) * ROWS + ra) * 2) = make_float2(mA, lA);
+        *reinterpret_cast<float2*>(sml + ((ks - 1) * ROWS + rbb) * 2) = make_float2(mB, lB);
+      }
+    }
+    __syncthreads();
+    if (ks == 0) {
+#pragma unroll
+      for (int k2 = 1; k2 < C::KS; ++k2) {
+        const float* src = so + (size_t)(k2 - 1) * ROWS * D;
+        const float2 mlA = *reinterpret_cast<const float2*>(sml + ((k2 - 1) * ROWS + ra) * 2);
+        const float2 mlB = *reinterpret_cast<const float2*>(sml + ((k2 - 1) * ROWS + rbb) * 2);
+        const float nA = fmaxf(mA, mlA.x), nB = fmaxf(mB, mlB.x);
+        const float a1A = (mA == -INFINITY) ? 0.f : exp2f(mA - nA), a2A = (mlA.x == -INFINITY) ? 0.f : exp2f(mlA.x - nA);
+        const float a1B = (mB == -INFINITY) ? 0.f : exp2f(mB - nB), a2B = (mlB.x == -INFINITY) ? 0.f : exp2f(mlB.x - nB);
+#pragma unroll
+        for (int n = 0; n < D / 8; ++n) {
+          const float2 pa = *reinterpret_cast<const float2*>(src + ra * D + n * 8 + 2 * tq);
+          const float2 pb = *reinterpret_cast<const float2*>(src + rbb * D + n * 8 + 2 * tq);
+          o[n][0] = o[n][0] * a1A + pa.x * a2A;
+          o[n][1] = o[n][1] * a1A + pa.y * a2A;
+          o[n][2] = o[n][2] * a1B + pb.x * a2B;
+          o[n][3] = o[n][3] * a1B + pb.y * a2B;
+        }
+        lA = lA * a1A + mlA.y * a2A;
+        lB = lB * a1B + mlB.y * a2B;
+        mA = nA;
+        mB = nB;
+      }
+    }
+  }
+  // ---- the split's partial -> workspace
+  if (ks == 0) {
+    float* ws = a.ws + (((size_t)grp * P + split) * 256) * D;
+    float* ml = a.ml + (((size_t)grp * P + split) * 256) * 2;
 #pragma unroll
     for (int n = 0; n < D / 8; ++n) {
       *reinterpret_cast<float2*>(ws + (size_t)ra * D + n * 8 + 2 * tq) = make_float2(o[n][0], o[n][1]);
@@ -225,18 +270,19 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
       *reinterpret_cast<float2*>(ml + rbb * 2) = make_float2(mB, lB);
     }
   }
-  // ---- meet the other splits of this (kv head, row chunk): every thread
-  // fences its partial stores, one thread arrives and spins on the flag.
-  __threadfence();
+  // ---- meet the other splits of this (kv head, row chunk): the barrier
+  // orders every thread's partial stores before thread 0's GPU-scope fence
+  // (cumulative), which precedes its arrival; thread 0 spins, fences again
+  // (acquire side) and releases the CTA.
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     atomicAdd(&a.bar[grp * 2], 1);
     while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) {
     }
     __threadfence();
   }
   __syncthreads();
-  __threadfence();
   // ---- merge a slice of the rows across the P partials (log-sum-exp, R11).
   // Items = (row, 4-float chunk); the CTA's items are a contiguous slice.  The
   // per-(row, partial) weights exp2(m_p - m*) / l* go through shared memory and
@@ -338,7 +384,7 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
   int S = cap / (a.Hkv_l * Z);
   const int max_tiles = (a.max_ctx_pad + kKvTile - 1) / kKvTile;
   if (S > max_tiles) S = max_tiles;
-  if (S * C::KS > 64) S = 64 / C::KS;  // workspace holds 64 partials per row chunk
+  if (S > 64) S = 64;  // workspace holds 64 partials (one per split) per row chunk
   if (S < 1) S = 1;
   a.splits = S;
   a.zchunks = Z;

@@ -46,8 +46,18 @@ struct GemmCfg {
 #endif
   static constexpr int SMEM = STAGES * UBYTES + 1024;
   static constexpr int KPARTS = NCW / 8;
-  static constexpr int NACC = NT <= 2 ? 2 : 1;     // independent accumulator sets per warp
+#ifdef SS_EXP_NACC
+  static constexpr int NACC = SS_EXP_NACC;
+#else
+  static constexpr int NACC = 1;  // one accumulator set per warp (a 2-set split measured slower: 8 more FADDs)
+#endif
   static constexpr int THREADS = 32 * (NCW + 1);  // + 1 producer warp
+  // resident CTAs per SM the register budget is sized for (3 at T <= 16)
+#ifdef SS_EXP_MINB
+  static constexpr int MINB = SS_EXP_MINB;
+#else
+  static constexpr int MINB = STAGES == 3 ? 3 : 1;
+#endif
 };
 
 // ---------------------------------------------------------------- epilogues
@@ -323,7 +333,7 @@ __device__ int g_ts_kind = -1;
 #endif
 
 template <int WFMT, int NT, int EPI>
-__global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>::MINB) gemm_kernel(GemmArgs g) {
   using C = GemmCfg<WFMT, NT>;
   constexpr int NCW = C::NCW, NCT = NCW * 32;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -456,13 +466,21 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
   uint32_t ph = 0;
   int cur_tg = -1, nst = 0;
   bool done = false;
+  // shared-window addresses, computed once: stage base + per-warp offsets
+  const uint32_t sm0 = opaque(smem_u32(smem)), full0 = opaque(smem_u32(full)), empty0 = opaque(smem_u32(empty));
+  const uint32_t su0 = opaque(smem_u32(s_unit));
+  const uint32_t o_w = opaque((uint32_t)(tile * 128 + lane) * 16);            // weight chunks
+  const uint32_t o_sc = opaque((uint32_t)(kW4Bytes + tile * 64 + gq * 4));     // [grp][gq] scale pairs
+  const uint32_t o_z = opaque((uint32_t)(kW4Bytes + 512 + tile * 16 + gq));    // [grp][gq] zero pairs
+  const uint32_t o_b = opaque((uint32_t)(C::WBYTES + lane * 16));              // B fragments
+  const uint32_t o_x = opaque((uint32_t)(C::WBYTES + NT * 4096 + 8 * tq));     // group sums X
   while (!done) {
     int tg = -1;
     // consume consecutive units of one tile-group; stop at a tile-group change
     // (the new unit stays in its slot for the next round) or at end of work
     while (true) {
-      mbar_wait(&full[s], ph);
-      tg = s_unit[s];
+      mbar_wait_a(full0 + 8 * s, ph);
+      tg = (int)lds32(su0 + 4 * s);
       if (tg < 0) { done = true; break; }
       if (cur_tg >= 0 && tg != cur_tg) break;
       cur_tg = tg;
@@ -471,6 +489,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
       if (nst == 1 && cur_tg == tg && s_ndone == 0) { TS(2); }
 #endif
       const uint8_t* stw = smem + s * C::UBYTES;
+      const uint32_t sst = sm0 + s * C::UBYTES;
 #ifdef SS_EXP_NOCOMPUTE
       if (false) {
 #else
@@ -481,15 +500,10 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
         //   rows g  : s * (acc - (1024 + z) X)          = s * sum (q - z) x
         //   rows g+8: s/16 * (acc - (1024 + 16 z) X)    = s * sum (q - z) x
         // exact integer weights, no per-weight subtract (R3, DESIGN "W4 GEMM").
-        const uint4* wl = reinterpret_cast<const uint4*>(stw) + tile * 128;
-        const uint32_t* sc = reinterpret_cast<const uint32_t*>(stw + kW4Bytes) + tile * 16;  // [grp][gq]
-        const uint8_t* zp = stw + kW4Bytes + 512 + tile * 16;                                  // [grp][gq]
-        const uint4* sa = reinterpret_cast<const uint4*>(stw + C::WBYTES);
-        const float* xs = reinterpret_cast<const float*>(stw + C::WBYTES + NT * 4096);
 #pragma unroll
         for (int gi = 0; gi < 2 / C::KPARTS; ++gi) {
         const int grp = part + gi;  // this warp's 128-deep group(s) of the unit
-        const uint4 w0 = wl[(grp * 2) * 32 + lane], w1 = wl[(grp * 2 + 1) * 32 + lane];
+        const uint4 w0 = lds128(sst + o_w + (grp * 2) * 512), w1 = lds128(sst + o_w + (grp * 2 + 1) * 512);
         const uint32_t wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
         // NACC accumulator sets (even / odd k16 steps) shorten the MMA dependency chain
         float cg[C::NACC][NT][4];
@@ -501,7 +515,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
         for (int jp = 0; jp < 4; ++jp) {  // pairs of k16 steps inside the group
           uint4 bb[NT];
 #pragma unroll
-          for (int n = 0; n < NT; ++n) bb[n] = sa[((grp * 4 + jp) * NT + n) * 32 + lane];
+          for (int n = 0; n < NT; ++n) bb[n] = lds128(sst + o_b + ((grp * 4 + jp) * NT + n) * 512);
 #pragma unroll
           for (int js = 0; js < 2; ++js) {
             uint32_t a[4];
@@ -517,14 +531,14 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
         }
         // c0 = 1024 + z, c8 = 1024 + 16 z built directly as fp32 bits (1024 = 0x44800000,
         // one ulp = 2^-13 there); scales are the bf16 halves of one word
-        const uint32_t zb = zp[grp * 8 + gq], sp = sc[grp * 8 + gq];
+        const uint32_t zb = lds8(sst + o_z + grp * 8), sp = lds32(sst + o_sc + grp * 32);
         const float c0 = __uint_as_float(0x44800000u | ((zb & 15u) << 13));
         const float c8 = __uint_as_float(0x44800000u | ((zb >> 4) << 17));
         const float s0 = __uint_as_float(sp << 16);
         const float s8 = __uint_as_float(sp & 0xFFFF0000u) * 0.0625f;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-          const float2 X = *reinterpret_cast<const float2*>(xs + grp * 8 * NT + n * 8 + 2 * tq);
+          const float2 X = lds64f(sst + o_x + (grp * 8 * NT + n * 8) * 4);
           float c[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) c[e] = C::NACC == 2 ? cg[0][n][e] + cg[C::NACC - 1][n][e] : cg[0][n][e];
@@ -556,7 +570,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS) gemm_kernel(GemmAr
         }  // ji
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive_a(empty0 + 8 * s);
       if (++s == C::STAGES) { s = 0; ph ^= 1; }
     }
     if (cur_tg < 0) break;  // no work at all

@@ -37,6 +37,17 @@ struct AttnCfg {
   static_assert((size_t)(KS - 1) * ROWS * (D + 2) * 4 <= 2 * NBUF * (size_t)TILE_ELEMS * 2, "merge buffer");
 };
 
+#ifdef SS_ATTN_TRACE
+__device__ unsigned long long g_at[256 * 8];
+SS_DEV unsigned long long gtime_at() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATR(ev) do { if (threadIdx.x == 0 && a.layer == 0) { const int cta = (blockIdx.y * gridDim.x + blockIdx.x) * gridDim.z + blockIdx.z; if (cta < 256) g_at[cta * 8 + (ev)] = gtime_at(); } } while (0)
+#else
+#define ATR(ev) do {} while (0)
+#endif
 template <int D, int RB>
 __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(AttnArgs a) {
   using C = AttnCfg<D, RB>;
@@ -66,6 +77,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
   const int ntiles = (L + T + kKvTile - 1) / kKvTile;
   const int t0 = (int)((long)split * ntiles / S), t1 = (int)((long)(split + 1) * ntiles / S);
   const size_t head_base = ((size_t)a.layer * a.Hkv_l + kvh) * a.max_ctx_pad * D;
+  ATR(0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NBUF; ++i) mbar_init(&full[i], 1);
@@ -86,6 +98,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
   }
   pdl_wait();
   pdl_trigger();
+  ATR(1);
   if (threadIdx.x == 0) {
     for (int i = issued; i < NBUF && t0 + i < t1; ++i) {
       const int tile = t0 + i;
@@ -99,6 +112,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     bulk_g2s_nohint(Qs, a.qbuf + ((size_t)kvh * (G * SS_MAX_TREE) + m0) * D, ROWS * D * 2, &qbar);
   }
   mbar_wait(&qbar, 0);
+  ATR(2);
   const int qr = rb * 16 + (lane & 15);
   const uint16_t* qrow = Qs + qr * D;
 
@@ -209,6 +223,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     }
   }
 
+  ATR(3);
   // ---- merge the KS key-slice partials of each row inside the CTA (shared
   // memory, reusing the K/V ring), so only one partial per split goes out
   const int grp = kvh * Z + z;
@@ -277,10 +292,12 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
+    ATR(4);
     atomicAdd(&a.bar[grp * 2], 1);
     while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) {
     }
     __threadfence();
+    ATR(5);
   }
   __syncthreads();
   // ---- merge a slice of the rows across the P partials (log-sum-exp, R11).
@@ -344,6 +361,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     }
   }
   __syncthreads();
+  ATR(6);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&a.bar[grp * 2 + 1], 1) == S - 1) {
@@ -423,3 +441,10 @@ int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st) {
 }
 
 }  // namespace ss
+
+#ifdef SS_ATTN_TRACE
+extern "C" int ss_debug_attn_trace(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, ss::g_at, sizeof(ss::g_at)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
   __shared__ int s_done_list[256];
   __shared__ int s_ndone;
+  __shared__ int s_flushed;          // consumer-warp flushes so far (signaler)
   __shared__ int s_unit[C::STAGES];  // tile-group of each ring slot (-1 = no more work)
 
   TS(0);
@@ -351,18 +352,14 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   }
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Hybrid schedule.  Units (tile-group, K-stage) are numbered tile-group
-  // major.  The first Us units are split into equal contiguous static ranges
-  // (one or two tile-groups per CTA, so few partial flushes and a spread-out
-  // HBM access pattern); the remaining units form a pool of CH-unit chunks
-  // that producers grab from an atomic queue once their static range is
-  // issued.  Per-SM HBM bandwidth on B200 is uneven (static-only ranges left
-  // 30-40% idle tails), the pool absorbs that.
+  // Static stream-K schedule: units (tile-group, K-stage) are numbered
+  // tile-group major and split into equal contiguous ranges, one per CTA
+  // (one or two tile-groups per CTA: few partial flushes, a spread-out HBM
+  // access pattern).  A dynamic work queue and a static + pool hybrid were
+  // both measured slower (profiles/r01_experiments.md).
   const int U = g.n_tg * g.S;
-  const int Us = (int)((long)U * g.static_pct / 100);
-  const int u0 = (int)((long)blockIdx.x * Us / gridDim.x), u1 = (int)((long)(blockIdx.x + 1) * Us / gridDim.x);
-  const int CH = g.chunk, n_chunks = (U - Us + CH - 1) / CH;
-  int* queue = g.counters + g.n_tg;  // [0] grab counter, [1] exit counter
+  const int u0 = (int)((long)blockIdx.x * U / gridDim.x), u1 = (int)((long)(blockIdx.x + 1) * U / gridDim.x);
+  int* queue = g.counters + g.n_tg;  // [1] exit counter
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -371,47 +368,26 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
     }
     fence_mbar_init();
     s_ndone = 0;
+    s_flushed = 0;
   }
   __syncthreads();
 
   if (warp == NCW) {
-    // ---------------- producer: grabs chunks, TMA bulk copies into the ring.
-    // The weights do not depend on earlier kernels, so the first STAGES units'
-    // weights are requested before the PDL wait (overlapping the previous
-    // kernel's tail); activations only after it.
+    // ---------------- producer (lane 0): TMA bulk copies of the CTA's static
+    // unit range into the ring.  The weights do not depend on earlier
+    // kernels, so the first STAGES units' weights are requested before the
+    // PDL wait (overlapping the previous kernel's tail); activations only
+    // after it.
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
-      // static range first, then pool chunks (the next chunk is grabbed one
-      // ahead so the atomic's round trip never stalls the copy stream)
-      int us = u0;
-      int c = -1, c_next = -1, ci = 0;
       int pre_u[C::STAGES], npre = 0;
       bool waited = false;
-      while (true) {
-        int u = -1;
-        if (us < u1) {
-          u = us++;
-        } else {
-          if (c < 0) {
-            c = atomicAdd(&queue[0], 1);
-            c_next = c < n_chunks ? atomicAdd(&queue[0], 1) : n_chunks;
-          }
-          if (c < n_chunks) {
-            // transposed grab order: spread concurrent chunks over the pool
-            const int G = gridDim.x, m = n_chunks / G;
-            const int pc = (c < m * G) ? (c % G) * m + c / G : c;
-            u = Us + pc * CH + ci;
-            if (++ci == CH || u + 1 >= U) {
-              ci = 0;
-              c = c_next;
-              if (c < n_chunks) c_next = atomicAdd(&queue[0], 1);
-            }
-          }
-        }
-        const int utg = u < 0 ? -1 : u / g.S, uks = u < 0 ? 0 : u - utg * g.S;
-        if (!waited && (npre == C::STAGES || u < 0)) {
+      for (int u = u0;; ++u) {
+        const bool have = u < u1;
+        const int utg = have ? u / g.S : -1, uks = have ? u - utg * g.S : 0;
+        if (!waited && (npre == C::STAGES || !have)) {
           pdl_wait();
           waited = true;
           for (int i = 0; i < npre; ++i)
@@ -420,28 +396,42 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         }
         mbar_wait(&empty[s], ph ^ 1);
         // the consumers' generic-proxy reads of this slot must be ordered
-        // before the async-proxy (TMA) overwrite: without this fence a slot
-        // can be refilled under a slow reader (observed as whole-tile-group
-        // errors at 3-4 CTAs/SM).
+        // before the async-proxy (TMA) overwrite (observed as whole-tile-group
+        // errors at 3-4 CTAs/SM without it)
         fence_proxy_async_smem();
         s_unit[s] = utg;
-        if (u < 0) {
+        if (!have) {
           mbar_arrive(&full[s]);  // publishes s_unit[s] = -1: no more work
           break;
         }
         uint8_t* dst = smem + s * C::UBYTES;
         mbar_expect_tx(&full[s], C::UBYTES);
-#ifdef SS_EXP_L2W
-        bulk_g2s(dst, g.W + (size_t)(u % 64) * C::WBYTES, C::WBYTES, &full[s], pol);
-#else
         bulk_g2s(dst, g.W + (size_t)u * C::WBYTES, C::WBYTES, &full[s], pol);
-#endif
         if (waited) bulk_g2s_nohint(dst + C::WBYTES, g.act + (size_t)uks * C::ABYTES, C::ABYTES, &full[s]);
         else pre_u[npre++] = uks;
         if (++s == C::STAGES) { s = 0; ph ^= 1; }
       }
       if (!waited) pdl_wait();
+    } else if (lane == 1 && u1 > u0) {
+      // ---------------- flush signaler: once all consumer warps have pushed
+      // a tile-group's partial sums (red.add), one GPU-scope fence + arrival
+      // count for the CTA, off the consumers' critical path
+      int k = 0;
+      for (int tg = u0 / g.S; tg <= (u1 - 1) / g.S; ++tg) {
+        const int nst = min(u1, (tg + 1) * g.S) - max(u0, tg * g.S);
+        ++k;
+        int v;
+        do {
+          asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_flushed)) : "memory");
+          if (v < NCW * k) __nanosleep(100);
+        } while (v < NCW * k);
+        fence_acq_rel_gpu();
+        const int old = atomicAdd(&g.counters[tg], nst);
+        if (old + nst == g.S) s_done_list[s_ndone++] = tg;
+      }
     }
+    __syncwarp();
+    named_bar_sync(3, NCT + 32);  // s_done_list is complete for the epilogue threads
     return;  // producer warp does not take part in epilogues
   }
   pdl_wait();
@@ -587,22 +577,19 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
       }
     }
-    // bar.sync orders every consumer's reductions before thread 0's GPU-scope
-    // release fence (cumulative), which precedes the arrival count.  Only
-    // thread 0 waits for the count; a completed tile-group is queued and its
-    // epilogue runs after the main loop, so the other warps never stall here.
-    named_bar_sync(1, NCT);
-    if (threadIdx.x == 0) {
-      fence_acq_rel_gpu();
-      const int old = atomicAdd(&g.counters[ftg], nst);
-      if (old + nst == g.S) s_done_list[s_ndone++] = ftg;
+    // hand the flush to the signaler lane: the block-scope release orders this
+    // warp's reductions before its fence (cumulative) and arrival count
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd_block(&s_flushed, 1);
     }
     cur_tg = done ? -1 : tg;  // the unit waiting in the current slot starts the next group
     nst = 0;
     TS(4);
   }
   // ---- epilogues of the tile-groups this CTA completed (last arriver)
-  named_bar_sync(1, NCT);
+  named_bar_sync(3, NCT + 32);  // with the signaler: s_done_list is complete
   if (s_ndone) fence_acq_rel_gpu();  // acquire side of the arrival counts
   const int ndone = s_ndone;
   for (int i = 0; i < ndone; ++i) {
@@ -661,7 +648,6 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
     if (atomicAdd(&queue[1], 1) == (int)gridDim.x - 1) {
-      queue[0] = 0;
       queue[1] = 0;
       if (g.norm_out) {
         g.nbar[0] = 0;
@@ -689,13 +675,7 @@ static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
   int o = (occ_cap > 0 && occ_cap < occ) ? occ_cap : occ;
   int grid = (int)std::min<long>(U, (long)g.n_sm * o);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  GemmArgs ga = g;
-  static const int static_pct = getenv("SS_STATIC_PCT") ? atoi(getenv("SS_STATIC_PCT")) : 100;  // tuning aid
-  static const int chunk_div = getenv("SS_CHUNK_DIV") ? atoi(getenv("SS_CHUNK_DIV")) : 4;       // tuning aid
-  ga.static_pct = static_pct;
-  // pool chunks: ~chunk_div chunks per CTA of the pool's share
-  ga.chunk = (int)std::max<long>(1, (U * (100 - static_pct) / 100) / ((long)grid * chunk_div));
-  launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, ga);
+  launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, g);
   return 1;
 }
 

@@ -58,10 +58,8 @@ struct GemmArgs {
   const uint8_t* W = nullptr;
   const uint8_t* act = nullptr;
   int n_tg = 0, S = 0;
-  int chunk = 4;             // units per pool chunk (dynamic part of the schedule)
-  int static_pct = 100;      // % of units assigned as static contiguous ranges
   float* accum = nullptr;
-  int* counters = nullptr;   // [n_tg] arrival counters + [2] queue head / exit count
+  int* counters = nullptr;   // [n_tg] arrival counters + [2] (exit count in [1])
   int n_sm = 148;
   // optional: zero the X (group-sum) slots of a W4 activation buffer that a
   // later kernel fills with atomics (attention -> O input, SwiGLU -> down input)

@@ -755,6 +755,9 @@ static Prof* g_prof = nullptr;
 static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, cudaStream_t st) {
   const ss_model_cfg& c = s->cfg;
   int n = 0;
+  // timing experiments only (results are wrong): SS_EXP_SKIP = bitmask of
+  // launches to leave out, 1 qkv, 2 attention, 4 o, 8 gate/up, 16 down
+  static const int skip = getenv("SS_EXP_SKIP") ? atoi(getenv("SS_EXP_SKIP")) : 0;
   const int cap = s->launch_cap;
   for (int l = 0; l < c.n_layers; ++l) {
     LayerW& lw = s->layers[l];
@@ -763,7 +766,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.zero_x_stages = lw.o.S;
     g.zero_x_nt = NT;
     PROF_BEGIN(1);
-    n += launch_gemm(g, 0, NT, cap, st);
+    if (!(skip & 1)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     AttnArgs a;
     a.st = s->dstate;
@@ -781,7 +784,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     a.bar = s->attn_bar;
     a.act_out = s->act_o;
     PROF_BEGIN(2);
-    n += launch_attention(a, cap, st);
+    if (!(skip & 2)) n += launch_attention(a, cap, st);
     PROF_END();
     g = gemm_args(s, lw.o, s->act_o, s->sc_o, EPI_RESID, l);
     g.epi.ar_seq = 2 * l;
@@ -792,11 +795,11 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.norm_out = s->act_h;
     g.norm_split = 0;
     PROF_BEGIN(3);
-    n += launch_gemm(g, 0, NT, cap, st);
+    if (!(skip & 4)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     g = gemm_args(s, lw.gu, s->act_h, s->sc_gu, EPI_SWIGLU, l);
     PROF_BEGIN(5);
-    n += launch_gemm(g, 0, NT, cap, st);
+    if (!(skip & 8)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     g = gemm_args(s, lw.down, s->act_d, s->sc_down, EPI_RESID, l);
     g.epi.ar_seq = 2 * l + 1;
@@ -805,7 +808,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.norm_out = l + 1 < c.n_layers ? s->act_h : s->act_lm;
     g.norm_split = l + 1 < c.n_layers ? 0 : 1;
     PROF_BEGIN(6);
-    n += launch_gemm(g, 0, NT, cap, st);
+    if (!(skip & 16)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
   }
   GemmArgs g = gemm_args(s, s->lm_head, s->act_lm, s->sc_lm, EPI_ARGMAX, 0);

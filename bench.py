@@ -346,6 +346,8 @@ def run_ours(args, cfg):
                             "algorithmic_bytes_per_launch": gateup_bytes(cfg, world),
                             "avg_launch_us": per * 1e3, "share_of_step": gu_ms / tot if tot else None}
         line["kernel_times_us"] = {k: {"total": v[0] * 1e3, "launches": v[1]} for k, v in prof.items()}
+    if world == 1 and not args.no_tp_emulate:
+        line["tp_emulated"] = tp_emulated(args, cfg, local, dev, peak)
     if rank == 0 and not args.no_cpu_baseline:
         smp = OracleSample(cfg, T, L)
         sec = smp.step_seconds(0)
@@ -360,6 +362,42 @@ def run_ours(args, cfg):
     return 0
 
 
+def tp_emulated(args, cfg, local, dev, peak):
+    """Per-GPU step latency of ONE rank of a TP = 2/4/8 group, emulated on this
+    single GPU (ss_import_loopback: the rank's weight shard, KV heads and LL
+    all-reduce stores, with its own partial standing in for the peers').
+    Timing only -- the logits are not the sharded model's -- and the
+    all-reduce cost is a lower bound (local stores instead of NVLink)."""
+    import torch
+    import paper_2506_11309_b200 as pkg
+    T, L = args.T, args.L
+    out = {"note": "one TP rank on one GPU, loopback all-reduce (timing emulation, not a multi-GPU run)"}
+    n = 3 + 10
+    for P in (2, 4, 8):
+        sh = pkg.Shard(cfg, 0, P, local, max_ctx=L + T * (3 * n + 8) + 64, max_tree=max(T, 8))
+        sh.synth_weights(args.seed)
+        sh.synth_prefix_kv(args.seed + 1, L)
+        sh.import_loopback()
+        trees = make_trees(cfg, T, n, seed=11)
+        d_tok = torch.tensor(np.stack([t for t, _ in trees]), dtype=torch.int32, device=dev)
+        d_par = torch.tensor(np.stack([p for _, p in trees]), dtype=torch.int32, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        for i in range(3):
+            sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(3, n):
+            sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / (n - 3)
+        b = step_bytes(cfg, T, L + 1, P)
+        out[f"tp{P}"] = {"us": ms * 1e3, "bytes_per_gpu": b, "roofline_frac": b / (ms / 1e3) / 1e9 / peak}
+        sh.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -371,6 +409,7 @@ def main():
     ap.add_argument("--L", type=int, default=4096)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tp-emulate", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

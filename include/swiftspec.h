@@ -134,6 +134,14 @@ ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_siz
 ss_status ss_export_handle(ss_shard* s, void* buf, size_t* len);
 ss_status ss_import_peers(ss_shard* s, const void* const* blobs, const size_t* lens);
 ss_status ss_import_local_peers(ss_shard* s, ss_shard* const* shards);
+/* Timing emulation of one rank of a tp_size group on a single GPU: the
+ * fused all-reduce and the argmax exchange write this rank's partial into
+ * every rank slot of its own receive buffer, so a rank's full step (its
+ * weight shard, its KV heads, the LL traffic volume per step) runs without
+ * peers.  Results are NOT the sharded model's (the sum is tp_size x this
+ * rank's partial); bench.py --tp-emulate uses it to report per-GPU step
+ * latency at TP 2/4/8 shapes on one B200.  Errors: SS_EINVAL if tp_size < 2. */
+ss_status ss_import_loopback(ss_shard* s);
 
 /* Launch-resource cap (fake-peer mode: several ranks share one GPU and every
  * rank's persistent kernels must be co-resident).  max_ctas_per_kernel <= 0

@@ -294,8 +294,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     __threadfence();
     ATR(4);
     atomicAdd(&a.bar[grp * 2], 1);
-    while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) {
-    }
+    while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) __nanosleep(100);
     __threadfence();
     ATR(5);
   }

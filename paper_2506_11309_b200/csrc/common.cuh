@@ -279,7 +279,11 @@ SS_DEV void ll_store(uint4* dst, uint32_t d1, uint32_t d2, uint32_t flag) {
 }
 SS_DEV bool ll_try_load(const uint4* src, uint32_t flag, uint32_t& d1, uint32_t& d2) {
   uint32_t a, f1, b, f2;
+#ifdef SS_EXP_LLRELAXED
+  asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+#else
   asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+#endif
                : "=r"(a), "=r"(f1), "=r"(b), "=r"(f2)
                : "l"(src)
                : "memory");

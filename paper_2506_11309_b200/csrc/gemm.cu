@@ -145,32 +145,48 @@ __device__ void epi_ar_send(const EpiArgs& e, int tg, const float* acc, int T) {
     int r = idx / pairs, tp = idx - r * pairs;
     float a = __ldcg(acc + (size_t)r * TP + 2 * tp);
     float b = __ldcg(acc + (size_t)r * TP + 2 * tp + 1);
-    size_t line = (((size_t)(e.ar_seq & 1) * e.P + e.rank) * e.n_tg_total + tg) * 128 * 32 + (size_t)r * 32 + tp;
-    for (int p = 0; p < e.P; ++p)
+    for (int p = 0; p < e.P; ++p) {
+      // loopback emulation (one rank on one GPU, timing only): every rank
+      // slot of the own buffer receives this rank's partial
+      const int slot = e.loopback ? p : e.rank;
+      const size_t line = (((size_t)(e.ar_seq & 1) * e.P + slot) * e.n_tg_total + tg) * 128 * 32 + (size_t)r * 32 + tp;
       ll_store(reinterpret_cast<uint4*>(e.peer_recv[p]) + line, __float_as_uint(a), __float_as_uint(b), flag);
+    }
   }
 }
 
 // tp > 1, phase 2 (after the CTA's compute loop): wait for every rank's
 // partial of the tile-group, sum in rank order (identical on all ranks), add.
-template <int NT>
+// The P lines of an item are loaded together (independent L2 / NVLink round
+// trips in flight) and only lines whose flags are not there yet are re-polled.
 __device__ void epi_ar_recv(const EpiArgs& e, int tg, int T, float* ss) {
   const uint32_t flag = e.st->epoch + e.ar_seq;
   const int pairs = (T + 1) >> 1;
   for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
     const int tp = idx >> 7, r = idx & 127;  // warp = 32 rows of one token pair
-    float s0 = 0.f, s1 = 0.f;
-    for (int p = 0; p < e.P; ++p) {
-      const uint4* src = reinterpret_cast<const uint4*>(e.recv) +
-                         (((size_t)(e.ar_seq & 1) * e.P + p) * e.n_tg_total + tg) * 128 * 32 + (size_t)r * 32 + tp;
-      uint32_t d1, d2;
-      long spins = 0;
-      while (!ll_try_load(src, flag, d1, d2)) {
-        if (++spins > (1L << 26)) { e.st->timeout = 1; break; }
-      }
-      s0 += __uint_as_float(d1);
-      s1 += __uint_as_float(d2);
+    const uint4* src0 = reinterpret_cast<const uint4*>(e.recv) +
+                        (((size_t)(e.ar_seq & 1) * e.P) * e.n_tg_total + tg) * 128 * 32 + (size_t)r * 32 + tp;
+    const size_t pstride = (size_t)e.n_tg_total * 128 * 32;
+    uint32_t d1[kMaxPeers], d2[kMaxPeers];
+    unsigned ready = 0;
+#pragma unroll
+    for (int p = 0; p < kMaxPeers; ++p)
+      if (p < e.P && ll_try_load(src0 + p * pstride, flag, d1[p], d2[p])) ready |= 1u << p;
+    const unsigned all = (1u << e.P) - 1u;
+    long spins = 0;
+    while (ready != all) {
+#pragma unroll
+      for (int p = 0; p < kMaxPeers; ++p)
+        if (p < e.P && !(ready & (1u << p)) && ll_try_load(src0 + p * pstride, flag, d1[p], d2[p])) ready |= 1u << p;
+      if (++spins > (1L << 24)) { e.st->timeout = 1; break; }
     }
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int p = 0; p < kMaxPeers; ++p)
+      if (p < e.P) {
+        s0 += __uint_as_float(d1[p]);
+        s1 += __uint_as_float(d2[p]);
+      }
     const int t0 = 2 * tp;
     float* x0 = e.x + (size_t)t0 * e.h + tg * 128 + r;
     const float n0 = *x0 + s0;
@@ -191,16 +207,16 @@ __device__ void epi_ar_recv(const EpiArgs& e, int tg, int T, float* ss) {
   }
 }
 
-// Fused RMSNorm of the updated residual (R5) into the next GEMM's input,
-// after every tile-group of this launch has been added (grid barrier): each
-// warp normalises one (token, 128-group) item -- fp16 fragments + group sum X
-// for a W4 GEMM, or bf16 hi/lo fragments for the LM head (split).
+// Fused RMSNorm of the updated residual (R5) into the next GEMM's input, for
+// one 128-column group of every token, after all tile-groups of the launch
+// are added (see the EPI_RESID tail of gemm_kernel): warp = token, 4 columns
+// per lane -- fp16 fragments + group sum X for a W4 GEMM, or bf16 hi/lo
+// fragments for the LM head (split).
 template <int NT>
-__device__ void norm_slice(const GemmArgs& g, int T, int ncw) {
+__device__ void norm_group(const GemmArgs& g, int T, int grp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = g.epi.h, ngr = h / 128;
-  for (int it = blockIdx.x + gridDim.x * warp; it < T * ngr; it += gridDim.x * ncw) {
-    const int t = it / ngr, grp = it - t * ngr;
+  const int h = g.epi.h;
+  for (int t = warp; t < T; t += 8) {
     const int k = grp * 128 + lane * 4;
     const float4 v = __ldcg(reinterpret_cast<const float4*>(g.epi.x + (size_t)t * h + k));
     const uint2 gw = *reinterpret_cast<const uint2*>(g.norm_gain + k);
@@ -254,8 +270,8 @@ __device__ void argmax_exchange(const EpiArgs& e, DevState* st) {
   for (int t = 0; t < T; ++t) {
     unsigned long long k = __ldcg(&st->argmax_key[t]);
     for (int p = 0; p < e.P; ++p)
-      ll_store(reinterpret_cast<uint4*>(e.peer_recv[p]) + base + (size_t)e.rank * 64 + t, (uint32_t)k,
-               (uint32_t)(k >> 32), flag);
+      ll_store(reinterpret_cast<uint4*>(e.peer_recv[p]) + base + (size_t)(e.loopback ? p : e.rank) * 64 + t,
+               (uint32_t)k, (uint32_t)(k >> 32), flag);
   }
   for (int t = 0; t < T; ++t) {
     unsigned long long best = 0;
@@ -623,38 +639,53 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
       }
     }
   }
-  TS(5);
   if constexpr (EPI == EPI_RESID) {
     if (g.epi.P > 1) {  // all sends are out: now wait for the peers' partials
+#ifdef SS_EXP_TIMING
+      if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && g.epi.layer == 0)
+        g_ts[(blockIdx.x * 8 + 6) & 0xFFFF] = (unsigned long long)ndone;
+#endif
+#ifdef SS_EXP_TIMING
+      if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && g.epi.layer == 0)
+        g_ts[(blockIdx.x * 8 + 2) & 0xFFFF] = gtimer();
+#endif
       named_bar_sync(1, NCT);
+#ifdef SS_EXP_TIMING
+      if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && g.epi.layer == 0)
+        g_ts[(blockIdx.x * 8 + 3) & 0xFFFF] = gtimer();
+#endif
       if (threadIdx.x < 256)
-        for (int i = 0; i < ndone; ++i) epi_ar_recv<NT>(g.epi, s_done_list[i], T, g.norm_out ? g.ss : nullptr);
+        for (int i = 0; i < ndone; ++i) epi_ar_recv(g.epi, s_done_list[i], T, g.norm_out ? g.ss : nullptr);
     }
-    if (g.norm_out) {  // fused RMSNorm: wait for every CTA's residual updates
+    TS(5);
+    if (g.norm_out && ndone > 0) {
+      // fused RMSNorm: only the CTAs that finalised tile-groups take part
+      // (the others have left already); they meet once every tile-group of
+      // the residual is added (per-token sums complete), then each
+      // normalises the 128-column groups of its own tile-groups
       named_bar_sync(1, NCT);
       if (threadIdx.x == 0) {
         fence_acq_rel_gpu();
-        atomicAdd(&g.nbar[0], 1);
-        while (*reinterpret_cast<volatile int*>(&g.nbar[0]) < (int)gridDim.x) {
-        }
+        atomicAdd(&g.nbar[0], ndone);
+        while (*reinterpret_cast<volatile int*>(&g.nbar[0]) < g.n_tg) __nanosleep(100);
         fence_acq_rel_gpu();
       }
       named_bar_sync(1, NCT);
-      norm_slice<NT>(g, T, NCW);
-    }
-  }
-  // last CTA out resets the work queue (and the norm barrier / sums)
-  named_bar_sync(1, NCT);
-  if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();
-    if (atomicAdd(&queue[1], 1) == (int)gridDim.x - 1) {
-      queue[1] = 0;
-      if (g.norm_out) {
-        g.nbar[0] = 0;
-        for (int t = 0; t < SS_MAX_TREE; ++t) g.ss[t] = 0.f;
+      if (threadIdx.x < 256)
+        for (int i = 0; i < ndone; ++i) norm_group<NT>(g, T, s_done_list[i]);
+      // the last finaliser out resets the barrier and the per-token sums
+      named_bar_sync(1, NCT);
+      if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();
+        if (atomicAdd(&g.nbar[1], ndone) + ndone == g.n_tg) {
+          g.nbar[0] = 0;
+          g.nbar[1] = 0;
+          for (int t = 0; t < SS_MAX_TREE; ++t) g.ss[t] = 0.f;
+        }
       }
     }
   }
+  TS(7);
 }
 
 // ---------------------------------------------------------------- launch

@@ -133,6 +133,7 @@ struct ss_shard {
   size_t recv_bytes = 0;
   float* peer_recv[ss::kMaxPeers] = {nullptr};
   bool peers_ready = false;
+  bool loopback = false;            // ss_import_loopback (timing emulation)
   bool ipc_opened[ss::kMaxPeers] = {false};
 
   // a13 mailbox: this shard's inbox (written by the draft group)

@@ -45,6 +45,7 @@ struct EpiArgs {
   float* x = nullptr;
   int h = 0;
   int rank = 0, P = 1, n_tg_total = 0, ar_seq = 0;
+  int loopback = 0;  // timing emulation of one TP rank on one GPU (ss_import_loopback)
   float* recv = nullptr;
   float* peer_recv[kMaxPeers] = {nullptr};
   // SWIGLU

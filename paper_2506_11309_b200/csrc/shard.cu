@@ -721,6 +721,7 @@ static GemmArgs gemm_args(ss_shard* s, const PackedLinear& pl, const uint8_t* ac
   e.n_tg_total = s->cfg.hidden / 128;
   e.recv = s->recv;
   for (int p = 0; p < s->P; ++p) e.peer_recv[p] = s->peer_recv[p];
+  e.loopback = s->loopback ? 1 : 0;
   e.act_out = s->act_d;
   e.V_l = s->V_l;
   e.V_off = s->V_off;
@@ -1037,6 +1038,18 @@ extern "C" ss_status ss_import_local_peers(ss_shard* s, ss_shard* const* shards)
     }
     s->peer_recv[p] = shards[p]->recv;
   }
+  s->peers_ready = true;
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" ss_status ss_import_loopback(ss_shard* s) {
+  if (!s) FAIL(SS_EINVAL, "null argument");
+  if (s->P < 2) FAIL(SS_EINVAL, "loopback needs tp_size > 1");
+  for (int p = 0; p < s->P; ++p) s->peer_recv[p] = s->recv;
+  s->loopback = true;
   s->peers_ready = true;
   for (auto& kv : s->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);

@@ -43,7 +43,7 @@ class VerifyResultC(C.Structure):
 
 _lib = None
 
-EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_local_peers",
+EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_local_peers", "ss_import_loopback",
            "ss_set_launch_cap", "ss_destroy", "ss_last_error", "ss_load_weights", "ss_synth_weights",
            "ss_set_prefix_kv", "ss_synth_prefix_kv", "ss_read_kv", "ss_set_committed_len",
            "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
@@ -66,6 +66,7 @@ def lib():
         "ss_export_handle": (i32, [vp, vp, C.POINTER(sz)]),
         "ss_import_peers": (i32, [vp, C.POINTER(vp), C.POINTER(sz)]),
         "ss_import_local_peers": (i32, [vp, C.POINTER(vp)]),
+        "ss_import_loopback": (i32, [vp]),
         "ss_set_launch_cap": (i32, [vp, i32]),
         "ss_destroy": (i32, [vp]),
         "ss_last_error": (C.c_char_p, []),
@@ -265,6 +266,10 @@ class Shard:
         arr = (C.c_void_p * len(shards))(*[s.h.value for s in shards])
         for s in shards:
             _check(lib().ss_import_local_peers(s.h, arr))
+
+    def import_loopback(self):
+        """Timing emulation of this rank alone (include/swiftspec.h ss_import_loopback)."""
+        _check(lib().ss_import_loopback(self.h))
 
     def set_launch_cap(self, cap: int):
         _check(lib().ss_set_launch_cap(self.h, cap))

@@ -8,8 +8,11 @@ import numpy as np, torch, synth
 import paper_2506_11309_b200 as pkg
 from paper_2506_11309_b200 import swiftspec as ssp
 cfg = dataclasses.replace(synth.CONFIGS["llama3-70b"], n_layers=1)
-sh = pkg.Shard(cfg, 0, 1, 0, max_ctx=4096 + 256, max_tree=8)
+TPE = int(os.environ.get("TP", "1"))  # >1: one rank of a TP group, loopback emulation
+sh = pkg.Shard(cfg, 0, TPE, 0, max_ctx=4096 + 256, max_tree=8)
 sh.synth_weights(0); sh.synth_prefix_kv(1, 4096)
+if TPE > 1:
+    sh.import_loopback()
 t, p = synth.tree_paperlike(8, cfg.vocab, np.random.default_rng(0))
 dt = torch.tensor(t, dtype=torch.int32, device="cuda"); dp = torch.tensor(p, dtype=torch.int32, device="cuda")
 L = ssp.lib()
@@ -31,12 +34,13 @@ ts = ts[ok]
 sm = ts[:, 6].copy()
 t0 = ts[:, 0].min()
 rel = (ts - t0) / 1000.0
-names = ["start", "pdl_wait done", "first data", "last unit done", "after flush+count", "end"]
+names = ["start", "pdl_wait done", "first data", "last unit done", "after flush+count", "after AR recv", "smid", "end"]
 for i, n in enumerate(names):
+    if n == 'smid': continue
     col = rel[:, i]
     print(f"kind {kind} {n:20s} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f} us")
 
-end = rel[:, 5]
+end = rel[:, 7]
 order = np.argsort(sm)
 print("end time by SM id (sorted by sm):")
 smu = np.unique(sm)
@@ -44,3 +48,11 @@ per_sm = np.array([end[sm == s].max() for s in smu])
 for i in range(0, len(smu), 16):
     print("  sm %3d-%3d:" % (smu[i], smu[min(i+15, len(smu)-1)]), " ".join("%5.1f" % x for x in per_sm[i:i+16]))
 print("ctas per sm:", np.bincount(np.bincount(sm.astype(int))))
+
+if os.environ.get("SHOW_SLOW"):
+    ar = rel[:, 5]
+    idx = np.argsort(-ar)[:12]
+    print("slowest CTAs after AR recv: (cta, t_flush, t_sent(slot2), t_bar(slot3), t_after_ar, ndone)")
+    for i in idx:
+        print(int(np.nonzero(ok)[0][i]), round(rel[i, 4], 2), round(rel[i, 2], 2), round(rel[i, 3], 2), round(ar[i], 2), int(ts[i, 6]))
+    print("ndone histogram:", np.bincount(ts[:, 6].astype(int)))

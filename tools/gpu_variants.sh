@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for v in "" ${VARIANTS}; do
   lib=libswiftspec${v:+_$v}.so
-  SWIFTSPEC_LIB=$lib timeout 150 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$v.json 2> gpurun_out/bench_$v.err
+  SWIFTSPEC_LIB=$lib timeout 150 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-tp-emulate > gpurun_out/bench_$v.json 2> gpurun_out/bench_$v.err
   python - "$v" <<'PY'
 import json, sys
 d = json.load(open(f'gpurun_out/bench_{sys.argv[1]}.json'))

@@ -39,6 +39,7 @@ struct AttnCfg {
 
 #ifdef SS_ATTN_TRACE
 __device__ unsigned long long g_at[256 * 8];
+__device__ unsigned long long g_att[256 * 16];  // per CTA: [tile][waited, computed]
 SS_DEV unsigned long long gtime_at() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -115,6 +116,11 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
   ATR(2);
   const int qr = rb * 16 + (lane & 15);
   const uint16_t* qrow = Qs + qr * D;
+  // the warp's Q fragments stay in registers for all tiles (shared-memory
+  // bandwidth, not math, bounds this loop: K/V are re-read by every row block)
+  uint32_t qf[D / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) ldmatrix_x4(qf[kk], qrow + (((kk * 2 + (lane >> 4)) ^ (qr & 7)) << 3));
 
   const int rowA = m0 + rb * 16 + gq, rowB = rowA + 8;
   const int tokA = min(rowA / G, SS_MAX_TREE - 1), tokB = min(rowB / G, SS_MAX_TREE - 1);
@@ -132,6 +138,12 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     const int b = (it - t0) % NBUF;
     const uint32_t phase = ((it - t0) / NBUF) & 1;
     mbar_wait(&full[b], phase);
+#ifdef SS_ATTN_TRACE
+    if (threadIdx.x == 0 && a.layer == 0 && it - t0 < 8) {
+      const int cta = (blockIdx.y * gridDim.x + blockIdx.x) * gridDim.z + blockIdx.z;
+      if (cta < 256) g_att[cta * 16 + (it - t0) * 2] = gtime_at();
+    }
+#endif
     const uint16_t* Kt = Ks + b * TILE_ELEMS;
     const uint16_t* Vt = Vs + b * TILE_ELEMS;
 
@@ -140,16 +152,14 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     for (int n = 0; n < C::NTK; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
-      uint32_t qa[4];
-      ldmatrix_x4(qa, qrow + (((kk * 2 + (lane >> 4)) ^ (qr & 7)) << 3));
 #pragma unroll
       for (int np = 0; np < C::NTK / 2; ++np) {
         const int key = kofs + np * 16 + (lane & 7) + ((lane >> 4) << 3);
         const int ch = kk * 2 + ((lane >> 3) & 1);
         uint32_t kb[4];
         ldmatrix_x4(kb, Kt + key * D + ((ch ^ (key & 7)) << 3));
-        mma_f16_16816(sc[2 * np], qa, kb[0], kb[1]);
-        mma_f16_16816(sc[2 * np + 1], qa, kb[2], kb[3]);
+        mma_f16_16816(sc[2 * np], qf[kk], kb[0], kb[1]);
+        mma_f16_16816(sc[2 * np + 1], qf[kk], kb[2], kb[3]);
       }
     }
     // mask: prefix always visible; tree rows by ancestor bit; beyond L+T never
@@ -194,9 +204,11 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
     lB = lB * alB + sumB;
     mA = mnA;
     mB = mnB;
+    if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {  // running max moved: rescale
 #pragma unroll
-    for (int n = 0; n < D / 8; ++n) {
-      o[n][0] *= alA; o[n][1] *= alA; o[n][2] *= alB; o[n][3] *= alB;
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= alA; o[n][1] *= alA; o[n][2] *= alB; o[n][3] *= alB;
+      }
     }
 #pragma unroll
     for (int kk = 0; kk < C::NTK / 2; ++kk) {
@@ -445,5 +457,9 @@ int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st) {
 extern "C" int ss_debug_attn_trace(unsigned long long* out) {
   cudaDeviceSynchronize();
   return cudaMemcpyFromSymbol(out, ss::g_at, sizeof(ss::g_at)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int ss_debug_attn_tiles(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, ss::g_att, sizeof(ss::g_att)) == cudaSuccess ? 0 : -1;
 }
 #endif

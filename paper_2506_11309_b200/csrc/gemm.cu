@@ -46,6 +46,14 @@ struct GemmCfg {
 #endif
   static constexpr int SMEM = STAGES * UBYTES + 1024;
   static constexpr int KPARTS = NCW / 8;
+  // W4: a warp owns two 16-row tiles x one 128-deep group of each unit, so the
+  // B fragments it loads serve two MMAs (half the activation reads of the
+  // one-tile-per-warp mapping)
+#ifdef SS_EXP_NOPAIR
+  static constexpr bool PAIR = false;
+#else
+  static constexpr bool PAIR = WFMT == 0 && NCW == 8;
+#endif
 #ifdef SS_EXP_NACC
   static constexpr int NACC = SS_EXP_NACC;
 #else
@@ -174,6 +182,9 @@ __device__ void epi_ar_recv(const EpiArgs& e, int tg, int T, float* ss) {
       if (p < e.P && ll_try_load(src0 + p * pstride, flag, d1[p], d2[p])) ready |= 1u << p;
     const unsigned all = (1u << e.P) - 1u;
     long spins = 0;
+#ifdef SS_EXP_NOPOLL
+    ready = all;  // timing experiment: take whatever the first loads returned
+#endif
     while (ready != all) {
 #pragma unroll
       for (int p = 0; p < kMaxPeers; ++p)
@@ -463,11 +474,16 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   }
 
   // ---------------- consumers
-  const int tile = warp & 7, part = warp >> 3;
+  // tile = 16-row tile of this warp (pair mode: first of its two tiles)
+  const int tile = C::PAIR ? 2 * (warp & 3) : (warp & 7), part = C::PAIR ? 0 : (warp >> 3);
+  const int pgrp = warp >> 2;  // pair mode: the warp's 128-deep group of each unit
   const int gq = lane >> 2, tq = lane & 3;
-  float acc[NT][4];
+  float acc[NT][4], acc1[NT][4];
 #pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  for (int n = 0; n < NT; ++n) {
+    acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+    acc1[n][0] = acc1[n][1] = acc1[n][2] = acc1[n][3] = 0.f;
+  }
   int s = 0;
   uint32_t ph = 0;
   int cur_tg = -1, nst = 0;
@@ -506,6 +522,55 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         //   rows g  : s * (acc - (1024 + z) X)          = s * sum (q - z) x
         //   rows g+8: s/16 * (acc - (1024 + 16 z) X)    = s * sum (q - z) x
         // exact integer weights, no per-weight subtract (R3, DESIGN "W4 GEMM").
+        if constexpr (C::PAIR) {
+          const int grp = pgrp;
+          uint32_t wa[2][8];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const uint4 w0 = lds128(sst + o_w + i * 2048 + (grp * 2) * 512);
+            const uint4 w1 = lds128(sst + o_w + i * 2048 + (grp * 2 + 1) * 512);
+            wa[i][0] = w0.x; wa[i][1] = w0.y; wa[i][2] = w0.z; wa[i][3] = w0.w;
+            wa[i][4] = w1.x; wa[i][5] = w1.y; wa[i][6] = w1.z; wa[i][7] = w1.w;
+          }
+          float cg[2][NT][4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) cg[i][n][0] = cg[i][n][1] = cg[i][n][2] = cg[i][n][3] = 0.f;
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) {  // pairs of k16 steps inside the group
+            uint4 bb[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) bb[n] = lds128(sst + o_b + ((grp * 4 + jp) * NT + n) * 512);
+#pragma unroll
+            for (int js = 0; js < 2; ++js)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                uint32_t a[4];
+                dequant8(wa[i][jp * 2 + js], a);
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+                  mma_f16_16816(cg[i][n], a, js ? bb[n].z : bb[n].x, js ? bb[n].w : bb[n].y);
+              }
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const uint32_t zb = lds8(sst + o_z + i * 16 + grp * 8), sp = lds32(sst + o_sc + i * 64 + grp * 32);
+            const float c0 = __uint_as_float(0x44800000u | ((zb & 15u) << 13));
+            const float c8 = __uint_as_float(0x44800000u | ((zb >> 4) << 17));
+            const float s0 = __uint_as_float(sp << 16);
+            const float s8 = __uint_as_float(sp & 0xFFFF0000u) * 0.0625f;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const float2 X = lds64f(sst + o_x + (grp * 8 * NT + n * 8) * 4);
+              float* ac = i ? acc1[n] : acc[n];
+              ac[0] = fmaf(s0, fmaf(-c0, X.x, cg[i][n][0]), ac[0]);
+              ac[1] = fmaf(s0, fmaf(-c0, X.y, cg[i][n][1]), ac[1]);
+              ac[2] = fmaf(s8, fmaf(-c8, X.x, cg[i][n][2]), ac[2]);
+              ac[3] = fmaf(s8, fmaf(-c8, X.y, cg[i][n][3]), ac[3]);
+            }
+          }
+        } else {
 #pragma unroll
         for (int gi = 0; gi < 2 / C::KPARTS; ++gi) {
         const int grp = part + gi;  // this warp's 128-deep group(s) of the unit
@@ -554,6 +619,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
           acc[n][3] = fmaf(s8, fmaf(-c8, X.y, c[3]), acc[n][3]);
         }
         }  // gi
+        }  // !PAIR
       } else if (WFMT == 1) {
         // bf16 LM head: this warp's k16 pair jp = part of the 64-deep unit
         const uint4* wl = reinterpret_cast<const uint4*>(stw) + tile * 128;
@@ -591,6 +657,11 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         red_add_v2(base + n * 8 + 2 * tq, acc[n][0], acc[n][1]);
         red_add_v2(base + 8 * TP + n * 8 + 2 * tq, acc[n][2], acc[n][3]);
         acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+        if constexpr (C::PAIR) {  // the warp's second tile
+          red_add_v2(base + 16 * TP + n * 8 + 2 * tq, acc1[n][0], acc1[n][1]);
+          red_add_v2(base + 24 * TP + n * 8 + 2 * tq, acc1[n][2], acc1[n][3]);
+          acc1[n][0] = acc1[n][1] = acc1[n][2] = acc1[n][3] = 0.f;
+        }
       }
     }
     // hand the flush to the signaler lane: the block-scope release orders this

@@ -35,3 +35,16 @@ names = ["entry", "pdl", "q", "loop_end", "fenced", "meet", "merged"]
 for e, n in enumerate(names):
     v = a[:, e] - t0
     print(f"{n:9s} min {v.min():7d} p50 {int(np.median(v)):7d} max {v.max():7d}")
+
+tb = (C.c_ulonglong * (256 * 16))()
+L.ss_debug_attn_tiles(tb)
+tt = np.array(tb, dtype=np.int64).reshape(256, 16)[:, 0::2]
+tt = tt[a.shape[0] and slice(0, a.shape[0])]
+q = a[:, 2]
+for i in range(5):
+    col = tt[:, i]
+    m = col > 0
+    if not m.any():
+        break
+    d = (col[m] - q[m])
+    print(f"tile {i} wait done after q: min {d.min():6d} p50 {int(np.median(d)):6d} max {d.max():6d} ns")

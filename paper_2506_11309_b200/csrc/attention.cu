@@ -17,13 +17,17 @@
 // thread blocks or extra kernel launches"): the CTAs of one kv head meet at a
 // flag counter and each then merges a slice of the rows by log-sum-exp,
 // writing fp16 straight into the O-projection's fragment-ordered input.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "kernels.h"
 
+namespace cg = cooperative_groups;
+
 namespace ss {
 
-template <int D, int RB>
+template <int D, int RB, bool CL = false>
 struct AttnCfg {
   static constexpr int KS = (8 / RB) < 1 ? 1 : ((8 / RB) > 4 ? 4 : (8 / RB));  // key slices
   static constexpr int WARPS = RB * KS;
@@ -31,10 +35,14 @@ struct AttnCfg {
   static constexpr int KEYS = kKvTile / KS;   // keys per warp per tile (64, 32 or 16)
   static constexpr int NTK = KEYS / 8;        // score n-tiles per warp
   static constexpr int TILE_ELEMS = kKvTile * D;
-  static constexpr int NBUF = 4;              // K/V tiles in flight (a CTA's whole range at L=4K)
+  // K/V tiles in flight: a CTA's whole range at L=4K; the cluster variant
+  // keeps 2 so that two CTAs fit an SM (16-CTA clusters must be co-resident)
+  static constexpr int NBUF = CL ? 2 : 4;
   static constexpr size_t SMEM = (size_t)ROWS * D * 2 + 2 * NBUF * (size_t)TILE_ELEMS * 2;
-  // the in-CTA key-slice merge reuses the K/V ring
+  // the in-CTA key-slice merge (and the cluster variant's published partial
+  // plus its merge weights) reuse the K/V ring
   static_assert((size_t)(KS - 1) * ROWS * (D + 2) * 4 <= 2 * NBUF * (size_t)TILE_ELEMS * 2, "merge buffer");
+  static_assert(!CL || (size_t)ROWS * D * 4 + 2 * 16 * 16 * 4 <= 2 * NBUF * (size_t)TILE_ELEMS * 2, "cluster buffer");
 };
 
 #ifdef SS_ATTN_TRACE
@@ -49,9 +57,12 @@ SS_DEV unsigned long long gtime_at() {
 #else
 #define ATR(ev) do {} while (0)
 #endif
-template <int D, int RB>
-__global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(AttnArgs a) {
-  using C = AttnCfg<D, RB>;
+// CL = true: the S splits of a (kv head, row chunk) form one thread-block
+// cluster and merge their partials through distributed shared memory (no
+// global workspace, no grid-level meet); CL = false: global workspace merge.
+template <int D, int RB, bool CL>
+__global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel(AttnArgs a) {
+  using C = AttnCfg<D, RB, CL>;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NBUF = C::NBUF;
   __shared__ __align__(8) uint64_t full[NBUF];
@@ -283,6 +294,83 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
       }
     }
   }
+  if constexpr (CL) {
+    // ---- publish the split's partial in shared memory, merge a slice of the
+    // rows from every split of the cluster (DSMEM), R11 log-sum-exp
+    __shared__ float2 s_pml[256];                      // (m, l) per row
+    float* pub = reinterpret_cast<float*>(Ks);         // [ROWS][D] fp32
+    __syncthreads();                                   // the in-CTA merge is done reading the ring
+    if (ks == 0) {
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        *reinterpret_cast<float2*>(pub + ra * D + n * 8 + 2 * tq) = make_float2(o[n][0], o[n][1]);
+        *reinterpret_cast<float2*>(pub + rbb * D + n * 8 + 2 * tq) = make_float2(o[n][2], o[n][3]);
+      }
+      if (tq == 0) {
+        s_pml[ra] = make_float2(mA, lA);
+        s_pml[rbb] = make_float2(mB, lB);
+      }
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    ATR(5);
+    float* s_w = reinterpret_cast<float*>(Ks) + ROWS * D;  // [rows_here][S] weights (after pub)
+    const int rows_per = (ROWS + S - 1) / S;
+    const int r_first = split * rows_per, r_end = min(ROWS, r_first + rows_per);
+    const int nr = r_end > r_first ? r_end - r_first : 0;
+    for (int i = threadIdx.x; i < nr * S; i += NTHR) {
+      const int rr = i / S, p2 = i - rr * S;
+      const float2* pml = cl.map_shared_rank(s_pml, p2);
+      const float2 v = pml[r_first + rr];
+      s_w[i] = v.x;
+      s_w[nr * S + i] = v.y;
+    }
+    __syncthreads();
+    for (int rr = warp; rr < nr; rr += C::WARPS) {  // one warp per row: m*, l*, weights
+      float mx = -INFINITY;
+      for (int p2 = lane; p2 < S; p2 += 32) mx = fmaxf(mx, s_w[rr * S + p2]);
+      mx = warp_max(mx);
+      float l = 0.f;
+      for (int p2 = lane; p2 < S; p2 += 32) {
+        const float ms = s_w[rr * S + p2];
+        const float w = (ms == -INFINITY) ? 0.f : exp2f(ms - mx);
+        l += w * s_w[nr * S + rr * S + p2];
+        s_w[rr * S + p2] = w;
+      }
+      l = warp_sum(l);
+      __syncwarp();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      for (int p2 = lane; p2 < S; p2 += 32) s_w[rr * S + p2] *= inv;
+    }
+    __syncthreads();
+    for (int itm = threadIdx.x; itm < nr * (D / 4); itm += NTHR) {
+      const int r = r_first + itm / (D / 4), c4 = itm % (D / 4);
+      const int m = m0 + r;
+      if (m >= Mrows) continue;
+      const float* wr = s_w + (r - r_first) * S;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+      for (int p2 = 0; p2 < S; ++p2) {
+        const float w = wr[p2];
+        const float4 ov = *reinterpret_cast<const float4*>(cl.map_shared_rank(pub, p2) + r * D + 4 * c4);
+        acc.x += w * ov.x;
+        acc.y += w * ov.y;
+        acc.z += w * ov.z;
+        acc.w += w * ov.w;
+      }
+      const int t = m / G, hq = kvh * G + (m % G);
+      const int k = hq * D + 4 * c4;
+      const uint32_t p01 = pack_half2(acc.x, acc.y), p23 = pack_half2(acc.z, acc.w);
+      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k, a.NT)) = p01;
+      *reinterpret_cast<uint32_t*>(a.act_out + act_frag_offset(t, k + 2, a.NT)) = p23;
+      // group sum X of the O-projection input (slots zeroed by the QKV kernel)
+      atomicAdd(reinterpret_cast<float*>(a.act_out + act_xsum_offset(t, k >> 7, a.NT)),
+                half2_sum(p01) + half2_sum(p23));
+    }
+    ATR(6);
+    cl.sync();  // peers may still be reading this CTA's partial
+    return;
+  }
   // ---- the split's partial -> workspace
   if (ks == 0) {
     float* ws = a.ws + (((size_t)grp * P + split) * 256) * D;
@@ -382,13 +470,13 @@ __global__ void __launch_bounds__(AttnCfg<D, RB>::WARPS * 32, 1) attn_kernel(Att
   }
 }
 
-template <int D, int RB>
+template <int D, int RB, bool CL>
 static int occ_of() {
   static int occ = -1;
-  using C = AttnCfg<D, RB>;
+  using C = AttnCfg<D, RB, CL>;
   if (occ < 0) {
-    cudaFuncSetAttribute(attn_kernel<D, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_kernel<D, RB>, C::WARPS * 32, C::SMEM);
+    cudaFuncSetAttribute(attn_kernel<D, RB, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_kernel<D, RB, CL>, C::WARPS * 32, C::SMEM);
     if (occ < 1) occ = 1;
   }
   return occ;
@@ -401,14 +489,75 @@ static int rb_for(int G, int NT) {
   return r;
 }
 
+constexpr int kAttnCluster = 16;  // splits per (kv head, row chunk) in the cluster variant (non-portable size)
+
+// Whether 16-CTA clusters of the cluster variant can be scheduled (queried once).
+template <int D, int RB>
+static bool cluster_ok() {
+  static int ok = -1;
+  if (ok < 0) {
+    using C = AttnCfg<D, RB, true>;
+    auto k = attn_kernel<D, RB, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kAttnCluster, 1, 1);
+    cfg.blockDim = dim3(C::WARPS * 32, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kAttnCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    ok = (cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n >= 1) ? 1 : 0;
+    cudaGetLastError();
+  }
+  return ok == 1;
+}
+
 template <int D, int RB>
 static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
-  using C = AttnCfg<D, RB>;
   const int rows = a.G * a.NT * 8;
-  const int Z = (rows + C::ROWS - 1) / C::ROWS;
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-  int cap = n_sm * occ_of<D, RB>();
+  // SS_ATTN_CLUSTER = 0 / 1 forces the variant (experiments)
+  static const int force = getenv("SS_ATTN_CLUSTER") ? atoi(getenv("SS_ATTN_CLUSTER")) : -1;
+  if constexpr (RB <= 4) {
+    using C = AttnCfg<D, RB, true>;
+    // The cluster variant has 16 CTAs per (kv head, row chunk): it wins when
+    // there are few of those (TP 4-8 shards, <= 2 kv heads per GPU: measured
+    // 7.33 -> 7.04 ms per TP8-rank step); with 8 kv heads (TP 1) the global
+    // merge over 18 splits per head is faster (more CTAs, deeper K/V ring).
+    // Uncapped launches only (fake-peer TP caps the CTAs per rank).
+    const int groups = a.Hkv_l * ((rows + C::ROWS - 1) / C::ROWS);
+    const bool want = force >= 0 ? force == 1 : groups <= 2;
+    if (want && max_ctas <= 0 && cluster_ok<D, RB>()) {
+      a.splits = kAttnCluster;
+      a.zchunks = (rows + C::ROWS - 1) / C::ROWS;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kAttnCluster, a.Hkv_l, a.zchunks);
+      cfg.blockDim = dim3(C::WARPS * 32, 1, 1);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kAttnCluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = getenv("SS_NO_PDL") ? 1 : 2;
+      cudaLaunchKernelEx(&cfg, attn_kernel<D, RB, true>, a);
+      return 1;
+    }
+  }
+  using C = AttnCfg<D, RB, false>;
+  const int Z = (rows + C::ROWS - 1) / C::ROWS;
+  int cap = n_sm * occ_of<D, RB, false>();
   if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
   int S = cap / (a.Hkv_l * Z);
   const int max_tiles = (a.max_ctx_pad + kKvTile - 1) / kKvTile;
@@ -417,7 +566,7 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
   if (S < 1) S = 1;
   a.splits = S;
   a.zchunks = Z;
-  launch_pdl(attn_kernel<D, RB>, dim3(S, a.Hkv_l, Z), dim3(C::WARPS * 32), C::SMEM, st, a);
+  launch_pdl(attn_kernel<D, RB, false>, dim3(S, a.Hkv_l, Z), dim3(C::WARPS * 32), C::SMEM, st, a);
   return 1;
 }
 
@@ -435,11 +584,14 @@ static int launch_d(const AttnArgs& a, int max_ctas, cudaStream_t st) {
 template <int D>
 static void warm_d() {
   cudaFuncAttributes at;
-  cudaFuncGetAttributes(&at, attn_kernel<D, 1>);
-  cudaFuncGetAttributes(&at, attn_kernel<D, 2>);
-  cudaFuncGetAttributes(&at, attn_kernel<D, 4>);
-  cudaFuncGetAttributes(&at, attn_kernel<D, 8>);
-  cudaFuncGetAttributes(&at, attn_kernel<D, 16>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 1, false>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 2, false>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 4, false>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 8, false>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 16, false>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 1, true>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 2, true>);
+  cudaFuncGetAttributes(&at, attn_kernel<D, 4, true>);
 }
 // see warm_misc_kernels (misc.cu)
 void warm_attention_kernels() {

@@ -157,7 +157,9 @@ __device__ void epi_ar_send(const EpiArgs& e, int tg, const float* acc, int T) {
       // loopback emulation (one rank on one GPU, timing only): every rank
       // slot of the own buffer receives this rank's partial
       const int slot = e.loopback ? p : e.rank;
-      const size_t line = (((size_t)(e.ar_seq & 1) * e.P + slot) * e.n_tg_total + tg) * 128 * 32 + (size_t)r * 32 + tp;
+      // dense line layout: PP = 4 NT token pairs per row (the launch's width)
+      const size_t line = (((size_t)(e.ar_seq & 1) * e.P + slot) * e.n_tg_total + tg) * 128 * (4 * NT) +
+                          (size_t)r * (4 * NT) + tp;
       ll_store(reinterpret_cast<uint4*>(e.peer_recv[p]) + line, __float_as_uint(a), __float_as_uint(b), flag);
     }
   }
@@ -167,14 +169,16 @@ __device__ void epi_ar_send(const EpiArgs& e, int tg, const float* acc, int T) {
 // partial of the tile-group, sum in rank order (identical on all ranks), add.
 // The P lines of an item are loaded together (independent L2 / NVLink round
 // trips in flight) and only lines whose flags are not there yet are re-polled.
+template <int NT>
 __device__ void epi_ar_recv(const EpiArgs& e, int tg, int T, float* ss) {
+  constexpr int PP = 4 * NT;  // token pairs per row in the LL line layout (epi_ar_send)
   const uint32_t flag = e.st->epoch + e.ar_seq;
   const int pairs = (T + 1) >> 1;
   for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
     const int tp = idx >> 7, r = idx & 127;  // warp = 32 rows of one token pair
     const uint4* src0 = reinterpret_cast<const uint4*>(e.recv) +
-                        (((size_t)(e.ar_seq & 1) * e.P) * e.n_tg_total + tg) * 128 * 32 + (size_t)r * 32 + tp;
-    const size_t pstride = (size_t)e.n_tg_total * 128 * 32;
+                        (((size_t)(e.ar_seq & 1) * e.P) * e.n_tg_total + tg) * 128 * PP + (size_t)r * PP + tp;
+    const size_t pstride = (size_t)e.n_tg_total * 128 * PP;
     uint32_t d1[kMaxPeers], d2[kMaxPeers];
     unsigned ready = 0;
 #pragma unroll
@@ -726,7 +730,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         g_ts[(blockIdx.x * 8 + 3) & 0xFFFF] = gtimer();
 #endif
       if (threadIdx.x < 256)
-        for (int i = 0; i < ndone; ++i) epi_ar_recv(g.epi, s_done_list[i], T, g.norm_out ? g.ss : nullptr);
+        for (int i = 0; i < ndone; ++i) epi_ar_recv<NT>(g.epi, s_done_list[i], T, g.norm_out ? g.ss : nullptr);
     }
     TS(5);
     if (g.norm_out && ndone > 0) {

@@ -138,6 +138,10 @@ SS_DEV void bulk_g2s_nohint(void* dst, const void* src, uint32_t bytes, uint64_t
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Bulk prefetch of global memory into L2 (no shared memory, no completion).
+SS_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 SS_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

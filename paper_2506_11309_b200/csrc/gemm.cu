@@ -358,7 +358,8 @@ SS_DEV unsigned long long gtimer() {
   return t;
 }
 __device__ int g_ts_kind = -1;
-#define TS(slot) do { if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && (WFMT == 1 || g.epi.layer == 0)) g_ts[(blockIdx.x * 8 + (slot)) & 0xFFFF] = gtimer(); } while (0)
+__device__ int g_ts_par = -1;  // RESID: 0 = O-proj, 1 = down, -1 = any
+#define TS(slot) do { if (threadIdx.x == 0 && blockIdx.x < 1024 && g.epi.kind == g_ts_kind && (WFMT == 1 || g.epi.layer == 0) && (g_ts_par < 0 || (g.epi.ar_seq & 1) == g_ts_par)) g_ts[(blockIdx.x * 8 + (slot)) & 0xFFFF] = gtimer(); } while (0)
 #else
 #define TS(slot) do {} while (0)
 #endif
@@ -824,7 +825,10 @@ int launch_gemm(const GemmArgs& g, int wfmt, int NT, int max_ctas, cudaStream_t 
 
 #ifdef SS_EXP_TIMING
 extern "C" int ss_debug_gemm_set_kind(int kind) {
-  return cudaMemcpyToSymbol(ss::g_ts_kind, &kind, 4) == cudaSuccess ? 0 : -1;
+  const int par = kind >= 10 ? kind / 10 - 1 : -1;  // 11 = O-proj (RESID, parity 0), 21 = down
+  const int k = kind % 10;
+  if (cudaMemcpyToSymbol(ss::g_ts_par, &par, 4) != cudaSuccess) return -1;
+  return cudaMemcpyToSymbol(ss::g_ts_kind, &k, 4) == cudaSuccess ? 0 : -1;
 }
 extern "C" int ss_debug_gemm_timestamps(unsigned long long* out, int n) {
   if (n > (1 << 16)) n = 1 << 16;

@@ -44,7 +44,8 @@ struct GemmCfg {
 #else
   static constexpr int STAGES = (UBYTES <= 26 * 1024) ? 3 : 4;
 #endif
-  static constexpr int SMEM = STAGES * UBYTES + 1024;
+  // no slack: 3 CTAs of the T <= 16 configurations must fit one SM's 228 KB
+  static constexpr int SMEM = STAGES * UBYTES;
   static constexpr int KPARTS = NCW / 8;
   // W4: a warp owns two 16-row tiles x one 128-deep group of each unit, so the
   // B fragments it loads serve two MMAs (half the activation reads of the
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   constexpr int NCW = C::NCW, NCT = NCW * 32;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
-  __shared__ int s_done_list[256];
+  __shared__ int s_done_list[64];  // tile-groups this CTA finalises (<= tile-groups its range touches)
   __shared__ int s_ndone;
   __shared__ int s_flushed;          // consumer-warp flushes so far (signaler)
   __shared__ int s_unit[C::STAGES];  // tile-group of each ring slot (-1 = no more work)
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         } while (v < NCW * k);
         fence_acq_rel_gpu();
         const int old = atomicAdd(&g.counters[tg], nst);
-        if (old + nst == g.S) s_done_list[s_ndone++] = tg;
+        if (old + nst == g.S && s_ndone < 64) s_done_list[s_ndone++] = tg;
       }
     }
     __syncwarp();

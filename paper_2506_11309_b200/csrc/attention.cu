@@ -37,7 +37,11 @@ struct AttnCfg {
   static constexpr int TILE_ELEMS = kKvTile * D;
   // K/V tiles in flight: a CTA's whole range at L=4K; the cluster variant
   // keeps 2 so that two CTAs fit an SM (16-CTA clusters must be co-resident)
+#ifdef SS_EXP_ANBUF
+  static constexpr int NBUF = CL ? 2 : SS_EXP_ANBUF;
+#else
   static constexpr int NBUF = CL ? 2 : 4;
+#endif
   static constexpr size_t SMEM = (size_t)ROWS * D * 2 + 2 * NBUF * (size_t)TILE_ELEMS * 2;
   // the in-CTA key-slice merge (and the cluster variant's published partial
   // plus its merge weights) reuse the K/V ring
@@ -557,7 +561,11 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
   }
   using C = AttnCfg<D, RB, false>;
   const int Z = (rows + C::ROWS - 1) / C::ROWS;
+#ifdef SS_EXP_AOCC1
+  int cap = n_sm;  // experiment: one split per SM even if two CTAs would fit
+#else
   int cap = n_sm * occ_of<D, RB, false>();
+#endif
   if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
   int S = cap / (a.Hkv_l * Z);
   const int max_tiles = (a.max_ctx_pad + kKvTile - 1) / kKvTile;

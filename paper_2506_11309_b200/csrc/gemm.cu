@@ -41,6 +41,8 @@ struct GemmCfg {
   // ring depth: NT <= 2 -> 3 stages (~63-76 KB, 3 CTAs/SM); larger NT -> 4
 #ifdef SS_EXP_STAGES
   static constexpr int STAGES = SS_EXP_STAGES;
+#elif defined(SS_EXP_STAGES_WIDE)
+  static constexpr int STAGES = (UBYTES <= 26 * 1024) ? 3 : SS_EXP_STAGES_WIDE;
 #else
   static constexpr int STAGES = (UBYTES <= 26 * 1024) ? 3 : 4;
 #endif
@@ -65,7 +67,7 @@ struct GemmCfg {
 #ifdef SS_EXP_MINB
   static constexpr int MINB = SS_EXP_MINB;
 #else
-  static constexpr int MINB = STAGES == 3 ? 3 : 1;
+  static constexpr int MINB = SMEM <= 75 * 1024 ? 3 : (SMEM <= 112 * 1024 ? 2 : 1);
 #endif
 };
 

@@ -72,34 +72,57 @@ struct GemmCfg {
 };
 
 // ---------------------------------------------------------------- epilogues
+// The epilogues run after the main loop on the CTA that completed the
+// tile-group: their accumulator reads are L2 round trips, so each thread
+// issues the loads of EB items before using any of them.
+constexpr int EB = 4;
+
 template <int NT>
 __device__ void epi_qkv(const EpiArgs& e, int tg, const float* acc, int T) {
   const int TP = NT * 8;
   const int d = e.d, half = d >> 1;
   const int nq = e.Hq_l * d, nk = e.Hkv_l * d;
   const int L = e.st->L;
-  for (int idx = threadIdx.x; idx < 128 * T; idx += 256) {
-    int r = idx / T, t = idx - r * T;
-    int row = tg * 128 + r;
-    float v = __ldcg(acc + (size_t)r * TP + t);
-    int j = row % d;
-    int pos = e.st->pos[t];
-    if (row < nq + nk) {  // q or k: rotate-half RoPE (R2)
-      int pr = (j < half) ? r + half : r - half;
-      float pv = __ldcg(acc + (size_t)pr * TP + t);
-      float2 cs = e.rope_cs[(size_t)pos * half + (j % half)];
-      v = (j < half) ? (v * cs.x - pv * cs.y) : (v * cs.x + pv * cs.y);
+  const int n = 128 * T;
+  for (int i0 = threadIdx.x; i0 < n; i0 += 256 * EB) {
+    float v[EB], pv[EB];
+    float2 cs[EB];
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      const int idx = i0 + 256 * b;
+      v[b] = pv[b] = 0.f;
+      cs[b] = make_float2(1.f, 0.f);
+      if (idx < n) {
+        const int r = idx / T, t = idx - r * T;
+        const int row = tg * 128 + r, j = row % d;
+        v[b] = __ldcg(acc + (size_t)r * TP + t);
+        if (row < nq + nk) {
+          const int pr = (j < half) ? r + half : r - half;
+          pv[b] = __ldcg(acc + (size_t)pr * TP + t);
+          cs[b] = e.rope_cs[(size_t)e.st->pos[t] * half + (j % half)];
+        }
+      }
     }
-    const uint16_t b = f32_to_f16_bits(v);  // q and the KV cache are fp16
-    if (row < nq) {
-      int hq = row / d, kvh = hq / e.G, jj = hq - kvh * e.G;
-      const int m = t * e.G + jj;  // attention row; 16-byte chunks swizzled by m % 8
-      e.qbuf[((size_t)kvh * (e.G * SS_MAX_TREE) + m) * d + ((((j >> 3) ^ (m & 7))) << 3) + (j & 7)] = b;
-    } else {
-      int kvh = (row < nq + nk) ? (row - nq) / d : (row - nq - nk) / d;
-      uint16_t* c = (row < nq + nk) ? e.kc : e.vc;
-      size_t base = ((size_t)e.layer * e.Hkv_l + kvh) * e.max_ctx_pad * d;
-      c[base + kv_elem_offset(L + t, j, d)] = b;
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      const int idx = i0 + 256 * b;
+      if (idx >= n) break;
+      const int r = idx / T, t = idx - r * T;
+      const int row = tg * 128 + r, j = row % d;
+      float x = v[b];
+      if (row < nq + nk)  // q or k: rotate-half RoPE (R2)
+        x = (j < half) ? (x * cs[b].x - pv[b] * cs[b].y) : (x * cs[b].x + pv[b] * cs[b].y);
+      const uint16_t h16 = f32_to_f16_bits(x);  // q and the KV cache are fp16
+      if (row < nq) {
+        const int hq = row / d, kvh = hq / e.G, jj = hq - kvh * e.G;
+        const int m = t * e.G + jj;  // attention row; 16-byte chunks swizzled by m % 8
+        e.qbuf[((size_t)kvh * (e.G * SS_MAX_TREE) + m) * d + ((((j >> 3) ^ (m & 7))) << 3) + (j & 7)] = h16;
+      } else {
+        const int kvh = (row < nq + nk) ? (row - nq) / d : (row - nq - nk) / d;
+        uint16_t* c = (row < nq + nk) ? e.kc : e.vc;
+        const size_t base = ((size_t)e.layer * e.Hkv_l + kvh) * e.max_ctx_pad * d;
+        c[base + kv_elem_offset(L + t, j, d)] = h16;
+      }
     }
   }
 }
@@ -132,14 +155,30 @@ __device__ void epi_resid_local(const EpiArgs& e, int tg, const float* acc, int 
   const int TP = NT * 8;
   // warp = 32 columns of one token: the new residual's squares reduce per
   // warp into the per-token sum the fused RMSNorm needs
-  for (int idx = threadIdx.x; idx < 128 * T; idx += 256) {
-    const int t = idx >> 7, r = idx & 127;
-    float* xp = e.x + (size_t)t * e.h + tg * 128 + r;
-    const float nx = *xp + __ldcg(acc + (size_t)r * TP + t);
-    *xp = nx;
-    if (ss) {
-      const float q = warp_sum(nx * nx);
-      if ((threadIdx.x & 31) == 0) atomicAdd(ss + t, q);
+  const int n = 128 * T;
+  for (int i0 = threadIdx.x; i0 < n; i0 += 256 * EB) {
+    float xv[EB], av[EB];
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      const int idx = i0 + 256 * b;
+      xv[b] = av[b] = 0.f;
+      if (idx < n) {
+        const int t = idx >> 7, r = idx & 127;
+        xv[b] = e.x[(size_t)t * e.h + tg * 128 + r];
+        av[b] = __ldcg(acc + (size_t)r * TP + t);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      const int idx = i0 + 256 * b;
+      if (idx >= n) break;  // warp-uniform (n is a multiple of 128)
+      const int t = idx >> 7, r = idx & 127;
+      const float nx = xv[b] + av[b];
+      e.x[(size_t)t * e.h + tg * 128 + r] = nx;
+      if (ss) {
+        const float q = warp_sum(nx * nx);
+        if ((threadIdx.x & 31) == 0) atomicAdd(ss + t, q);
+      }
     }
   }
 }

@@ -191,18 +191,33 @@ __device__ void epi_ar_send(const EpiArgs& e, int tg, const float* acc, int T) {
   const int TP = NT * 8;
   const uint32_t flag = e.st->epoch + e.ar_seq;
   const int pairs = (T + 1) >> 1;
-  for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
-    int r = idx / pairs, tp = idx - r * pairs;
-    float a = __ldcg(acc + (size_t)r * TP + 2 * tp);
-    float b = __ldcg(acc + (size_t)r * TP + 2 * tp + 1);
-    for (int p = 0; p < e.P; ++p) {
-      // loopback emulation (one rank on one GPU, timing only): every rank
-      // slot of the own buffer receives this rank's partial
-      const int slot = e.loopback ? p : e.rank;
-      // dense line layout: PP = 4 NT token pairs per row (the launch's width)
-      const size_t line = (((size_t)(e.ar_seq & 1) * e.P + slot) * e.n_tg_total + tg) * 128 * (4 * NT) +
-                          (size_t)r * (4 * NT) + tp;
-      ll_store(reinterpret_cast<uint4*>(e.peer_recv[p]) + line, __float_as_uint(a), __float_as_uint(b), flag);
+  const int n = 128 * pairs;
+  for (int i0 = threadIdx.x; i0 < n; i0 += 256 * EB) {
+    float2 v[EB];
+#pragma unroll
+    for (int q = 0; q < EB; ++q) {
+      const int idx = i0 + 256 * q;
+      v[q] = make_float2(0.f, 0.f);
+      if (idx < n) {
+        const int r = idx / pairs, tp = idx - r * pairs;
+        v[q] = __ldcg(reinterpret_cast<const float2*>(acc + (size_t)r * TP + 2 * tp));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EB; ++q) {
+      const int idx = i0 + 256 * q;
+      if (idx >= n) break;
+      const int r = idx / pairs, tp = idx - r * pairs;
+      for (int p = 0; p < e.P; ++p) {
+        // loopback emulation (one rank on one GPU, timing only): every rank
+        // slot of the own buffer receives this rank's partial
+        const int slot = e.loopback ? p : e.rank;
+        // dense line layout: PP = 4 NT token pairs per row (the launch's width)
+        const size_t line = (((size_t)(e.ar_seq & 1) * e.P + slot) * e.n_tg_total + tg) * 128 * (4 * NT) +
+                            (size_t)r * (4 * NT) + tp;
+        ll_store(reinterpret_cast<uint4*>(e.peer_recv[p]) + line, __float_as_uint(v[q].x), __float_as_uint(v[q].y),
+                 flag);
+      }
     }
   }
 }

@@ -18,6 +18,8 @@
 // evenly over a persistent grid (stream-K); partial tiles are reduced with
 // red.global.add.v2.f32 and a per-tile-group arrival counter picks the CTA
 // that runs the epilogue (no extra kernel, no grid barrier).
+#include <cstdio>
+
 #include "common.cuh"
 #include "internal.h"
 #include "kernels.h"
@@ -832,6 +834,12 @@ static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, C::SMEM);
     if (occ < 1) occ = 1;
+    if (getenv("SS_DEBUG_OCC")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, k);
+      fprintf(stderr, "gemm WFMT=%d NT=%d EPI=%d: stages %d, dyn smem %d, static smem %zu, regs %d, CTAs/SM %d\n",
+              WFMT, NT, EPI, C::STAGES, C::SMEM, fa.sharedSizeBytes, fa.numRegs, occ);
+    }
     attr_set = true;
   }
   long U = (long)g.n_tg * g.S;

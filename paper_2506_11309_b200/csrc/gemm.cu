@@ -56,6 +56,8 @@ struct GemmCfg {
   // one-tile-per-warp mapping)
 #ifdef SS_EXP_NOPAIR
   static constexpr bool PAIR = false;
+#elif defined(SS_EXP_PAIRMAXNT)
+  static constexpr bool PAIR = WFMT == 0 && NCW == 8 && NT <= SS_EXP_PAIRMAXNT;
 #else
   static constexpr bool PAIR = WFMT == 0 && NCW == 8;
 #endif

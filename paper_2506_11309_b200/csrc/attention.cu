@@ -539,12 +539,21 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
     const int groups = a.Hkv_l * ((rows + C::ROWS - 1) / C::ROWS);
     const bool want = force >= 0 ? force == 1 : groups <= 2;
     if (want && max_ctas <= 0 && cluster_ok<D, RB>()) {
+      // optional dynamic shared-memory padding (KB) that keeps one cluster
+      // CTA per SM (two would share an SM's tensor pipe)
+      static const int pad_kb = getenv("SS_ATTN_CL_SMEM_KB") ? atoi(getenv("SS_ATTN_CL_SMEM_KB")) : 0;
+      const int smem = std::max((int)C::SMEM, pad_kb * 1024);
+      static int attr_smem = 0;
+      if (smem > attr_smem) {
+        cudaFuncSetAttribute(attn_kernel<D, RB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_smem = smem;
+      }
       a.splits = kAttnCluster;
       a.zchunks = (rows + C::ROWS - 1) / C::ROWS;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(kAttnCluster, a.Hkv_l, a.zchunks);
       cfg.blockDim = dim3(C::WARPS * 32, 1, 1);
-      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
       cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;

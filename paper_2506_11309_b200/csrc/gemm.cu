@@ -847,7 +847,10 @@ static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
   long U = (long)g.n_tg * g.S;
   static const int occ_cap = getenv("SS_GEMM_OCC") ? atoi(getenv("SS_GEMM_OCC")) : 0;  // debugging aid
   int o = (occ_cap > 0 && occ_cap < occ) ? occ_cap : occ;
-  int grid = (int)std::min<long>(U, (long)g.n_sm * o);
+  // optional minimum units per CTA (fewer, longer stream-K ranges: fewer
+  // partial flushes per tile-group for small GEMMs; tuning aid)
+  static const int min_units = getenv("SS_GEMM_MINU") ? std::max(1, atoi(getenv("SS_GEMM_MINU"))) : 1;
+  int grid = (int)std::min<long>((U + min_units - 1) / min_units, (long)g.n_sm * o);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, g);
   return 1;

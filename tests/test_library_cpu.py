@@ -65,4 +65,5 @@ def test_null_args():
     assert L.ss_verify_tree(None, None, None, 1, None, None, None) == -1
     assert L.ss_commit_kv(None, None, 1, None) == -1
     assert L.ss_committed_len(None) == -1
+    assert L.ss_import_loopback(None) == -1
     assert L.ss_destroy(None) == 0

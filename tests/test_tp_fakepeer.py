@@ -107,3 +107,21 @@ def test_fakepeer_tp_autocommit_many_steps():
         assert [sh.L for sh in shards] == [L + total] * 2
     for sh in shards:
         sh.close()
+
+
+def test_loopback_emulation_runs():
+    """ss_import_loopback (bench.py tp_emulated): one rank of a TP group runs its whole
+    step alone -- the fused all-reduce and argmax exchange complete without peers."""
+    import paper_2506_11309_b200 as pkg
+    cfg = synth.CONFIGS["small-tp"]
+    sh = pkg.Shard(cfg, 0, 2, 0, max_ctx=64 + 128, max_tree=16)
+    sh.synth_weights(0)
+    sh.synth_prefix_kv(1, 64)
+    sh.import_loopback()
+    for T in (1, 8, 13):
+        tokens, parents = synth.tree_paperlike(T, cfg.vocab, np.random.default_rng(T))
+        r = sh.verify(tokens, parents)
+        assert r["status"] == 0
+        assert all(0 <= a < cfg.vocab for a in r["argmax"])
+        sh.commit_accepted()
+    sh.close()

@@ -581,6 +581,15 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
   if (S > max_tiles) S = max_tiles;
   if (S > 64) S = 64;  // workspace holds 64 partials (one per split) per row chunk
   if (S < 1) S = 1;
+  // fewest splits with the same longest split (same critical path, fewer
+  // partials to merge), from the committed length the host knows
+  if (a.L_hint > 0) {
+    const int nt = (a.L_hint + a.NT * 8 + kKvTile - 1) / kKvTile;
+    const int per = (nt + S - 1) / S;
+    const int S2 = (nt + per - 1) / per;
+    static const bool no_bal = getenv("SS_ATTN_NO_BALANCE") != nullptr;  // experiment switch
+    if (!no_bal && S2 >= 1 && S2 < S) S = S2;
+  }
   a.splits = S;
   a.zchunks = Z;
   launch_pdl(attn_kernel<D, RB, false>, dim3(S, a.Hkv_l, Z), dim3(C::WARPS * 32), C::SMEM, st, a);

@@ -81,6 +81,7 @@ struct AttnArgs {
   DevState* st = nullptr;
   int layer = 0, Hkv_l = 0, G = 1, d = 128, max_ctx_pad = 0, NT = 1;
   int splits = 1, zchunks = 1;
+  int L_hint = 0;  // committed length at enqueue time (host view; 0 = unknown): split balancing only
   const uint16_t* qbuf = nullptr;
   const uint16_t* kc = nullptr;
   const uint16_t* vc = nullptr;

@@ -777,6 +777,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     a.d = c.head_dim;
     a.max_ctx_pad = s->max_ctx_pad;
     a.NT = NT;
+    a.L_hint = s->L_known ? s->L_host : 0;
     a.qbuf = s->qbuf;
     a.kc = s->kcache;
     a.vc = s->vcache;

@@ -9,15 +9,20 @@
 //                accept walk (a11) in the CTA that finishes last.
 //
 // Design (B200): weights stream HBM -> SMEM through the TMA bulk engine
-// (cp.async.bulk + mbarrier ring, one producer warp), 8 consumer warps
-// dequantise int4 -> bf16 in registers ((128+q) via lop3, minus (128+z) with
-// one bf16x2 subtract: exact integers) and issue mma.sync m16n8k16 with the
-// weights as the M=16 operand and the T tree tokens as N=8 columns.  The
-// group scale is applied in fp32 after each 128-deep group, so no weight is
-// ever rounded (R3).  Work = (tile-group of 128 rows) x (K stage) units split
-// evenly over a persistent grid (stream-K); partial tiles are reduced with
-// red.global.add.v2.f32 and a per-tile-group arrival counter picks the CTA
-// that runs the epilogue (no extra kernel, no grid barrier).
+// (cp.async.bulk + mbarrier ring; producer warp lane 0), 8 consumer warps --
+// each owns two 16-row tiles x one 128-deep AWQ group of every 128 x 256
+// unit, so one load of B fragments feeds two MMAs -- turn int4 nibbles into
+// fp16 (1024 + q) / (1024 + 16 q) with mul.hi + lop3 (exact integers) and
+// issue mma.sync m16n8k16 with the weights as the M=16 operand and the T tree
+// tokens as the N=8 columns.  Per group, s (acc - (1024 + z) X) in fp32 (X =
+// the group's activation sum from the producer): no weight is ever rounded
+// (R3, R19, R20).  Work = (tile-group of 128 rows) x (K stage) units in
+// contiguous static ranges over a persistent grid (stream-K); partial tiles
+// are reduced with red.global.add.v2.f32; the producer warp's lane 1 (flush
+// signaler) publishes a CTA's share of a tile-group with one GPU-scope fence
+// + arrival count, and the last arriver runs the epilogue (no extra kernel).
+// The tcgen05 (TMEM A operand) variant of this kernel lives on the
+// `tcgen05-w4` branch.
 #include <cstdio>
 
 #include "common.cuh"
@@ -642,7 +647,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
         const int grp = part + gi;  // this warp's 128-deep group(s) of the unit
         const uint4 w0 = lds128(sst + o_w + (grp * 2) * 512), w1 = lds128(sst + o_w + (grp * 2 + 1) * 512);
         const uint32_t wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        // NACC accumulator sets (even / odd k16 steps) shorten the MMA dependency chain
+        // NACC accumulator sets (even / odd k16 steps) -- 1 in the product (see GemmCfg)
         float cg[C::NACC][NT][4];
 #pragma unroll
         for (int h = 0; h < C::NACC; ++h)

@@ -347,6 +347,7 @@ def run_ours(args, cfg):
                             "avg_launch_us": per * 1e3, "share_of_step": gu_ms / tot if tot else None}
         line["kernel_times_us"] = {k: {"total": v[0] * 1e3, "launches": v[1]} for k, v in prof.items()}
     if world == 1 and not args.no_tp_emulate:
+        line["decode_planted"] = decode_planted(sh, cfg, T, L)
         line["tp_emulated"] = tp_emulated(args, cfg, local, dev, peak)
     if rank == 0 and not args.no_cpu_baseline:
         smp = OracleSample(cfg, T, L)
@@ -360,6 +361,74 @@ def run_ours(args, cfg):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def planted_tree(seq, pos, d, T, V, rng):
+    """Tree rooted at seq[pos] whose first d nodes after the root are the chain
+    seq[pos+1 .. pos+d] (the target's own greedy continuation, so exactly d draft
+    tokens are accepted), padded to T nodes with random leaves (depth <= 7, P:166;
+    siblings distinct)."""
+    toks, par, depth = [int(seq[pos])], [-1], [0]
+    for i in range(1, d + 1):
+        toks.append(int(seq[pos + i]))
+        par.append(i - 1)
+        depth.append(i)
+    while len(toks) < T:
+        p = int(rng.integers(0, len(toks)))
+        if depth[p] >= 7:
+            continue
+        sib = {toks[j] for j in range(len(toks)) if par[j] == p}
+        if p < d:
+            sib.add(int(seq[pos + p + 1]))  # never a second copy of the planted child
+        t = int(rng.integers(0, V))
+        if t in sib:
+            continue
+        toks.append(t)
+        par.append(p)
+        depth.append(depth[p] + 1)
+    return np.array(toks, dtype=np.int32), np.array(par, dtype=np.int32)
+
+
+def decode_planted(sh, cfg, T, L, n_steps=24, mean_emit=3.1, seed=5):
+    """Decode tokens/s of one request through the public host API with trees that
+    contain the target's greedy continuation at a random depth (mean emitted
+    tokens per step ~3.1, the MT-bench-like acceptance of P:587): first the
+    greedy continuation is produced by T=1 steps, then the cache is rewound to L
+    and the same tokens are re-generated with planted trees (verify + commit per
+    step, host buffers, wall clock).  The emitted tokens are checked against the
+    greedy continuation: a divergence is possible only at a near-tie of the top
+    two logits (R14), because the stream-K partial sums are reduced in a
+    run-dependent fp32 order; `mismatches` lists the first ones."""
+    rng = np.random.default_rng(seed)
+    need = n_steps * (T + 1) + T + 2
+    sh.set_committed_len(L)
+    seq = [1]
+    for _ in range(need):
+        r = sh.verify(np.array([seq[-1]], dtype=np.int32), np.array([-1], dtype=np.int32))
+        sh.commit_accepted()
+        seq.append(int(r["bonus"]))
+    sh.set_committed_len(L)
+    pos, emitted, match = 0, 0, True
+    mism, mism_steps = [], []
+    import time as _t
+    t0 = _t.perf_counter()
+    for _ in range(n_steps):
+        d = int(min(T - 1, 7, rng.geometric(1.0 / mean_emit) - 1))
+        toks, par = planted_tree(seq, pos, d, T, cfg.vocab, rng)
+        r = sh.verify(toks, par)
+        sh.commit_accepted()
+        n = int(r["n_accepted"])                     # root + accepted draft nodes
+        got = [int(toks[i]) for i in r["accepted"][1:]] + [int(r["bonus"])]
+        if got != seq[pos + 1:pos + 1 + n]:
+            match = False
+            mism.append({"step": len(mism_steps), "d": d, "n": n, "got": got, "want": seq[pos + 1:pos + 1 + n]})
+        mism_steps.append(0)
+        emitted += n                                 # (n - 1) accepted + 1 bonus
+        pos += n
+    dt = _t.perf_counter() - t0
+    return {"tokens_per_s": emitted / dt, "mean_emitted_per_step": emitted / n_steps, "steps": n_steps,
+            "T": T, "tokens": emitted, "matches_greedy": bool(match), "mismatches": mism[:3],
+            "how": "host API (ss_verify_tree + ss_commit_accepted per step, wall clock), planted trees"}
 
 
 def tp_emulated(args, cfg, local, dev, peak):

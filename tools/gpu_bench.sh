@@ -10,6 +10,7 @@ d = json.load(open('gpurun_out/bench.json'))
 print('step us', round(d['value'], 1), 'e2e', round(d['e2e']['value'], 1), 'frac', round(d['step_roofline_frac'], 3),
       'gu frac', round(d.get('roofline', {}).get('frac', 0), 3), d['clocks'])
 print({k: round(v['total'] / max(v['launches'], 1), 1) for k, v in d.get('kernel_times_us', {}).items()})
+print('decode_planted', {k: v for k, v in d.get('decode_planted', {}).items() if k != 'how'})
 print('tp_emulated', {k: (round(v['us'], 1), round(v['roofline_frac'], 3)) for k, v in d.get('tp_emulated', {}).items() if k.startswith('tp')})
 PY
 tail -2 gpurun_out/bench.err

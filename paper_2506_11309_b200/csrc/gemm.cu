@@ -392,7 +392,9 @@ __device__ void accept_walk_dev(DevState* st) {
   }
   for (int i = n; i < SS_MAX_TREE; ++i) res.accepted[i] = -1;
   res.n_accepted = n;
-  res.status = st->status;
+  // a peer poll that ran out of budget makes the step's result invalid
+  res.status = st->timeout ? SS_ETIMEOUT : st->status;
+  st->timeout = 0;
   st->have_verify = 1;
   // a13: post the verified path to the draft group's outbox (Alg. 1
   // "Send the verified tokens"; P:293 STOP at the end of generation): lines

@@ -14,6 +14,11 @@ enum { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_ARGMAX = 3 };
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while its predecessor drains; kernels call pdl_wait() before consuming
 // their predecessors' outputs.  Works under stream capture (graph edges).
+inline thread_local int ss_pdl_pos = 31;  // launch position in the layer body (debugging aid)
+// Set while enqueueing a fake-peer shard (several TP ranks on one GPU, capped
+// grids): an early-launched PDL grid holds SM slots while it waits, which can
+// starve a peer rank's kernel that this rank's all-reduce is polling for.
+inline thread_local bool ss_pdl_off = false;
 template <typename... ExpT, typename... ActT>
 inline cudaError_t launch_pdl(void (*k)(ExpT...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               ActT&&... args) {
@@ -27,7 +32,9 @@ inline cudaError_t launch_pdl(void (*k)(ExpT...), dim3 grid, dim3 block, size_t 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   static const bool no_pdl = getenv("SS_NO_PDL") != nullptr;  // debugging aid
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  // debugging aid: SS_NO_PDL_MASK bit i = no PDL for body launch position i (ss_pdl_pos)
+  static const int no_pdl_mask = getenv("SS_NO_PDL_MASK") ? atoi(getenv("SS_NO_PDL_MASK")) : 0;
+  cfg.numAttrs = (no_pdl || ss_pdl_off || ((no_pdl_mask >> ss_pdl_pos) & 1)) ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, k, std::forward<ActT>(args)...);
 }
 

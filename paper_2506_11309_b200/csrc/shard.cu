@@ -760,6 +760,8 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
   // launches to leave out, 1 qkv, 2 attention, 4 o, 8 gate/up, 16 down
   static const int skip = getenv("SS_EXP_SKIP") ? atoi(getenv("SS_EXP_SKIP")) : 0;
   const int cap = s->launch_cap;
+  // fake-peer TP (ranks share this GPU): no PDL, see ss_pdl_off
+  ss_pdl_off = s->P > 1 && cap > 0 && !s->loopback;
   for (int l = 0; l < c.n_layers; ++l) {
     LayerW& lw = s->layers[l];
     GemmArgs g = gemm_args(s, lw.qkv, s->act_h, s->sc_qkv, EPI_QKV, l);
@@ -767,6 +769,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.zero_x_stages = lw.o.S;
     g.zero_x_nt = NT;
     PROF_BEGIN(1);
+    ss_pdl_pos = 0;
     if (!(skip & 1)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     AttnArgs a;
@@ -786,6 +789,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     a.bar = s->attn_bar;
     a.act_out = s->act_o;
     PROF_BEGIN(2);
+    ss_pdl_pos = 1;
     if (!(skip & 2)) n += launch_attention(a, cap, st);
     PROF_END();
     g = gemm_args(s, lw.o, s->act_o, s->sc_o, EPI_RESID, l);
@@ -797,10 +801,12 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.norm_out = s->act_h;
     g.norm_split = 0;
     PROF_BEGIN(3);
+    ss_pdl_pos = 2;
     if (!(skip & 4)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     g = gemm_args(s, lw.gu, s->act_h, s->sc_gu, EPI_SWIGLU, l);
     PROF_BEGIN(5);
+    ss_pdl_pos = 3;
     if (!(skip & 8)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
     g = gemm_args(s, lw.down, s->act_d, s->sc_down, EPI_RESID, l);
@@ -810,6 +816,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     g.norm_out = l + 1 < c.n_layers ? s->act_h : s->act_lm;
     g.norm_split = l + 1 < c.n_layers ? 0 : 1;
     PROF_BEGIN(6);
+    ss_pdl_pos = 4;
     if (!(skip & 16)) n += launch_gemm(g, 0, NT, cap, st);
     PROF_END();
   }
@@ -817,8 +824,11 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
   g.epi.logits = want_logits ? s->logits_dev : nullptr;
   g.epi.ar_seq = 2 * c.n_layers;
   PROF_BEGIN(7);
+  ss_pdl_pos = 5;
   n += launch_gemm(g, 1, NT, cap, st);
   PROF_END();
+  ss_pdl_pos = 31;
+  ss_pdl_off = false;
   if (auto_commit) {
     PROF_BEGIN(8);
     launch_commit(s, 1, st);

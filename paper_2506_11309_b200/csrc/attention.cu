@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
     __threadfence();
     ATR(4);
     atomicAdd(&a.bar[grp * 2], 1);
-    while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) __nanosleep(100);
+    while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) spin_pause();
     __threadfence();
     ATR(5);
   }

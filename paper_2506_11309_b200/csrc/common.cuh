@@ -155,6 +155,10 @@ SS_DEV uint64_t policy_evict_last() {
 
 // Programmatic dependent launch (PDL): the next kernel in the stream may start
 // its prologue while this one drains; it must wait before reading our outputs.
+#ifndef SS_SPIN_NS
+#define SS_SPIN_NS 100  // back-off of the grid-level spin waits (experiment knob)
+#endif
+SS_DEV void spin_pause() { if (SS_SPIN_NS > 0) __nanosleep(SS_SPIN_NS); }
 SS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 SS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
       if (threadIdx.x == 0) {
         fence_acq_rel_gpu();
         atomicAdd(&g.nbar[0], ndone);
-        while (*reinterpret_cast<volatile int*>(&g.nbar[0]) < g.n_tg) __nanosleep(100);
+        while (*reinterpret_cast<volatile int*>(&g.nbar[0]) < g.n_tg) spin_pause();
         fence_acq_rel_gpu();
       }
       named_bar_sync(1, NCT);

@@ -128,16 +128,41 @@ def test_loopback_emulation_runs():
     sh.close()
 
 
-def test_70b_shaped_layer_tp2_fakepeer_sampled():
-    """TP = 2 at full Llama3-70B layer shape (h 8192, I 28672, 64/8 heads, 128256-row
-    vocab-parallel LM head, 4K prefix): two fake-peer shards synthesised on the device,
-    the fused all-reduces over h/128 = 64 tile-groups and the argmax exchange; logits of
-    both shards vs the float64 oracle on a seeded vocab sample (cf. the TP 1 test in
-    test_gpu_parity.py)."""
+_ORACLE_70B = {}
+
+
+def _oracle_70b_layer(cfg, L, tokens, parents):
+    """Float64 oracle of the unsharded 1-layer 70B-shaped model up to the final norm
+    (TP is exact up to summation order), cached across the TP sizes."""
+    import dataclasses
+    key = (L, tuple(tokens), tuple(parents))
+    if key not in _ORACLE_70B:
+        canon = {"layers": [synth.gen_model(dataclasses.replace(cfg, vocab=8), 0, with_lm_head=False)["layers"][0]],
+                 "embed": None, "final_norm": synth.gen_norm(0, -1, synth.KIND["FINAL_NORM"], cfg.hidden)}
+        m = O.OracleModel(cfg, canon, cache_dense=False)
+        kv = O.KVCache(cfg, L + 64)
+        k, v = synth.gen_prefix_kv(1, 0, L, cfg.n_kv_heads, cfg.head_dim)
+        kv.set_prefix(0, k, v)
+        kv.L = L
+        depth, pos, anc = O.tree_meta(parents, L)
+        x = O.bf16_to_f64(synth.gen_embed(0, cfg.vocab, cfg.hidden, rows=tokens))
+        x, _, _ = O.layer_forward(cfg, m, 0, x, kv, L, pos, anc)
+        _ORACLE_70B[key] = O.rmsnorm(x, canon["final_norm"], cfg.rms_eps)
+    return _ORACLE_70B[key]
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_70b_shaped_layer_tp_fakepeer_sampled(P):
+    """TP = 2 / 4 / 8 at full Llama3-70B layer shape (h 8192, I 28672, 64/8 heads,
+    128256-row vocab-parallel LM head, 4K prefix): P fake-peer shards synthesised on the
+    device, the fused all-reduces over h/128 = 64 tile-groups and the argmax exchange;
+    logits of all shards vs the float64 oracle on a seeded vocab sample (cf. the TP 1
+    test in test_gpu_parity.py).  TP 8 = one kv head per rank (the paper's headline
+    70B configuration)."""
     import dataclasses
     import paper_2506_11309_b200 as pkg
     cfg = dataclasses.replace(synth.CONFIGS["llama3-70b"], n_layers=1)
-    L, T, P = 4096, 8, 2
+    L, T = 4096, 8
     shards = []
     for r in range(P):
         sh = pkg.Shard(cfg, r, P, 0, max_ctx=L + 64, max_tree=8)
@@ -158,18 +183,7 @@ def test_70b_shaped_layer_tp2_fakepeer_sampled():
     assert [res["status"] for res, _ in outs] == [0] * P
     for res, _ in outs[1:]:
         assert res["argmax"] == res0["argmax"] and res["accepted"] == res0["accepted"]
-    # oracle: the unsharded layer in float64 (TP is exact up to summation order)
-    canon = {"layers": [synth.gen_model(dataclasses.replace(cfg, vocab=8), 0, with_lm_head=False)["layers"][0]],
-             "embed": None, "final_norm": synth.gen_norm(0, -1, synth.KIND["FINAL_NORM"], cfg.hidden)}
-    m = O.OracleModel(cfg, canon, cache_dense=False)
-    kv = O.KVCache(cfg, L + 64)
-    k, v = synth.gen_prefix_kv(1, 0, L, cfg.n_kv_heads, cfg.head_dim)
-    kv.set_prefix(0, k, v)
-    kv.L = L
-    depth, pos, anc = O.tree_meta(parents, L)
-    x = O.bf16_to_f64(synth.gen_embed(0, cfg.vocab, cfg.hidden, rows=tokens))
-    x, _, _ = O.layer_forward(cfg, m, 0, x, kv, L, pos, anc)
-    xn = O.rmsnorm(x, canon["final_norm"], cfg.rms_eps)
+    xn = _oracle_70b_layer(cfg, L, tokens, parents)
     sample = np.unique(np.concatenate([rng.choice(cfg.vocab, 4096, replace=False), res0["argmax"][:T]]))
     lo = xn @ O.bf16_to_f64(synth.gen_lm_head(0, cfg.vocab, cfg.hidden, rows=sample)).T
     lg = logits[:, sample]

@@ -451,18 +451,22 @@ def tp_emulated(args, cfg, local, dev, peak):
         d_tok = torch.tensor(np.stack([t for t, _ in trees]), dtype=torch.int32, device=dev)
         d_par = torch.tensor(np.stack([p for _, p in trees]), dtype=torch.int32, device=dev)
         stream = torch.cuda.current_stream(dev)
+        from paper_2506_11309_b200 import swiftspec as ssp
+        res = torch.zeros(ssp.result_nbytes() // 4, dtype=torch.int32, device=dev)
         for i in range(3):
-            sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+            sh.verify_dev(d_tok[i], d_par[i], T, d_result=res, auto_commit=True, stream=stream)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(3, n):
-            sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+            sh.verify_dev(d_tok[i], d_par[i], T, d_result=res, auto_commit=True, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / (n - 3)
         b = step_bytes(cfg, T, L + 1, P)
-        out[f"tp{P}"] = {"us": ms * 1e3, "bytes_per_gpu": b, "roofline_frac": b / (ms / 1e3) / 1e9 / peak}
+        status = ssp.parse_result(res.cpu().numpy(), T)["status"]  # -5 = a poll ran out of budget
+        out[f"tp{P}"] = {"us": ms * 1e3, "bytes_per_gpu": b, "roofline_frac": b / (ms / 1e3) / 1e9 / peak,
+                         "status_ok": status == 0}
         sh.close()
     return out
 

@@ -598,7 +598,18 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
 
 template <int D>
 static int launch_d(const AttnArgs& a, int max_ctas, cudaStream_t st) {
-  switch (rb_for(a.G, a.NT)) {
+  int rb = rb_for(a.G, a.NT);
+  // With <= 2 kv heads per GPU (TP 4 / 8) the few CTAs per head are bound by
+  // each CTA's tile loop, so split the rows over two chunks of 2 row blocks
+  // (twice the CTAs, each half the rows): TP4-rank step 6.64 -> 6.48 ms, TP8
+  // 6.08 -> 5.97 ms.  With 8 kv heads (TP 1) it costs 1.5 us per layer.
+  // SS_ATTN_RB overrides the cap (tuning aid).  The workspace and meet
+  // counters hold two row chunks per kv head, so Z = rows / (16 rb) <= 2.
+  static const int rb_env = getenv("SS_ATTN_RB") ? atoi(getenv("SS_ATTN_RB")) : 0;
+  const int rb_cap = rb_env > 0 ? rb_env : (a.Hkv_l <= 2 ? 2 : 0);
+  const int rows = a.G * a.NT * 8;
+  while (rb_cap > 0 && rb > rb_cap && rows <= (rb / 2) * 16 * 2) rb /= 2;
+  switch (rb) {
     case 1: return launch_rb<D, 1>(a, max_ctas, st);
     case 2: return launch_rb<D, 2>(a, max_ctas, st);
     case 4: return launch_rb<D, 4>(a, max_ctas, st);

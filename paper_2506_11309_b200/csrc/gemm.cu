@@ -811,7 +811,9 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
       if (threadIdx.x == 0) {
         fence_acq_rel_gpu();
         atomicAdd(&g.nbar[0], ndone);
+#ifndef SS_EXP_NONORMMEET  // timing experiment only: norm without waiting for the other tile-groups
         while (*reinterpret_cast<volatile int*>(&g.nbar[0]) < g.n_tg) spin_pause();
+#endif
         fence_acq_rel_gpu();
       }
       named_bar_sync(1, NCT);

@@ -27,11 +27,14 @@ def main():
     ap.add_argument("--L", type=int, default=4096)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--eager-profile", action="store_true")
+    ap.add_argument("--tp", type=int, default=1, help="one rank of a TP group, loopback all-reduce (timing emulation)")
     a = ap.parse_args()
     cfg = dataclasses.replace(synth.CONFIGS[a.config], n_layers=a.layers)
-    sh = pkg.Shard(cfg, 0, 1, 0, max_ctx=a.L + 64 * (a.steps + 4), max_tree=max(8, a.T))
+    sh = pkg.Shard(cfg, 0, a.tp, 0, max_ctx=a.L + 64 * (a.steps + 4), max_tree=max(8, a.T))
     sh.synth_weights(0)
     sh.synth_prefix_kv(1, a.L)
+    if a.tp > 1:
+        sh.import_loopback()
     trees = [synth.tree_paperlike(a.T, cfg.vocab, np.random.default_rng(i)) for i in range(a.steps)]
     dev = torch.device("cuda", 0)
     st = torch.cuda.current_stream()

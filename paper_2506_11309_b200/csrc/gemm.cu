@@ -862,7 +862,15 @@ static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
   // ms) at no cost at TP 1-2; at T >= 16 a unit is longer and spreading wins.
   // SS_GEMM_MINU overrides (tuning aid).
   static const int minu_env = getenv("SS_GEMM_MINU") ? std::max(1, atoi(getenv("SS_GEMM_MINU"))) : 0;
-  const int min_units = minu_env ? minu_env : (NT == 1 ? 2 : 1);
+  // A GEMM whose whole K fits in <= 4 units (the O projection at TP 8) gives
+  // every CTA whole tile-groups: no partial flush, no shared arrival counts
+  // (TP8-rank step 5.97 -> 5.87 ms).  The residual (+ all-reduce) GEMMs take
+  // >= 4 units per CTA while that still leaves >= 200 CTAs (TP 8 down, TP 2
+  // O): fewer partial flushes ahead of the all-reduce tail.
+  int min_units = NT == 1 ? 2 : 1;
+  if (g.S <= 4) min_units = std::max(min_units, g.S);
+  if (EPI == EPI_RESID && U >= 800) min_units = std::max(min_units, 4);
+  if (minu_env) min_units = minu_env;
   int grid = (int)std::min<long>((U + min_units - 1) / min_units, (long)g.n_sm * o);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, st, g);

@@ -17,9 +17,15 @@
  * ss_commit_kv / ss_commit_accepted -- KV compaction of the accepted path.
  *
  * Conventions
- *  - Every function returns an ss_status; on error nothing was launched and
- *    the shard state is unchanged; ss_last_error() gives a message
- *    (thread-local).
+ *  - Every function returns an ss_status; on a host-detected error nothing
+ *    was launched and the shard state is unchanged; ss_last_error(shard)
+ *    gives that shard's last message (ss_last_error(NULL): the calling
+ *    thread's last message, e.g. after a failed ss_init_shard).
+ *  - Call order: a verify without auto-commit leaves the tree
+ *    rows pending; the next verify on the shard is refused with SS_ESTATE
+ *    until they are committed (ss_commit_kv / ss_commit_accepted) or
+ *    discarded (ss_set_committed_len).  Checks run in the order SS_EINVAL,
+ *    SS_ESTATE, SS_ECAPACITY.
  *  - Collective semantics (NCCL-style): every rank of a TP group calls
  *    ss_verify_tree* / ss_commit_* with identical arguments, in the same order.
  *  - Ownership: the library owns every device allocation it makes (weights in
@@ -48,7 +54,7 @@ typedef enum {
   SS_EINVAL = -1,        /* bad argument: tree not root-first/topological, T out of range,
                             token out of vocab, chain not root-anchored, bad shape/kind/bytes */
   SS_ECAPACITY = -2,     /* L + T > max_ctx (no eviction) */
-  SS_ECONSISTENCY = -3,  /* ranks disagree (debug checksum) or device-side validation failed */
+  SS_ECONSISTENCY = -3,  /* TP ranks were called with different trees (SS_DEBUG_CONSISTENCY checksum) */
   SS_ECUDA = -4,         /* a CUDA runtime error; message has cudaGetErrorString */
   SS_ETIMEOUT = -5,      /* a peer flag poll exceeded its budget */
   SS_ESTATE = -6         /* call order violated (commit without a verify, weights missing, ...) */
@@ -75,7 +81,11 @@ typedef struct ss_shard ss_shard;
  *  bonus_token = the target's greedy token after the last accepted node; it is
  *                emitted but not committed (it is the next call's root, R9).
  *  argmax[i]   = the target's greedy token at tree node i (ties -> lowest id).
- *  status      = device-side validation result (SS_OK or SS_EINVAL). */
+ *  status      = device-side result of the step: SS_OK, SS_EINVAL (tree
+ *                invalid, e.g. a mailbox tree larger than the graph's
+ *                capacity), SS_ETIMEOUT (a peer / inbox poll ran out of
+ *                budget) or SS_ECONSISTENCY (ranks disagree, debug
+ *                mode).  A step whose status is not SS_OK is never committed. */
 typedef struct {
   int32_t n_accepted;
   int32_t accepted[SS_MAX_TREE];
@@ -149,7 +159,18 @@ ss_status ss_import_loopback(ss_shard* s);
 ss_status ss_set_launch_cap(ss_shard* s, int32_t max_ctas_per_kernel);
 
 ss_status ss_destroy(ss_shard* s);
-const char* ss_last_error(void);
+/* Last error message of shard s (s != NULL) or of the calling thread (s ==
+ * NULL).  The pointer stays valid until the next failing call. */
+const char* ss_last_error(const ss_shard* s);
+
+/* Debug flags (SURVEY 8(b) "a debug mode checksums the arguments across
+ * ranks"): with SS_DEBUG_CONSISTENCY every verify exchanges a checksum of
+ * (T, tokens, parents) between the TP ranks over the peer buffers (one LL
+ * round trip) and fails the step with result.status = SS_ECONSISTENCY on
+ * every rank if any two disagree.  Set it identically on all ranks.
+ * Errors: SS_EINVAL (unknown flag). */
+#define SS_DEBUG_CONSISTENCY 1
+ss_status ss_set_debug(ss_shard* s, int32_t flags);
 
 /* ---- weights and KV ------------------------------------------------------ */
 
@@ -177,7 +198,11 @@ ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len);
  * K/V as fp16 (exact for the bf16 prefix inputs).
  * Synchronises the device. */
 ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, float* k_out, float* v_out);
-/* Set the committed length (truncate; cannot grow beyond rows ever written). */
+/* Set the committed length: truncate, or grow over rows that already hold
+ * data (prefix rows, or tree rows written by an earlier verify: chain
+ * prefill).  Discards a pending verify.  Synchronises the device.
+ * Errors: SS_ECAPACITY (L + max_tree > max_ctx), SS_EINVAL (L beyond the
+ * rows ever written). */
 ss_status ss_set_committed_len(ss_shard* s, int32_t L);
 /* Committed length L (synchronises with the device if the last commit was
  * device-driven).  Negative on error. */
@@ -191,7 +216,10 @@ int32_t ss_committed_len(ss_shard* s);
  * out: filled before return (the call synchronises `stream`).
  * logits_out: nullable float[T][vocab_shard] (this rank's vocab slice
  * [rank*ceil(V/tp), ...)), for parity checks.
- * Errors: SS_EINVAL, SS_ECAPACITY (L + T > max_ctx), SS_ESTATE, SS_ECUDA. */
+ * Errors: SS_EINVAL, SS_ESTATE (weights / peers missing, or a verify still
+ * pending), SS_ECAPACITY (L + T > max_ctx), SS_ECUDA; a device-side failure
+ * (out->status: SS_ETIMEOUT, SS_ECONSISTENCY) is returned as well, with out
+ * filled and nothing pending. */
 ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T,
                          ss_verify_result* out, float* logits_out, void* stream);
 
@@ -208,8 +236,9 @@ ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t
 /* Commit a root-anchored chain of tree nodes from the last verify:
  * accepted[0] == 0 and accepted[k] a child of accepted[k-1] (any such chain,
  * not only the accepted one: chain prefill, EOS truncation).  K/V rows
- * L + accepted[k] move to L + k in every layer; L += n.
- * Errors: SS_EINVAL (not a chain / n out of range), SS_ESTATE (no verify). */
+ * L + accepted[k] move to L + k in every layer; L += n.  Synchronises.
+ * Errors: SS_ESTATE (no pending verify, or its device status was not SS_OK),
+ * SS_EINVAL (not a chain / n out of range). */
 ss_status ss_commit_kv(ss_shard* s, const int32_t* accepted, int32_t n, void* stream);
 /* Commit the accepted path of the last verify, decided on the device. */
 ss_status ss_commit_accepted(ss_shard* s, void* stream);
@@ -237,7 +266,9 @@ ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d
  *   inbox  (owned by the target shard): line 0 = (T, seq), line 1+i =
  *          (token_i, parent_i);
  *   outbox (owned by the draft side):   line 1+k = (accepted[k], token),
- *          then line 0 = (n_accepted | stop << 31, bonus_token).
+ *          then line 0 = (n_accepted | (-status & 0xFF) << 16 | stop << 31,
+ *          bonus_token); a failed step posts n_accepted = 0 and its status,
+ *          and a timed-out inbox message is polled again by the next step.
  * Sequence numbers are consecutive per shard, starting at 1. */
 
 /* Device pointer of this shard's inbox ((1 + SS_MAX_TREE) lines x 16 B, a
@@ -253,8 +284,11 @@ ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eos_token);
  * is committed in the same launch sequence.  Errors as ss_verify_tree_dev. */
 ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream);
 /* Draft-side helpers: post a tree into an inbox / wait for a verified path in
- * an outbox and copy it to dev_out = [n, bonus, stop, (node, token) x n]
- * (int32, device).  Both enqueue one small kernel on `stream`. */
+ * an outbox and copy it to dev_out = [n, bonus, stop, status, (node, token)
+ * x n] (int32, device; status != SS_OK -> n = 0; a message that never
+ * arrives -> n = -1, status SS_ETIMEOUT).  The target refuses (status
+ * SS_EINVAL) a tree larger than its max_tree.  Both enqueue one small
+ * kernel on `stream`. */
 ss_status ss_mailbox_post_tree(void* inbox_dev, const int32_t* tokens, const int32_t* parents, int32_t T,
                                uint32_t seq, void* stream);
 ss_status ss_mailbox_recv_result(const void* outbox_dev, uint32_t seq, int32_t* dev_out, void* stream);

@@ -28,6 +28,8 @@ paper; they are pinned by the HF-Llama equivalence and the decode invariants
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -82,14 +84,20 @@ def tree_meta(parents, L: int):
 # scale (reading R3): W[k, n] = (q[k, n] - z[k // 128, n]) * s[k // 128, n].
 # ---------------------------------------------------------------------------
 def dequant(q, z, s_bits, group: int = GROUP) -> np.ndarray:
+    """W[k, n] = (q[k, n] - z[k // group, n]) * s[k // group, n]: the rows of
+    group g are rows [g*group, (g+1)*group), so W is formed group-major as
+    (q[g, i, n] - z[g, n]) * s[g, n] over a [G][group][N] view (same values)."""
     q = np.asarray(q)
     z = np.asarray(z)
     K, N = q.shape
     if K % group:
         raise ValueError("K must be a multiple of the group size")
+    G = K // group
     s = bf16_to_f64(s_bits)
-    g = np.arange(K) // group
-    return (q.astype(np.float64) - z[g, :].astype(np.float64)) * s[g, :]
+    W = np.empty((G, group, N))
+    np.subtract(q.reshape(G, group, N), z[:, None, :], out=W, dtype=np.float64)
+    W *= s[:, None, :]
+    return W.reshape(K, N)
 
 
 def rmsnorm(x, g_bits, eps: float) -> np.ndarray:
@@ -172,15 +180,50 @@ def accept_walk(tokens, parents, argmax):
 # ---------------------------------------------------------------------------
 # Model containers.
 # ---------------------------------------------------------------------------
+def linear_streamed(x, cols, N: int, chunk: int = 1024, workers: int = 0) -> np.ndarray:
+    """x @ W for a W whose canonical columns [n0, n1) come from cols(n0, n1) ->
+    (q, z, s).  Each output column is the plain dot product x @ dequant(...)[:, n]
+    (column j of x @ W depends only on column j of W), so W is never held whole:
+    chunks of columns are generated, dequantised and multiplied in a thread pool
+    (the 70B-shaped layers of the full-size parity tests: ~0.86 G weights each)."""
+    from threadpoolctl import threadpool_limits
+    out = np.empty((x.shape[0], N))
+
+    def job(n0):
+        n1 = min(N, n0 + chunk)
+        q, z, s = cols(n0, n1)
+        out[:, n0:n1] = x @ dequant(q, z, s)
+
+    with threadpool_limits(limits=1), ThreadPoolExecutor(max_workers=workers or os.cpu_count()) as ex:
+        list(ex.map(job, range(0, N, chunk)))
+    return out
+
+
 @dataclass
 class OracleModel:
-    """Canonical (quantised) weights from synth.gen_model; dequantised lazily."""
+    """Canonical (quantised) weights from synth.gen_model; dequantised lazily.
+
+    cols (optional): a streamed weight provider cols(layer, name, n0, n1) ->
+    (q, z, s) of canonical columns [n0, n1) -- used when a whole model's dense
+    weights would not fit in host memory (70B-shaped parity tests)."""
     cfg: object
     canon: dict
     cache_dense: bool = True
+    cols: object = None
 
     def __post_init__(self):
         self._dense = {}
+
+    def out_features(self, name: str) -> int:
+        c = self.cfg
+        return dict(wq=c.n_heads * c.head_dim, wk=c.n_kv_heads * c.head_dim, wv=c.n_kv_heads * c.head_dim,
+                    wo=c.hidden, wgate=c.intermediate, wup=c.intermediate, wdown=c.hidden)[name]
+
+    def matmul(self, layer: int, name: str, x) -> np.ndarray:
+        """x @ W[layer][name] with W = dequant(q, z, s) (P:501)."""
+        if self.cols is not None:
+            return linear_streamed(x, lambda n0, n1: self.cols(layer, name, n0, n1), self.out_features(name))
+        return x @ self.w(layer, name)
 
     def w(self, layer: int, name: str) -> np.ndarray:
         key = (layer, name)
@@ -239,9 +282,9 @@ def layer_forward(cfg, model: OracleModel, layer: int, x, kv: KVCache, L: int, p
     T = x.shape[0]
     Hq, Hkv, d = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
     xn = rmsnorm(x, model.norm(layer, "attn_norm"), cfg.rms_eps)          # a2
-    q = (xn @ model.w(layer, "wq")).reshape(T, Hq, d)                     # a3
-    k = (xn @ model.w(layer, "wk")).reshape(T, Hkv, d)
-    v = (xn @ model.w(layer, "wv")).reshape(T, Hkv, d)
+    q = model.matmul(layer, "wq", xn).reshape(T, Hq, d)                   # a3
+    k = model.matmul(layer, "wk", xn).reshape(T, Hkv, d)
+    v = model.matmul(layer, "wv", xn).reshape(T, Hkv, d)
     for i in range(T):                                                    # a4: RoPE at L + depth
         q[i] = rope(q[i], pos[i], cfg.rope_theta)
         k[i] = rope(k[i], pos[i], cfg.rope_theta)
@@ -252,10 +295,10 @@ def layer_forward(cfg, model: OracleModel, layer: int, x, kv: KVCache, L: int, p
         keys = np.concatenate([Kp, k[sel]], axis=0)
         vals = np.concatenate([Vp, v[sel]], axis=0)
         attn[i] = attend_node(q[i], keys, vals, Hkv).reshape(-1)
-    x = x + attn @ model.w(layer, "wo")                                   # a6
+    x = x + model.matmul(layer, "wo", attn)                               # a6
     xn2 = rmsnorm(x, model.norm(layer, "mlp_norm"), cfg.rms_eps)          # a7
-    hmid = silu(xn2 @ model.w(layer, "wgate")) * (xn2 @ model.w(layer, "wup"))  # a8
-    x = x + hmid @ model.w(layer, "wdown")                                # a9
+    hmid = silu(model.matmul(layer, "wgate", xn2)) * model.matmul(layer, "wup", xn2)  # a8
+    x = x + model.matmul(layer, "wdown", hmid)                            # a9
     return x, k, v
 
 

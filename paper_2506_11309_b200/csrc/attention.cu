@@ -91,7 +91,14 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
   const int Mrows = G * T;
   const int m0 = z * ROWS;
   const int ntiles = (L + T + kKvTile - 1) / kKvTile;
-  const int t0 = (int)((long)split * ntiles / S), t1 = (int)((long)(split + 1) * ntiles / S);
+  // Split count from the RUNTIME length (a captured graph replays at any L):
+  // the fewest splits with the same longest split; surplus CTAs leave at once
+  // (the cluster variant keeps all S CTAs: they meet in cl.sync).
+  const int per = (ntiles + S - 1) / S;
+  const int SE = CL ? S : (ntiles + per - 1) / per;
+  if (!CL && split >= SE) return;
+  const int t0 = CL ? (int)((long)split * ntiles / S) : split * per;
+  const int t1 = CL ? (int)((long)(split + 1) * ntiles / S) : min(ntiles, t0 + per);
   const size_t head_base = ((size_t)a.layer * a.Hkv_l + kvh) * a.max_ctx_pad * D;
   ATR(0);
 
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
   // ---- merge the KS key-slice partials of each row inside the CTA (shared
   // memory, reusing the K/V ring), so only one partial per split goes out
   const int grp = kvh * Z + z;
-  const int P = S;  // partials per (kv head, row chunk)
+  const int P = SE;  // partials per (kv head, row chunk)
   const int ra = rb * 16 + gq, rbb = ra + 8;
   if constexpr (C::KS > 1) {
     __syncthreads();  // every warp is done with the K/V ring
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
     __threadfence();
     ATR(4);
     atomicAdd(&a.bar[grp * 2], 1);
-    while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < S) spin_pause();
+    while (*reinterpret_cast<volatile int*>(&a.bar[grp * 2]) < SE) spin_pause();
     __threadfence();
     ATR(5);
   }
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
   {
     float* s_w = reinterpret_cast<float*>(Ks);  // reuse the K/V ring: [rows_here][P] x 2
     const int n_items = ROWS * (D / 4);
-    const int i_lo = (int)((long)split * n_items / S), i_hi = (int)((long)(split + 1) * n_items / S);
+    const int i_lo = (int)((long)split * n_items / SE), i_hi = (int)((long)(split + 1) * n_items / SE);
     const int r_first = i_lo / (D / 4), r_last = (i_hi - 1) / (D / 4);
     const int nr = (i_hi > i_lo) ? r_last - r_first + 1 : 0;
     const float* wsg = a.ws + ((size_t)grp * P * 256) * D;
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
   ATR(6);
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&a.bar[grp * 2 + 1], 1) == S - 1) {
+    if (atomicAdd(&a.bar[grp * 2 + 1], 1) == SE - 1) {
       a.bar[grp * 2] = 0;
       a.bar[grp * 2 + 1] = 0;
     }
@@ -476,14 +483,16 @@ __global__ void __launch_bounds__(AttnCfg<D, RB, CL>::WARPS * 32, 1) attn_kernel
 
 template <int D, int RB, bool CL>
 static int occ_of() {
-  static int occ = -1;
+  static int occ_dev[kMaxDevices] = {0};  // per device (the smem opt-in is per device)
   using C = AttnCfg<D, RB, CL>;
-  if (occ < 0) {
+  const int dev = current_device();
+  if (!occ_dev[dev]) {
+    int occ = 1;
     cudaFuncSetAttribute(attn_kernel<D, RB, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_kernel<D, RB, CL>, C::WARPS * 32, C::SMEM);
-    if (occ < 1) occ = 1;
+    occ_dev[dev] = occ < 1 ? 1 : occ;
   }
-  return occ;
+  return occ_dev[dev];
 }
 
 static int rb_for(int G, int NT) {
@@ -498,8 +507,10 @@ constexpr int kAttnCluster = 16;  // splits per (kv head, row chunk) in the clus
 // Whether 16-CTA clusters of the cluster variant can be scheduled (queried once).
 template <int D, int RB>
 static bool cluster_ok() {
-  static int ok = -1;
-  if (ok < 0) {
+  static int ok_dev[kMaxDevices] = {0};  // 0 unknown, 1 yes, 2 no (per device)
+  const int dev = current_device();
+  int& ok = ok_dev[dev];
+  if (ok == 0) {
     using C = AttnCfg<D, RB, true>;
     auto k = attn_kernel<D, RB, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -516,7 +527,7 @@ static bool cluster_ok() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    ok = (cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n >= 1) ? 1 : 0;
+    ok = (cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n >= 1) ? 1 : 2;
     cudaGetLastError();
   }
   return ok == 1;
@@ -526,9 +537,9 @@ template <int D, int RB>
 static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
   const int rows = a.G * a.NT * 8;
   int n_sm = 148;
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-  // SS_ATTN_CLUSTER = 0 / 1 forces the variant (experiments)
-  static const int force = getenv("SS_ATTN_CLUSTER") ? atoi(getenv("SS_ATTN_CLUSTER")) : -1;
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, current_device());
+  // SS_ATTN_CLUSTER = 0 / 1 forces the variant (experiment builds)
+  static const int force = exp_env_int("SS_ATTN_CLUSTER", -1);
   if constexpr (RB <= 4) {
     using C = AttnCfg<D, RB, true>;
     // The cluster variant has 16 CTAs per (kv head, row chunk): it wins when
@@ -541,12 +552,12 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
     if (want && max_ctas <= 0 && cluster_ok<D, RB>()) {
       // optional dynamic shared-memory padding (KB) that keeps one cluster
       // CTA per SM (two would share an SM's tensor pipe)
-      static const int pad_kb = getenv("SS_ATTN_CL_SMEM_KB") ? atoi(getenv("SS_ATTN_CL_SMEM_KB")) : 0;
+      static const int pad_kb = exp_env_int("SS_ATTN_CL_SMEM_KB", 0);
       const int smem = std::max((int)C::SMEM, pad_kb * 1024);
-      static int attr_smem = 0;
-      if (smem > attr_smem) {
+      static int attr_smem[kMaxDevices] = {0};
+      if (smem > attr_smem[current_device()]) {
         cudaFuncSetAttribute(attn_kernel<D, RB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_smem = smem;
+        attr_smem[current_device()] = smem;
       }
       a.splits = kAttnCluster;
       a.zchunks = (rows + C::ROWS - 1) / C::ROWS;
@@ -563,7 +574,7 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
-      cfg.numAttrs = getenv("SS_NO_PDL") ? 1 : 2;
+      cfg.numAttrs = (exp_env("SS_NO_PDL") || ss_pdl_off) ? 1 : 2;
       cudaLaunchKernelEx(&cfg, attn_kernel<D, RB, true>, a);
       return 1;
     }
@@ -581,15 +592,6 @@ static int launch_rb(AttnArgs a, int max_ctas, cudaStream_t st) {
   if (S > max_tiles) S = max_tiles;
   if (S > 64) S = 64;  // workspace holds 64 partials (one per split) per row chunk
   if (S < 1) S = 1;
-  // fewest splits with the same longest split (same critical path, fewer
-  // partials to merge), from the committed length the host knows
-  if (a.L_hint > 0) {
-    const int nt = (a.L_hint + a.NT * 8 + kKvTile - 1) / kKvTile;
-    const int per = (nt + S - 1) / S;
-    const int S2 = (nt + per - 1) / per;
-    static const bool no_bal = getenv("SS_ATTN_NO_BALANCE") != nullptr;  // experiment switch
-    if (!no_bal && S2 >= 1 && S2 < S) S = S2;
-  }
   a.splits = S;
   a.zchunks = Z;
   launch_pdl(attn_kernel<D, RB, false>, dim3(S, a.Hkv_l, Z), dim3(C::WARPS * 32), C::SMEM, st, a);
@@ -605,7 +607,7 @@ static int launch_d(const AttnArgs& a, int max_ctas, cudaStream_t st) {
   // 6.08 -> 5.97 ms.  With 8 kv heads (TP 1) it costs 1.5 us per layer.
   // SS_ATTN_RB overrides the cap (tuning aid).  The workspace and meet
   // counters hold two row chunks per kv head, so Z = rows / (16 rb) <= 2.
-  static const int rb_env = getenv("SS_ATTN_RB") ? atoi(getenv("SS_ATTN_RB")) : 0;
+  static const int rb_env = exp_env_int("SS_ATTN_RB", 0);
   const int rb_cap = rb_env > 0 ? rb_env : (a.Hkv_l <= 2 ? 2 : 0);
   const int rows = a.G * a.NT * 8;
   while (rb_cap > 0 && rb > rb_cap && rows <= (rb / 2) * 16 * 2) rb /= 2;

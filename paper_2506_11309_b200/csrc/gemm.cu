@@ -398,16 +398,22 @@ __device__ void accept_walk_dev(DevState* st) {
   st->have_verify = 1;
   // a13: post the verified path to the draft group's outbox (Alg. 1
   // "Send the verified tokens"; P:293 STOP at the end of generation): lines
-  // 1..n = (node index, token), then line 0 = (n | stop << 31, bonus).
+  // 1..n = (node index, token), then line 0 = (n | -status << 16 | stop << 31,
+  // bonus).  A failed step posts n = 0 and its status; a timed-out inbox
+  // message is polled again by the next step (the sequence number does not
+  // advance).
   if (st->mbox_mode) {
     const uint32_t seq = st->mbox_cur;
+    const bool ok = res.status == SS_OK;
     if (st->mbox_post && st->mbox_out) {
-      for (int k = 0; k < n; ++k)
+      const int np = ok ? n : 0;
+      for (int k = 0; k < np; ++k)
         ll_store(st->mbox_out + 1 + k, (uint32_t)res.accepted[k], (uint32_t)st->tokens[res.accepted[k]], seq);
-      const uint32_t stop = (st->eos >= 0 && res.bonus_token == st->eos) ? 1u : 0u;
-      ll_store(st->mbox_out, (uint32_t)n | (stop << 31), (uint32_t)res.bonus_token, seq);
+      const uint32_t stop = (ok && st->eos >= 0 && res.bonus_token == st->eos) ? 1u : 0u;
+      ll_store(st->mbox_out, (uint32_t)np | ((uint32_t)(-res.status) & 0xFFu) << 16 | (stop << 31),
+               ok ? (uint32_t)res.bonus_token : 0u, seq);
     }
-    st->mbox_seq = seq;
+    if (res.status != SS_ETIMEOUT) st->mbox_seq = seq;
   }
 }
 
@@ -459,7 +465,6 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   // both measured slower (profiles/r01_experiments.md).
   const int U = g.n_tg * g.S;
   const int u0 = (int)((long)blockIdx.x * U / gridDim.x), u1 = (int)((long)(blockIdx.x + 1) * U / gridDim.x);
-  int* queue = g.counters + g.n_tg;  // [1] exit counter
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -839,29 +844,31 @@ template <int WFMT, int NT, int EPI>
 static int launch_t(const GemmArgs& g, int max_ctas, cudaStream_t st) {
   using C = GemmCfg<WFMT, NT>;
   auto k = gemm_kernel<WFMT, NT, EPI>;
-  static bool attr_set = false;
-  static int occ = 1;
-  if (!attr_set) {
+  static int occ_dev[kMaxDevices] = {0};  // 0 = attributes not yet set on that device
+  const int dev = current_device();
+  if (!occ_dev[dev]) {
+    int occ = 1;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, C::SMEM);
     if (occ < 1) occ = 1;
-    if (getenv("SS_DEBUG_OCC")) {
+    if (exp_env("SS_DEBUG_OCC")) {
       cudaFuncAttributes fa;
       cudaFuncGetAttributes(&fa, k);
       fprintf(stderr, "gemm WFMT=%d NT=%d EPI=%d: stages %d, dyn smem %d, static smem %zu, regs %d, CTAs/SM %d\n",
               WFMT, NT, EPI, C::STAGES, C::SMEM, fa.sharedSizeBytes, fa.numRegs, occ);
     }
-    attr_set = true;
+    occ_dev[dev] = occ;
   }
+  const int occ = occ_dev[dev];
   long U = (long)g.n_tg * g.S;
-  static const int occ_cap = getenv("SS_GEMM_OCC") ? atoi(getenv("SS_GEMM_OCC")) : 0;  // debugging aid
+  static const int occ_cap = exp_env_int("SS_GEMM_OCC", 0);  // debugging aid
   int o = (occ_cap > 0 && occ_cap < occ) ? occ_cap : occ;
   // minimum stream-K units per CTA: at T <= 8 (NT = 1) two units per CTA
   // (fewer, longer ranges: fewer partial flushes per tile-group) make the
   // small per-rank GEMMs of TP 4 / 8 faster (TP4-rank emulation 6.86 -> 6.61
   // ms) at no cost at TP 1-2; at T >= 16 a unit is longer and spreading wins.
   // SS_GEMM_MINU overrides (tuning aid).
-  static const int minu_env = getenv("SS_GEMM_MINU") ? std::max(1, atoi(getenv("SS_GEMM_MINU"))) : 0;
+  static const int minu_env = std::max(0, exp_env_int("SS_GEMM_MINU", 0));
   // A GEMM whose whole K fits in <= 4 units (the O projection at TP 8) gives
   // every CTA whole tile-groups: no partial flush, no shared arrival counts
   // (TP8-rank step 5.97 -> 5.87 ms).  The residual (+ all-reduce) GEMMs take

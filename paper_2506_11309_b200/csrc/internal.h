@@ -8,6 +8,7 @@
 #include <map>
 
 #include "../../include/swiftspec.h"
+#include "host_logic.h"
 
 namespace ss {
 
@@ -39,8 +40,10 @@ struct DevState {
   int32_t mbox_mode;         // 1 while the current step came from the inbox
   int32_t mbox_post;         // 1 on the rank that posts the verified path
   int32_t eos;               // STOP when the bonus token equals eos (-1: never)
-  int32_t pad1;
+  int32_t max_written;       // highest KV row ever written + 1 (prefix, tree rows)
   uint4* mbox_out;           // draft group's outbox (peer-mapped), nullptr = none
+  int32_t debug;             // SS_DEBUG_* flags (ss_set_debug)
+  int32_t pad2;
 };
 
 // One packed linear (W4 format, see common.cuh) or bf16 matrix.
@@ -121,12 +124,9 @@ struct ss_shard {
   ss::DevState* hstate = nullptr;  // pinned host mirror for results
   int32_t* d_tree_in = nullptr;    // device staging for host trees [2*64]
   int32_t* h_tree_in = nullptr;    // pinned staging
-  int L_host = 0;
-  bool L_known = true;
-  int L_upper = 0;
-  int max_rows_written = 0;
-  bool have_verify = false;
-  int last_T = 0;
+  ss::host::CallState hs;          // host view: committed length, pending verify, rows written
+  std::string err;                 // message of the last failed call on this shard
+  int debug = 0;                   // SS_DEBUG_* flags
 
   // TP peers
   float* recv = nullptr;            // this rank's LL receive buffer
@@ -143,3 +143,9 @@ struct ss_shard {
   std::map<int, ss::Graph> graphs;
   cudaStream_t cap_stream = nullptr;
 };
+
+// LL line index of the cross-rank consistency area (SS_DEBUG_CONSISTENCY) in a
+// receive buffer: after the two all-reduce parities and the argmax area.
+inline size_t consistency_line_offset(const ss_shard* s) {
+  return (size_t)2 * s->P * (s->cfg.hidden / 128) * 128 * 32 + (size_t)s->P * 64;
+}

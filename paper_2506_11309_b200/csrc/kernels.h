@@ -11,6 +11,29 @@ namespace ss {
 
 enum { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_ARGMAX = 3 };
 
+// Tuning / debugging environment knobs exist only in experiment builds
+// (`python -m paper_2506_11309_b200.build --variant x -D SS_EXPERIMENTS`): the
+// product library reads no environment variable and can never skip work.
+#ifdef SS_EXPERIMENTS
+inline const char* exp_env(const char* name) { return getenv(name); }
+#else
+inline const char* exp_env(const char*) { return nullptr; }
+#endif
+inline int exp_env_int(const char* name, int dflt) {
+  const char* v = exp_env(name);
+  return v ? atoi(v) : dflt;
+}
+
+// Per-device launch caches (function attributes, occupancy): the dynamic
+// shared-memory opt-in is per device, and one process may drive several GPUs
+// (ss_import_local_peers).
+constexpr int kMaxDevices = 16;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while its predecessor drains; kernels call pdl_wait() before consuming
 // their predecessors' outputs.  Works under stream capture (graph edges).
@@ -31,9 +54,9 @@ inline cudaError_t launch_pdl(void (*k)(ExpT...), dim3 grid, dim3 block, size_t 
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  static const bool no_pdl = getenv("SS_NO_PDL") != nullptr;  // debugging aid
+  static const bool no_pdl = exp_env("SS_NO_PDL") != nullptr;  // debugging aid
   // debugging aid: SS_NO_PDL_MASK bit i = no PDL for body launch position i (ss_pdl_pos)
-  static const int no_pdl_mask = getenv("SS_NO_PDL_MASK") ? atoi(getenv("SS_NO_PDL_MASK")) : 0;
+  static const int no_pdl_mask = exp_env_int("SS_NO_PDL_MASK", 0);
   cfg.numAttrs = (no_pdl || ss_pdl_off || ((no_pdl_mask >> ss_pdl_pos) & 1)) ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, k, std::forward<ActT>(args)...);
 }
@@ -88,7 +111,6 @@ struct AttnArgs {
   DevState* st = nullptr;
   int layer = 0, Hkv_l = 0, G = 1, d = 128, max_ctx_pad = 0, NT = 1;
   int splits = 1, zchunks = 1;
-  int L_hint = 0;  // committed length at enqueue time (host view; 0 = unknown): split balancing only
   const uint16_t* qbuf = nullptr;
   const uint16_t* kc = nullptr;
   const uint16_t* vc = nullptr;

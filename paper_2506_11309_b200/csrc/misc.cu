@@ -36,18 +36,33 @@ SS_DEV bool ll_wait(const uint4* line, uint32_t seq, uint32_t& d1, uint32_t& d2)
   return false;
 }
 
+// Cross-rank consistency check (debug mode, SS_DEBUG_CONSISTENCY; SURVEY 8(b)
+// "a debug mode checksums the arguments across ranks"): every rank posts a
+// checksum of (T, tokens, parents) to every peer's receive buffer as an LL
+// line flagged with this step's epoch, then compares all P lines.
+struct ConsistencyArgs {
+  uint4* recv = nullptr;                  // own receive buffer (consistency area)
+  uint4* peer_recv[kMaxPeers] = {nullptr};  // every rank's consistency area
+  int rank = 0, P = 1, loopback = 0, flag_ofs = 0;
+};
+
 __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int32_t* tokens,
                                                          const int32_t* parents, int T_in, const uint16_t* E,
                                                          int V, int h, float* x, const uint16_t* gain,
                                                          uint8_t* act, int NT, float eps, int epoch_stride,
-                                                         const uint4* mbox_in) {
+                                                         const uint4* mbox_in, int max_tree, ConsistencyArgs ca) {
   __shared__ int s_tok[SS_MAX_TREE], s_par[SS_MAX_TREE];
   __shared__ int s_bad;
   __shared__ int s_T;
+  __shared__ int s_tmo;
   __shared__ float s_red[8];
   pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
+  // graph capacity: the step was captured for 8*NT token slots (and the KV /
+  // RoPE capacity checks assumed max_tree): larger trees are refused
+  const int cap = min(8 * NT, max_tree);
+  if (tid == 0) s_tmo = 0;
   // a13: the tree arrives in the inbox as LL lines ("sends a
   // sub-graph ... to the target worker"): line 0 = (T, seq), line 1+i =
   // (token_i, parent_i), every line flagged with the message sequence number.
@@ -56,24 +71,28 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     const uint32_t seq = st->mbox_seq + 1;
     if (tid == 0) {
       uint32_t d1 = 0, d2 = 0;
-      s_T = ll_wait(mbox_in, seq, d1, d2) ? (int)d1 : 0;
+      const bool ok = ll_wait(mbox_in, seq, d1, d2);
+      s_T = ok ? (int)d1 : 0;
+      if (!ok) s_tmo = 1;
       if (blockIdx.x == 0 && blockIdx.y == 0) {
         st->mbox_cur = seq;
         st->mbox_mode = 1;
-        if (s_T == 0) st->timeout = 1;
       }
     }
     __syncthreads();
     T_in = s_T;
-    if (tid < min(max(T_in, 0), SS_MAX_TREE)) {
-      if (!ll_wait(mbox_in + 1 + tid, seq, mtok, mpar)) { mtok = 0; mpar = 0; }
+    if (tid < min(max(T_in, 0), cap)) {
+      // a line that never arrives is a timeout of the whole message (never a
+      // silently substituted node)
+      if (!ll_wait(mbox_in + 1 + tid, seq, mtok, mpar)) { mtok = 0; mpar = 0; s_tmo = 1; }
     }
   } else if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
     st->mbox_mode = 0;
   }
-  const int T = min(max(T_in, 1), SS_MAX_TREE);
-  if (tid == 0) s_bad = (T_in < 1 || T_in > SS_MAX_TREE) ? 1 : 0;
+  const int T = min(max(T_in, 1), cap);
+  if (tid == 0) s_bad = (T_in < 1 || T_in > cap) ? 1 : 0;
   __syncthreads();
+  if (s_tmo && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) st->timeout = 1;
   if (tid < T) {
     int p = mbox_in ? (int)mpar : parents[tid], tk = mbox_in ? (int)mtok : tokens[tid];
     bool bad = (tid == 0) ? (p != -1) : (p < 0 || p >= tid);
@@ -104,12 +123,32 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     }
     if (tid == 0) {
       st->T = T;
-      st->status = s_bad ? SS_EINVAL : SS_OK;
+      int status = s_bad ? SS_EINVAL : SS_OK;
       // LL flag epoch of this step: flags epoch + [0, epoch_stride) are used
       // by the all-reduces and the argmax exchange; 0 is never a live flag.
       uint32_t e = st->epoch + (uint32_t)epoch_stride;
       if (e < st->epoch || e + (uint32_t)epoch_stride < e) e = 1;
       st->epoch = e;
+      st->max_written = max(st->max_written, st->L + T);
+      if ((st->debug & SS_DEBUG_CONSISTENCY) && ca.P > 1) {
+        uint32_t hsh = 2166136261u ^ (uint32_t)T_in;
+        for (int i = 0; i < T; ++i) {
+          hsh = (hsh ^ (uint32_t)s_tok[i]) * 16777619u;
+          hsh = (hsh ^ (uint32_t)s_par[i]) * 16777619u;
+        }
+        hsh ^= (uint32_t)s_bad << 31;
+        const uint32_t flag = e + (uint32_t)ca.flag_ofs;
+        for (int p = 0; p < ca.P; ++p)
+          ll_store(ca.peer_recv[p] + (ca.loopback ? p : ca.rank), hsh, (uint32_t)T, flag);
+        for (int p = 0; p < ca.P; ++p) {
+          uint32_t d1 = 0, d2 = 0;
+          long spins = 0;
+          while (!ll_try_load(ca.recv + p, flag, d1, d2))
+            if (++spins > (1L << 26)) { st->timeout = 1; break; }
+          if (d1 != hsh) status = SS_ECONSISTENCY;
+        }
+      }
+      st->status = status;
     }
   }
   const int nv = h / 4;  // 4-element vectors per row
@@ -165,9 +204,21 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
                        cudaStream_t st, bool from_mailbox) {
   const uint16_t* g0 = s->layers[0].attn_norm;
+  ConsistencyArgs ca;
+  ca.rank = s->rank;
+  ca.P = s->P;
+  ca.loopback = s->loopback ? 1 : 0;
+  ca.flag_ofs = 2 * s->cfg.n_layers + 1;  // inside the step's epoch stride, unused by the all-reduces
+  if (s->P > 1 && s->recv) {
+    const size_t ofs = consistency_line_offset(s);
+    ca.recv = reinterpret_cast<uint4*>(s->recv) + ofs;
+    for (int p = 0; p < s->P; ++p)
+      ca.peer_recv[p] = s->peer_recv[p] ? reinterpret_cast<uint4*>(s->peer_recv[p]) + ofs : nullptr;
+  }
   launch_pdl(embed_meta_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, s->dstate, tokens, parents, T,
              (const uint16_t*)s->embed, s->cfg.vocab, s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
-             2 * s->cfg.n_layers + 2, from_mailbox ? (const uint4*)s->mbox_in : (const uint4*)nullptr);
+             2 * s->cfg.n_layers + 2, from_mailbox ? (const uint4*)s->mbox_in : (const uint4*)nullptr,
+             s->cfg.max_tree, ca);
 }
 
 // ---------------------------------------------------------------- a13 draft-side helpers
@@ -192,23 +243,26 @@ void launch_mailbox_post(void* inbox, const int32_t* tokens, const int32_t* pare
   mailbox_post_kernel<<<1, SS_MAX_TREE, 0, st>>>((uint4*)inbox, t, T, seq);
 }
 // Wait for the verified path with sequence number seq in an outbox and copy
-// it out: out[0] = n_accepted, out[1] = bonus, out[2] = stop, then n
-// (node index, token) pairs.
+// it out: out[0] = n_accepted, out[1] = bonus, out[2] = stop, out[3] = the
+// step's status (SS_OK, or SS_EINVAL / SS_ETIMEOUT / SS_ECONSISTENCY: then
+// n = 0 and no path follows), then n (node index, token) pairs.  A message
+// that never arrives gives n = -1, status SS_ETIMEOUT.
 __global__ void mailbox_recv_kernel(const uint4* outbox, uint32_t seq, int32_t* out) {
   __shared__ int s_n;
   uint32_t d1 = 0, d2 = 0;
   if (threadIdx.x == 0) {
     const bool ok = ll_wait(outbox, seq, d1, d2);
-    s_n = ok ? (int)(d1 & 0x7FFFFFFFu) : -1;
+    s_n = ok ? (int)(d1 & 0xFFFFu) : -1;
     out[0] = s_n;
-    out[1] = (int)d2;
-    out[2] = (int)(d1 >> 31);
+    out[1] = ok ? (int)d2 : 0;
+    out[2] = ok ? (int)(d1 >> 31) : 0;
+    out[3] = ok ? -(int)((d1 >> 16) & 0xFFu) : SS_ETIMEOUT;
   }
   __syncthreads();
   const int i = threadIdx.x;
   if (i < s_n && ll_wait(outbox + 1 + i, seq, d1, d2)) {
-    out[3 + 2 * i] = (int)d1;
-    out[4 + 2 * i] = (int)d2;
+    out[4 + 2 * i] = (int)d1;
+    out[5 + 2 * i] = (int)d2;
   }
 }
 void launch_mailbox_recv(const void* outbox, uint32_t seq, int32_t* dev_out, cudaStream_t st) {

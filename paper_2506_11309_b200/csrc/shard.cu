@@ -18,23 +18,44 @@
 using namespace ss;
 
 
+// Error messages: the calling thread's last one (ss_last_error(NULL), e.g.
+// after a failed ss_init_shard) and the last one per shard.  SCOPE(s) at the
+// top of an entry point makes FAIL / CUDA_TRY record into that shard too.
 static thread_local std::string g_err;
+static thread_local ss_shard* g_scope = nullptr;
+struct ScopeGuard {
+  ss_shard* prev;
+  explicit ScopeGuard(ss_shard* s) : prev(g_scope) { g_scope = s; }
+  ~ScopeGuard() { g_scope = prev; }
+};
+#define SCOPE(s) ScopeGuard scope_guard_((s))
+static void set_err(const std::string& m) {
+  g_err = m;
+  if (g_scope) g_scope->err = m;
+}
 
 #define FAIL(code, msg)  \
   do {                   \
-    g_err = (msg);       \
+    set_err(msg);        \
     return (code);       \
   } while (0)
 #define CUDA_TRY(x)                                                            \
   do {                                                                         \
     cudaError_t e_ = (x);                                                      \
     if (e_ != cudaSuccess) {                                                   \
-      g_err = std::string(#x) + ": " + cudaGetErrorString(e_);                 \
+      set_err(std::string(#x) + ": " + cudaGetErrorString(e_));                \
       return SS_ECUDA;                                                         \
     }                                                                          \
   } while (0)
+// a host_logic.h check: propagate its status and message
+#define HOST_CHECK(call, ...)                              \
+  do {                                                     \
+    std::string m_;                                        \
+    ss_status r_ = ss::host::call(__VA_ARGS__, m_);        \
+    if (r_ != SS_OK) FAIL(r_, m_);                         \
+  } while (0)
 
-extern "C" const char* ss_last_error(void) { return g_err.c_str(); }
+extern "C" const char* ss_last_error(const ss_shard* s) { return s ? s->err.c_str() : g_err.c_str(); }
 
 // ------------------------------------------------------------ generator keys
 // Mirror of synth/generators.py stream_key / tensor_id.
@@ -264,6 +285,10 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   s->V_l = std::max(0, std::min(c.vocab, (tp_rank + 1) * vp) - s->V_off);
   s->V_l_pad = round_up(std::max(s->V_l, 1), 128);
   s->max_ctx_pad = round_up(c.max_ctx, 64);
+  s->hs.max_ctx = c.max_ctx;
+  s->hs.max_tree = c.max_tree;
+  s->hs.vocab = c.vocab;
+  s->hs.peers_ready = tp_size == 1;
   const int h = c.hidden, d = c.head_dim;
 
   auto fail = [&](ss_status st) {
@@ -274,7 +299,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   do {                                                                       \
     cudaError_t e_ = dalloc(&(ptr), (bytes));                                \
     if (e_ != cudaSuccess) {                                                 \
-      g_err = std::string("cudaMalloc ") + #ptr + ": " + cudaGetErrorString(e_); \
+      set_err(std::string("cudaMalloc ") + #ptr + ": " + cudaGetErrorString(e_)); \
       return fail(SS_ECUDA);                                                 \
     }                                                                        \
   } while (0)
@@ -329,7 +354,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   if (!mk_scratch(s->sc_qkv, s->layers[0].qkv.n_tg) || !mk_scratch(s->sc_o, s->layers[0].o.n_tg) ||
       !mk_scratch(s->sc_gu, s->layers[0].gu.n_tg) || !mk_scratch(s->sc_down, s->layers[0].down.n_tg) ||
       !mk_scratch(s->sc_lm, s->lm_head.n_tg)) {
-    g_err = "cudaMalloc scratch failed";
+    set_err("cudaMalloc scratch failed");
     return fail(SS_ECUDA);
   }
   A(s->logits_dev, (size_t)SS_MAX_TREE * s->V_l_pad * 4);
@@ -337,7 +362,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   A(s->d_tree_in, 2 * SS_MAX_TREE * 4);
   if (cudaMallocHost((void**)&s->hstate, sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost((void**)&s->h_tree_in, 2 * SS_MAX_TREE * 4) != cudaSuccess) {
-    g_err = "cudaMallocHost failed";
+    set_err("cudaMallocHost failed");
     return fail(SS_ECUDA);
   }
   {
@@ -346,22 +371,24 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
     init.eos = -1;
     init.mbox_post = tp_rank == 0 ? 1 : 0;
     if (cudaMemcpy(s->dstate, &init, sizeof(DevState), cudaMemcpyHostToDevice) != cudaSuccess) {
-      g_err = "init state copy failed";
+      set_err("init state copy failed");
       return fail(SS_ECUDA);
     }
   }
-  // LL receive buffer: [P][n_tg_total][128 rows][32 lines] x 16 B (fp32 pairs + flags)
+  // LL receive buffer: [2 parities][P][n_tg_total][128 rows][32 lines] x 16 B
+  // (fp32 pairs + flags), then the argmax area [P][64] and the debug
+  // consistency area [P] (consistency_line_offset)
   A(s->mbox_in, (size_t)(1 + SS_MAX_TREE) * 16);
   if (tp_size > 1) {
-    s->recv_bytes = ((size_t)2 * tp_size * (h / 128) * 128 * 32 + (size_t)tp_size * 64) * 16;
+    s->recv_bytes = ((size_t)2 * tp_size * (h / 128) * 128 * 32 + (size_t)tp_size * 64 + (size_t)tp_size) * 16;
     A(s->recv, s->recv_bytes);
   }
   if (cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
-    g_err = "stream create failed";
+    set_err("stream create failed");
     return fail(SS_ECUDA);
   }
   if (cudaDeviceSynchronize() != cudaSuccess) {
-    g_err = std::string("init: ") + cudaGetErrorString(cudaGetLastError());
+    set_err(std::string("init: ") + cudaGetErrorString(cudaGetLastError()));
     return fail(SS_ECUDA);
   }
 #undef A
@@ -396,6 +423,7 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
 }
 
 extern "C" ss_status ss_set_launch_cap(ss_shard* s, int32_t cap) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
   s->launch_cap = cap > 0 ? cap : 0;
   for (auto& kv : s->graphs)
@@ -458,6 +486,7 @@ static ss_status try_pack_layer(ss_shard* s, int layer, int group_kind) {
 
 extern "C" ss_status ss_load_weights(ss_shard* s, int32_t layer, int32_t kind, int32_t sub, const void* host,
                                      size_t bytes) {
+  SCOPE(s);
   if (!s || !host) FAIL(SS_EINVAL, "null argument");
   const ss_model_cfg& c = s->cfg;
   const int h = c.hidden;
@@ -520,6 +549,7 @@ extern "C" ss_status ss_load_weights(ss_shard* s, int32_t layer, int32_t kind, i
 }
 
 extern "C" ss_status ss_synth_weights(ss_shard* s, uint64_t seed) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
   cudaSetDevice(s->device);
   const ss_model_cfg& c = s->cfg;
@@ -575,15 +605,21 @@ static bool weights_complete(const ss_shard* s) {
 }
 
 // ------------------------------------------------------------ KV
-static ss_status write_L(ss_shard* s, int L) {
-  CUDA_TRY(cudaMemcpy(&s->dstate->L, &L, 4, cudaMemcpyHostToDevice));
-  s->L_host = L;
-  s->L_known = true;
-  s->L_upper = L;
+// Set the committed length on the device and the host view; rows [0, rows)
+// now hold data (prefix) -- DevState::max_written mirrors hs.max_written.
+static ss_status write_L(ss_shard* s, int L, int rows_written) {
+  s->hs.max_written = std::max(s->hs.max_written, rows_written);
+  int32_t v[2] = {L, 0};
+  CUDA_TRY(cudaMemcpy(&s->dstate->L, &v[0], 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(&s->dstate->max_written, &s->hs.max_written, 4, cudaMemcpyHostToDevice));
+  ss::host::on_set_len(s->hs, L);
+  int zero = 0;
+  CUDA_TRY(cudaMemcpy(&s->dstate->have_verify, &zero, 4, cudaMemcpyHostToDevice));
   return SS_OK;
 }
 
 extern "C" ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k, const void* v, int32_t len) {
+  SCOPE(s);
   if (!s || (!k && len) || (!v && len)) FAIL(SS_EINVAL, "null argument");
   const ss_model_cfg& c = s->cfg;
   if (layer < 0 || layer >= c.n_layers) FAIL(SS_EINVAL, "layer out of range");
@@ -612,12 +648,12 @@ extern "C" ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k,
       CUDA_TRY(cudaMemcpy(cache + base, buf.data(), (size_t)rows * d * 2, cudaMemcpyHostToDevice));
     }
   }
-  s->max_rows_written = std::max(s->max_rows_written, len);
-  if (layer == c.n_layers - 1) return write_L(s, len);
+  if (layer == c.n_layers - 1) return write_L(s, len, len);
   return SS_OK;
 }
 
 extern "C" ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
   const ss_model_cfg& c = s->cfg;
   if (len < 0 || len + c.max_tree > c.max_ctx) FAIL(SS_ECAPACITY, "prefix + max_tree exceeds max_ctx");
@@ -630,11 +666,11 @@ extern "C" ss_status ss_synth_prefix_kv(ss_shard* s, uint64_t seed, int32_t len)
                         stream_key(seed, tensor_id(l, 13, 0)), 0);
   }
   CUDA_TRY(cudaDeviceSynchronize());
-  s->max_rows_written = std::max(s->max_rows_written, len);
-  return write_L(s, len);
+  return write_L(s, len, len);
 }
 
 extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_t n, float* k_out, float* v_out) {
+  SCOPE(s);
   if (!s || !k_out || !v_out) FAIL(SS_EINVAL, "null argument");
   const ss_model_cfg& c = s->cfg;
   if (layer < 0 || layer >= c.n_layers || row0 < 0 || n < 0 || row0 + n > s->max_ctx_pad)
@@ -662,29 +698,40 @@ extern "C" ss_status ss_read_kv(ss_shard* s, int32_t layer, int32_t row0, int32_
   return SS_OK;
 }
 
-extern "C" ss_status ss_set_committed_len(ss_shard* s, int32_t L) {
-  if (!s) FAIL(SS_EINVAL, "null shard");
-  if (L < 0 || L + s->cfg.max_tree > s->cfg.max_ctx) FAIL(SS_ECAPACITY, "length out of range");
+// Read the device-side committed length and rows-written bound back (after
+// device-driven commits the host only knows an upper bound).
+static ss_status sync_L(ss_shard* s) {
+  if (s->hs.L_known) return SS_OK;
   cudaSetDevice(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
-  s->have_verify = false;
-  int zero = 0;
-  CUDA_TRY(cudaMemcpy(&s->dstate->have_verify, &zero, 4, cudaMemcpyHostToDevice));
-  return write_L(s, L);
+  int32_t L = -1, mw = 0;
+  CUDA_TRY(cudaMemcpy(&L, &s->dstate->L, 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&mw, &s->dstate->max_written, 4, cudaMemcpyDeviceToHost));
+  s->hs.L = L;
+  s->hs.L_known = true;
+  s->hs.max_written = std::max(s->hs.max_written, std::max(mw, L));
+  return SS_OK;
+}
+
+extern "C" ss_status ss_set_committed_len(ss_shard* s, int32_t L) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  ss_status r = sync_L(s);
+  if (r != SS_OK) return r;
+  int32_t mw = 0;
+  CUDA_TRY(cudaMemcpy(&mw, &s->dstate->max_written, 4, cudaMemcpyDeviceToHost));
+  s->hs.max_written = std::max(s->hs.max_written, mw);
+  HOST_CHECK(check_set_len, s->hs, L);
+  return write_L(s, L, 0);
 }
 
 extern "C" int32_t ss_committed_len(ss_shard* s) {
+  SCOPE(s);
   if (!s) return -1;
-  if (!s->L_known) {
-    cudaSetDevice(s->device);
-    int L = -1;
-    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpy(&L, &s->dstate->L, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    s->L_host = L;
-    s->L_upper = L;
-    s->L_known = true;
-  }
-  return s->L_host;
+  if (sync_L(s) != SS_OK) return -1;
+  return s->hs.L;
 }
 
 // ------------------------------------------------------------ the step
@@ -756,9 +803,14 @@ static Prof* g_prof = nullptr;
 static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, cudaStream_t st) {
   const ss_model_cfg& c = s->cfg;
   int n = 0;
-  // timing experiments only (results are wrong): SS_EXP_SKIP = bitmask of
+  // timing experiments only (results are wrong; experiment builds only, the
+  // product library always runs every launch): SS_EXP_SKIP = bitmask of
   // launches to leave out, 1 qkv, 2 attention, 4 o, 8 gate/up, 16 down
-  static const int skip = getenv("SS_EXP_SKIP") ? atoi(getenv("SS_EXP_SKIP")) : 0;
+#ifdef SS_EXPERIMENTS
+  static const int skip = exp_env_int("SS_EXP_SKIP", 0);
+#else
+  constexpr int skip = 0;
+#endif
   const int cap = s->launch_cap;
   // fake-peer TP (ranks share this GPU): no PDL, see ss_pdl_off
   ss_pdl_off = s->P > 1 && cap > 0 && !s->loopback;
@@ -780,7 +832,6 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     a.d = c.head_dim;
     a.max_ctx_pad = s->max_ctx_pad;
     a.NT = NT;
-    a.L_hint = s->L_known ? s->L_host : 0;
     a.qbuf = s->qbuf;
     a.kc = s->kcache;
     a.vc = s->vcache;
@@ -860,25 +911,14 @@ static ss_status get_graph(ss_shard* s, int NT, int auto_commit, int want_logits
   return SS_OK;
 }
 
-static ss_status validate_tree(const ss_shard* s, const int32_t* tokens, const int32_t* parents, int T) {
-  if (!tokens || !parents) FAIL(SS_EINVAL, "null tree");
-  if (T < 1 || T > s->cfg.max_tree) FAIL(SS_EINVAL, "T out of [1, max_tree]");
-  if (parents[0] != -1) FAIL(SS_EINVAL, "parents[0] must be -1 (root first)");
-  for (int i = 1; i < T; ++i)
-    if (parents[i] < 0 || parents[i] >= i) FAIL(SS_EINVAL, "parents[i] must be in [0, i)");
-  for (int i = 0; i < T; ++i)
-    if (tokens[i] < 0 || tokens[i] >= s->cfg.vocab) FAIL(SS_EINVAL, "token out of vocab");
-  return SS_OK;
-}
-
 static ss_status check_ready(ss_shard* s, int T) {
-  if (!weights_complete(s)) FAIL(SS_ESTATE, "weights not fully loaded");
-  if (s->P > 1 && !s->peers_ready) FAIL(SS_ESTATE, "peers not imported (tp_size > 1)");
-  int L = s->L_known ? s->L_host : s->L_upper;
-  if (L + T > s->cfg.max_ctx) {
-    L = ss_committed_len(s);
-    if (L + T > s->cfg.max_ctx) FAIL(SS_ECAPACITY, "L + T exceeds max_ctx");
+  s->hs.weights_ready = weights_complete(s);
+  s->hs.peers_ready = s->P == 1 || s->peers_ready;
+  if (!s->hs.L_known && (int64_t)s->hs.L + T > s->cfg.max_ctx) {  // upper bound too loose: read L back
+    ss_status r = sync_L(s);
+    if (r != SS_OK) return r;
   }
+  HOST_CHECK(check_verify, s->hs, T);
   return SS_OK;
 }
 
@@ -891,17 +931,25 @@ static ss_status run_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d
   launch_embed_meta(s, d_tokens, d_parents, T, NT, st, from_mailbox);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaGraphLaunch(gr->exec, st));
-  s->last_T = T;
   return SS_OK;
+}
+
+static const char* status_msg(int st) {
+  switch (st) {
+    case SS_EINVAL: return "device-side tree validation failed";
+    case SS_ETIMEOUT: return "a peer / mailbox flag poll exceeded its budget";
+    case SS_ECONSISTENCY: return "TP ranks were called with different trees (debug checksum)";
+    default: return "verify failed";
+  }
 }
 
 extern "C" ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T,
                                     ss_verify_result* out, float* logits_out, void* stream) {
+  SCOPE(s);
   if (!s || !out) FAIL(SS_EINVAL, "null argument");
-  ss_status r = validate_tree(s, tokens, parents, T);
-  if (r != SS_OK) return r;
+  HOST_CHECK(check_tree, s->hs, tokens, parents, T);
   cudaSetDevice(s->device);
-  r = check_ready(s, T);
+  ss_status r = check_ready(s, T);
   if (r != SS_OK) return r;
   cudaStream_t st = (cudaStream_t)stream;
   std::memcpy(s->h_tree_in, tokens, T * 4);
@@ -916,13 +964,18 @@ extern "C" ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const in
                                (size_t)s->V_l * 4, T, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   std::memcpy(out, &s->hstate->result, sizeof(ss_verify_result));
-  s->have_verify = true;
+  if (out->status != SS_OK) {  // device-detected failure: nothing to commit (out is still filled)
+    s->hs.max_written = std::max(s->hs.max_written, s->hs.L + T);
+    FAIL((ss_status)out->status, status_msg(out->status));
+  }
+  ss::host::on_verify(s->hs, T, parents, false);
   return SS_OK;
 }
 
 extern "C" ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
                                         ss_verify_result* d_result, float* d_logits, int32_t auto_commit,
                                         void* stream) {
+  SCOPE(s);
   if (!s || !d_tokens || !d_parents) FAIL(SS_EINVAL, "null argument");
   if (T < 1 || T > s->cfg.max_tree) FAIL(SS_EINVAL, "T out of [1, max_tree]");
   cudaSetDevice(s->device);
@@ -936,33 +989,36 @@ extern "C" ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, co
   if (d_logits)
     CUDA_TRY(cudaMemcpy2DAsync(d_logits, (size_t)s->V_l * 4, s->logits_dev, (size_t)s->V_l_pad * 4,
                                (size_t)s->V_l * 4, T, cudaMemcpyDeviceToDevice, st));
-  if (auto_commit) {
-    s->L_known = false;
-    s->L_upper += T;
-    s->have_verify = false;
-  } else {
-    s->have_verify = true;
-  }
+  ss::host::on_verify(s->hs, T, nullptr, auto_commit != 0);  // parents live on the device
+  return SS_OK;
+}
+
+// Parents of the last verified tree and its device status (device truth:
+// the tree of a *_dev / mailbox verify never passed through the host).
+static ss_status read_last_tree(ss_shard* s, cudaStream_t st, int32_t* status) {
+  CUDA_TRY(cudaMemcpyAsync(s->hs.last_parents, s->dstate->parents, sizeof(s->hs.last_parents),
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&s->hstate->result.status, &s->dstate->result.status, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&s->hstate->T, &s->dstate->T, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *status = s->hstate->result.status;
+  s->hs.last_T = s->hstate->T;
   return SS_OK;
 }
 
 extern "C" ss_status ss_commit_kv(ss_shard* s, const int32_t* accepted, int32_t n, void* stream) {
+  SCOPE(s);
   if (!s || !accepted) FAIL(SS_EINVAL, "null argument");
-  if (!s->have_verify) FAIL(SS_ESTATE, "commit without a preceding verify");
-  if (n < 1 || n > s->last_T) FAIL(SS_EINVAL, "n out of [1, T]");
-  if (accepted[0] != 0) FAIL(SS_EINVAL, "chain must start at the root (node 0)");
-  // chain: accepted[k] must be a child of accepted[k-1] in the last tree
-  int32_t hpar[SS_MAX_TREE];
+  if (!s->hs.have_verify) FAIL(SS_ESTATE, "commit without a preceding verify");
   cudaSetDevice(s->device);
   cudaStream_t st = (cudaStream_t)stream;
-  CUDA_TRY(cudaMemcpyAsync(hpar, s->dstate->parents, sizeof(hpar), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  for (int k = 1; k < n; ++k) {
-    if (accepted[k] <= 0 || accepted[k] >= s->last_T || hpar[accepted[k]] != accepted[k - 1])
-      FAIL(SS_EINVAL, "accepted is not a root-anchored chain of the last tree");
-  }
-  int L = ss_committed_len(s);
-  if (L < 0) FAIL(SS_ECUDA, "cannot read committed length");
+  int32_t vstatus = 0;
+  ss_status r = read_last_tree(s, st, &vstatus);
+  if (r != SS_OK) return r;
+  if (vstatus != SS_OK) FAIL(SS_ESTATE, "the last verify failed on the device; nothing to commit");
+  HOST_CHECK(check_commit, s->hs, accepted, n);
+  r = sync_L(s);
+  if (r != SS_OK) return r;
   std::vector<int32_t> buf(1 + SS_MAX_TREE, 0);
   buf[0] = n;
   for (int k = 0; k < n; ++k) buf[1 + k] = accepted[k];
@@ -971,24 +1027,32 @@ extern "C" ss_status ss_commit_kv(ss_shard* s, const int32_t* accepted, int32_t 
   launch_commit(s, 0, st);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
-  s->L_host = L + n;
-  s->L_upper = s->L_host;
-  s->L_known = true;
-  s->max_rows_written = std::max(s->max_rows_written, s->L_host);
-  s->have_verify = false;
+  ss::host::on_commit(s->hs, n);
   return SS_OK;
 }
 
 extern "C" ss_status ss_commit_accepted(ss_shard* s, void* stream) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
-  if (!s->have_verify) FAIL(SS_ESTATE, "commit without a preceding verify");
+  if (!s->hs.have_verify) FAIL(SS_ESTATE, "commit without a preceding verify");
   cudaSetDevice(s->device);
   cudaStream_t st = (cudaStream_t)stream;
-  launch_commit(s, 1, st);
+  launch_commit(s, 1, st);  // the device commits only a verify whose status is SS_OK
   CUDA_TRY(cudaGetLastError());
-  s->L_known = false;
-  s->L_upper += s->last_T;
-  s->have_verify = false;
+  s->hs.L_known = false;
+  s->hs.L += s->hs.last_T;  // upper bound until read back
+  s->hs.have_verify = false;
+  return SS_OK;
+}
+
+extern "C" ss_status ss_set_debug(ss_shard* s, int32_t flags) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  if (flags & ~SS_DEBUG_CONSISTENCY) FAIL(SS_EINVAL, "unknown debug flag");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(&s->dstate->debug, &flags, 4, cudaMemcpyHostToDevice));
+  s->debug = flags;
   return SS_OK;
 }
 
@@ -1001,6 +1065,7 @@ extern "C" int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_comm
 
 // ------------------------------------------------------------ peers (TP)
 extern "C" ss_status ss_export_handle(ss_shard* s, void* buf, size_t* len) {
+  SCOPE(s);
   if (!s || !buf || !len) FAIL(SS_EINVAL, "null argument");
   if (s->P == 1) {
     *len = 0;
@@ -1015,6 +1080,7 @@ extern "C" ss_status ss_export_handle(ss_shard* s, void* buf, size_t* len) {
 }
 
 extern "C" ss_status ss_import_peers(ss_shard* s, const void* const* blobs, const size_t* lens) {
+  SCOPE(s);
   if (!s || !blobs || !lens) FAIL(SS_EINVAL, "null argument");
   cudaSetDevice(s->device);
   for (int p = 0; p < s->P; ++p) {
@@ -1038,6 +1104,7 @@ extern "C" ss_status ss_import_peers(ss_shard* s, const void* const* blobs, cons
 }
 
 extern "C" ss_status ss_import_local_peers(ss_shard* s, ss_shard* const* shards) {
+  SCOPE(s);
   if (!s || !shards) FAIL(SS_EINVAL, "null argument");
   cudaSetDevice(s->device);
   for (int p = 0; p < s->P; ++p) {
@@ -1057,6 +1124,7 @@ extern "C" ss_status ss_import_local_peers(ss_shard* s, ss_shard* const* shards)
 }
 
 extern "C" ss_status ss_import_loopback(ss_shard* s) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null argument");
   if (s->P < 2) FAIL(SS_EINVAL, "loopback needs tp_size > 1");
   for (int p = 0; p < s->P; ++p) s->peer_recv[p] = s->recv;
@@ -1070,6 +1138,7 @@ extern "C" ss_status ss_import_loopback(ss_shard* s) {
 
 extern "C" ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
                                      float* ms, int32_t* count, void* stream) {
+  SCOPE(s);
   if (!s || !d_tokens || !d_parents || !ms || !count) FAIL(SS_EINVAL, "null argument");
   if (T < 1 || T > s->cfg.max_tree) FAIL(SS_EINVAL, "T out of [1, max_tree]");
   cudaSetDevice(s->device);
@@ -1102,20 +1171,20 @@ extern "C" ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const
     ms[prof.ev[i].first] += t;
     count[prof.ev[i].first] += 1;
   }
-  s->L_known = false;
-  s->L_upper += T;
-  s->have_verify = false;
+  ss::host::on_verify(s->hs, T, nullptr, true);
   return SS_OK;
 }
 
 // ------------------------------------------------------------ a13 mailbox
 extern "C" ss_status ss_mailbox_inbox(ss_shard* s, void** dev_ptr) {
+  SCOPE(s);
   if (!s || !dev_ptr) FAIL(SS_EINVAL, "null argument");
   *dev_ptr = s->mbox_in;
   return SS_OK;
 }
 
 extern "C" ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eos_token) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
   cudaSetDevice(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
@@ -1126,6 +1195,7 @@ extern "C" ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eo
 }
 
 extern "C" ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream) {
+  SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
   cudaSetDevice(s->device);
   const int T = s->cfg.max_tree;  // the tree size arrives with the message
@@ -1134,14 +1204,7 @@ extern "C" ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, vo
   cudaStream_t st = (cudaStream_t)stream;
   r = run_step(s, nullptr, nullptr, T, auto_commit ? 1 : 0, 0, st, true);
   if (r != SS_OK) return r;
-  if (auto_commit) {
-    s->L_known = false;
-    s->L_upper += T;
-    s->have_verify = false;
-  } else {
-    s->have_verify = true;
-    s->last_T = T;
-  }
+  ss::host::on_verify(s->hs, T, nullptr, auto_commit != 0);  // T: upper bound (the message carries it)
   return SS_OK;
 }
 

@@ -48,7 +48,9 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_set_prefix_kv", "ss_synth_prefix_kv", "ss_read_kv", "ss_set_committed_len",
            "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
-           "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result"]
+           "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
+           "ss_set_debug"]
+SS_DEBUG_CONSISTENCY = 1
 
 
 def lib():
@@ -69,7 +71,8 @@ def lib():
         "ss_import_loopback": (i32, [vp]),
         "ss_set_launch_cap": (i32, [vp, i32]),
         "ss_destroy": (i32, [vp]),
-        "ss_last_error": (C.c_char_p, []),
+        "ss_last_error": (C.c_char_p, [vp]),
+        "ss_set_debug": (i32, [vp, i32]),
         "ss_load_weights": (i32, [vp, i32, i32, i32, vp, sz]),
         "ss_synth_weights": (i32, [vp, u64]),
         "ss_set_prefix_kv": (i32, [vp, i32, vp, vp, i32]),
@@ -97,9 +100,9 @@ def lib():
     return L
 
 
-def _check(code: int):
+def _check(code: int, shard=None):
     if code != 0:
-        raise SwiftSpecError(code, lib().ss_last_error().decode())
+        raise SwiftSpecError(code, lib().ss_last_error(shard).decode())
 
 
 def _ptr(a: np.ndarray):
@@ -132,6 +135,13 @@ class Shard:
         self.v_l = max(0, min(cfg.vocab, (tp_rank + 1) * vp) - self.v_off)
         self.hkv_l = cfg.n_kv_heads // tp_size
 
+    def _ck(self, code: int):
+        _check(code, self.h)
+
+    def set_debug(self, flags: int):
+        """SS_DEBUG_CONSISTENCY: cross-rank checksum of every verify's tree."""
+        self._ck(lib().ss_set_debug(self.h, flags))
+
     def close(self):
         if getattr(self, "h", None):
             try:
@@ -145,7 +155,7 @@ class Shard:
     # ---- weights / KV
     def load_tensor(self, layer: int, kind: int, sub: int, arr: np.ndarray):
         a = np.ascontiguousarray(arr)
-        _check(lib().ss_load_weights(self.h, layer, kind, sub, _ptr(a), a.nbytes))
+        self._ck(lib().ss_load_weights(self.h, layer, kind, sub, _ptr(a), a.nbytes))
 
     def load_canonical(self, m: dict):
         """Load a canonical model dict (synth.gen_model layout)."""
@@ -164,32 +174,32 @@ class Shard:
         self.load_tensor(0, KIND["LM_HEAD"], 0, m["lm_head"])
 
     def synth_weights(self, seed: int):
-        _check(lib().ss_synth_weights(self.h, seed))
+        self._ck(lib().ss_synth_weights(self.h, seed))
 
     def set_prefix_kv(self, layer: int, k_bits: np.ndarray, v_bits: np.ndarray):
         k = np.ascontiguousarray(k_bits, dtype=np.uint16)
         v = np.ascontiguousarray(v_bits, dtype=np.uint16)
-        _check(lib().ss_set_prefix_kv(self.h, layer, _ptr(k), _ptr(v), k.shape[0]))
+        self._ck(lib().ss_set_prefix_kv(self.h, layer, _ptr(k), _ptr(v), k.shape[0]))
 
     def synth_prefix_kv(self, seed: int, L: int):
-        _check(lib().ss_synth_prefix_kv(self.h, seed, L))
+        self._ck(lib().ss_synth_prefix_kv(self.h, seed, L))
 
     def read_kv(self, layer: int, row0: int, n: int):
         """Cache rows as float32 [n][n_kv_heads/tp][head_dim] (stored fp16)."""
         d = self.cfg.head_dim
         k = np.zeros((n, self.hkv_l, d), dtype=np.float32)
         v = np.zeros((n, self.hkv_l, d), dtype=np.float32)
-        _check(lib().ss_read_kv(self.h, layer, row0, n, _ptr(k), _ptr(v)))
+        self._ck(lib().ss_read_kv(self.h, layer, row0, n, _ptr(k), _ptr(v)))
         return k, v
 
     def set_committed_len(self, L: int):
-        _check(lib().ss_set_committed_len(self.h, L))
+        self._ck(lib().ss_set_committed_len(self.h, L))
 
     @property
     def L(self) -> int:
         r = lib().ss_committed_len(self.h)
         if r < 0:
-            raise SwiftSpecError(-4, lib().ss_last_error().decode())
+            raise SwiftSpecError(-4, lib().ss_last_error(self.h).decode())
         return r
 
     # ---- the step
@@ -199,7 +209,7 @@ class Shard:
         T = len(t)
         res = VerifyResultC()
         logits = np.zeros((T, self.v_l), dtype=np.float32) if want_logits else None
-        _check(lib().ss_verify_tree(self.h, _ptr(t), _ptr(p), T, C.byref(res),
+        self._ck(lib().ss_verify_tree(self.h, _ptr(t), _ptr(p), T, C.byref(res),
                                     _ptr(logits) if want_logits else None, _stream_handle(stream)))
         n = res.n_accepted
         return dict(n_accepted=n, accepted=list(res.accepted[:n]), bonus=res.bonus_token,
@@ -209,15 +219,15 @@ class Shard:
                    auto_commit: bool = False, stream=None):
         """All-device step: d_* are torch CUDA tensors (or raw pointers)."""
         ptr = lambda x: None if x is None else (x if isinstance(x, int) else x.data_ptr())
-        _check(lib().ss_verify_tree_dev(self.h, ptr(d_tokens), ptr(d_parents), T, ptr(d_result),
+        self._ck(lib().ss_verify_tree_dev(self.h, ptr(d_tokens), ptr(d_parents), T, ptr(d_result),
                                         ptr(d_logits), 1 if auto_commit else 0, _stream_handle(stream)))
 
     def commit_kv(self, accepted, stream=None):
         a = np.ascontiguousarray(accepted, dtype=np.int32)
-        _check(lib().ss_commit_kv(self.h, _ptr(a), len(a), _stream_handle(stream)))
+        self._ck(lib().ss_commit_kv(self.h, _ptr(a), len(a), _stream_handle(stream)))
 
     def commit_accepted(self, stream=None):
-        _check(lib().ss_commit_accepted(self.h, _stream_handle(stream)))
+        self._ck(lib().ss_commit_accepted(self.h, _stream_handle(stream)))
 
     def kernels_per_step(self, T: int, auto_commit: bool = False) -> int:
         return lib().ss_kernels_per_step(self.h, T, 1 if auto_commit else 0)
@@ -230,27 +240,27 @@ class Shard:
         ms = np.zeros(9, dtype=np.float32)
         cnt = np.zeros(9, dtype=np.int32)
         ptr = lambda x: x if isinstance(x, int) else x.data_ptr()
-        _check(lib().ss_profile_step(self.h, ptr(d_tokens), ptr(d_parents), T, _ptr(ms), _ptr(cnt),
+        self._ck(lib().ss_profile_step(self.h, ptr(d_tokens), ptr(d_parents), T, _ptr(ms), _ptr(cnt),
                                      _stream_handle(stream)))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PROF_KINDS)}
 
     # ---- a13 mailbox handoff
     def mailbox_inbox(self) -> int:
         ptr = C.c_void_p()
-        _check(lib().ss_mailbox_inbox(self.h, C.byref(ptr)))
+        self._ck(lib().ss_mailbox_inbox(self.h, C.byref(ptr)))
         return ptr.value
 
     def attach_mailbox(self, outbox_ptr: int, eos: int = -1):
-        _check(lib().ss_attach_mailbox(self.h, outbox_ptr, eos))
+        self._ck(lib().ss_attach_mailbox(self.h, outbox_ptr, eos))
 
     def verify_mailbox(self, auto_commit: bool = True, stream=None):
-        _check(lib().ss_verify_tree_mailbox(self.h, 1 if auto_commit else 0, _stream_handle(stream)))
+        self._ck(lib().ss_verify_tree_mailbox(self.h, 1 if auto_commit else 0, _stream_handle(stream)))
 
     # ---- tensor parallel peers
     def export_handle(self) -> bytes:
         buf = C.create_string_buffer(4096)
         n = C.c_size_t(0)
-        _check(lib().ss_export_handle(self.h, buf, C.byref(n)))
+        self._ck(lib().ss_export_handle(self.h, buf, C.byref(n)))
         return buf.raw[:n.value]
 
     def import_peers(self, blobs):
@@ -259,20 +269,20 @@ class Shard:
         for i, k in enumerate(keep):
             arr[i] = C.cast(k, C.c_void_p)
         lens = (C.c_size_t * len(blobs))(*[len(b) for b in blobs])
-        _check(lib().ss_import_peers(self.h, arr, lens))
+        self._ck(lib().ss_import_peers(self.h, arr, lens))
 
     @staticmethod
     def import_local_peers(shards):
         arr = (C.c_void_p * len(shards))(*[s.h.value for s in shards])
         for s in shards:
-            _check(lib().ss_import_local_peers(s.h, arr))
+            s._ck(lib().ss_import_local_peers(s.h, arr))
 
     def import_loopback(self):
         """Timing emulation of this rank alone (include/swiftspec.h ss_import_loopback)."""
-        _check(lib().ss_import_loopback(self.h))
+        self._ck(lib().ss_import_loopback(self.h))
 
     def set_launch_cap(self, cap: int):
-        _check(lib().ss_set_launch_cap(self.h, cap))
+        self._ck(lib().ss_set_launch_cap(self.h, cap))
 
 
 def result_nbytes() -> int:

@@ -50,7 +50,7 @@ def test_init_rejects_bad_shapes(bad):
     h = C.c_void_p()
     r = pkg.lib().ss_init_shard(C.byref(_cfg(**bad)), 0, 1, 0, C.byref(h))
     assert r == -1 and not h.value
-    assert pkg.lib().ss_last_error()
+    assert pkg.lib().ss_last_error(None)
 
 
 @pytest.mark.parametrize("rank,size", [(0, 3), (2, 2), (-1, 1)])

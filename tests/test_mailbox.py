@@ -36,7 +36,7 @@ def test_mailbox_golden_decode():
     outbox = torch.zeros((1 + 64) * 4, dtype=torch.int32, device="cuda")
     sh.attach_mailbox(outbox.data_ptr(), eos=-1)
     inbox = sh.mailbox_inbox()
-    res = torch.zeros(3 + 2 * 64, dtype=torch.int32, device="cuda")
+    res = torch.zeros(4 + 2 * 64, dtype=torch.int32, device="cuda")
     target_stream, draft_stream = torch.cuda.Stream(), torch.cuda.Stream()
     rng = np.random.default_rng(0)
     out, cur, seq = [], root, 0
@@ -52,10 +52,10 @@ def test_mailbox_golden_decode():
         ssp.mailbox_recv_result(outbox.data_ptr(), seq, res.data_ptr(), stream=draft_stream)
         torch.cuda.synchronize()
         r = res.cpu().numpy()
-        n, bonus, stop = int(r[0]), int(r[1]), int(r[2])
-        nodes = [int(x) for x in r[3:3 + 2 * n:2]]
-        path_tokens = [int(x) for x in r[4:4 + 2 * n:2]]
-        assert stop == 0 and nodes[0] == 0 and path_tokens[0] == cur
+        n, bonus, stop, status = int(r[0]), int(r[1]), int(r[2]), int(r[3])
+        nodes = [int(x) for x in r[4:4 + 2 * n:2]]
+        path_tokens = [int(x) for x in r[5:5 + 2 * n:2]]
+        assert status == 0 and stop == 0 and nodes[0] == 0 and path_tokens[0] == cur
         # distractor children may collide with the greedy token only by chance
         assert n >= len(chain) + 1 or any(toks[c] == ref[len(out) + n - 1] for c in range(1, 8))
         out += path_tokens[1:] + [bonus]
@@ -77,11 +77,11 @@ def test_mailbox_stop_on_eos():
     nxt = O.greedy_decode(cfg, m, kv, 5, 1)[0]
     outbox = torch.zeros((1 + 64) * 4, dtype=torch.int32, device="cuda")
     sh.attach_mailbox(outbox.data_ptr(), eos=nxt)       # the next greedy token is the EOS
-    res = torch.zeros(3 + 2 * 64, dtype=torch.int32, device="cuda")
+    res = torch.zeros(4 + 2 * 64, dtype=torch.int32, device="cuda")
     sh.verify_mailbox(auto_commit=True)
     ssp.mailbox_post_tree(sh.mailbox_inbox(), [5], [-1], 1, stream=torch.cuda.Stream())
     ssp.mailbox_recv_result(outbox.data_ptr(), 1, res.data_ptr(), stream=torch.cuda.Stream())
     torch.cuda.synchronize()
     r = res.cpu().numpy()
-    assert int(r[0]) == 1 and int(r[1]) == nxt and int(r[2]) == 1
+    assert int(r[0]) == 1 and int(r[1]) == nxt and int(r[2]) == 1 and int(r[3]) == 0
     sh.close()

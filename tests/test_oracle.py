@@ -377,3 +377,31 @@ def test_repeated_verify_commit_reproduces_greedy(tiny16):
         out += [int(toks[i]) for i in r["accepted"][1:]] + [r["bonus"]]
         cur = r["bonus"]
     assert out[:12] == ref
+
+
+def test_streamed_weights_equal_dense():
+    """OracleModel with a streamed column provider (the 70B / 8B full-size parity
+    tests) computes the same verify as the dense weights: only the evaluation
+    order of independent output columns differs."""
+    from synth import fast
+    cfg = synth.CONFIGS["tiny"]
+    canon = synth.gen_model(cfg, 0)
+    dense = O.OracleModel(cfg, canon)
+    names = dict(wq=synth.KIND["WQ"], wk=synth.KIND["WK"], wv=synth.KIND["WV"], wo=synth.KIND["WO"],
+                 wgate=synth.KIND["WGATE"], wup=synth.KIND["WUP"], wdown=synth.KIND["WDOWN"])
+
+    def cols(layer, name, n0, n1):
+        K = cfg.intermediate if name == "wdown" else (cfg.n_heads * cfg.head_dim if name == "wo" else cfg.hidden)
+        return fast.gen_linear_cols(0, layer, names[name], K, dense.out_features(name), n0, n1)
+
+    streamed = O.OracleModel(cfg, canon, cols=cols)
+    kv = O.KVCache(cfg, 128)
+    for l in range(cfg.n_layers):
+        k, v = synth.gen_prefix_kv(1, l, 32, cfg.n_kv_heads, cfg.head_dim)
+        kv.set_prefix(l, k, v)
+    kv.L = 32
+    toks, par = synth.tree_paperlike(8, cfg.vocab, np.random.default_rng(0))
+    a = O.verify(cfg, dense, kv, toks, par)
+    b = O.verify(cfg, streamed, kv, toks, par)
+    np.testing.assert_allclose(b["logits"], a["logits"], rtol=1e-12, atol=1e-12)
+    assert list(a["argmax"]) == list(b["argmax"])

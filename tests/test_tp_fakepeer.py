@@ -82,6 +82,8 @@ def test_fakepeer_tp_parity(P):
             assert a == b or abs(ro["logits"][i][a] - ro["logits"][i][b]) < 2e-2
         acc, bonus = O.accept_walk(tokens, parents, res0["argmax"])
         assert res0["accepted"] == acc and res0["bonus"] == bonus
+        for sh in shards:  # discard the pending (uncommitted) verify before the next tree
+            sh.set_committed_len(L)
         # each rank holds its own kv heads of the tree rows
         hk = cfg.n_kv_heads // P
         for r, sh in enumerate(shards):

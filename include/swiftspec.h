@@ -267,8 +267,9 @@ ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d
  *          (token_i, parent_i);
  *   outbox (owned by the draft side):   line 1+k = (accepted[k], token),
  *          then line 0 = (n_accepted | (-status & 0xFF) << 16 | stop << 31,
- *          bonus_token); a failed step posts n_accepted = 0 and its status,
- *          and a timed-out inbox message is polled again by the next step.
+ *          bonus_token); a failed step posts n_accepted = 0 and its status;
+ *          an inbox message that timed out (2 s of device time) gets no post
+ *          and is polled again by the next step.
  * Sequence numbers are consecutive per shard, starting at 1. */
 
 /* Device pointer of this shard's inbox ((1 + SS_MAX_TREE) lines x 16 B, a
@@ -292,6 +293,34 @@ ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream)
 ss_status ss_mailbox_post_tree(void* inbox_dev, const int32_t* tokens, const int32_t* parents, int32_t T,
                                uint32_t seq, void* stream);
 ss_status ss_mailbox_recv_result(const void* outbox_dev, uint32_t seq, int32_t* dev_out, void* stream);
+
+/* ---- inspection and test hooks (parity tests; not on the step's path) ---- */
+
+/* Tree metadata of the last step as the device computed it (a0; P:321 square
+ * ancestor mask, R8 positions): T, pos[64] = L + depth, anc[64] = ancestor-or-
+ * self bitmask (bit j = node j), and optionally tokens[64] / parents[64] as
+ * ingested.  Synchronises the device. */
+ss_status ss_read_tree_meta(ss_shard* s, int32_t* T, int32_t* pos, uint64_t* anc, int32_t* tokens,
+                            int32_t* parents);
+
+/* Raw bytes of a device region in kernel layout: which = 0 QKV, 1 O, 2 gate/up,
+ * 3 down (packed W4 units of `layer`), 4 LM head (bf16 units), 5 embedding,
+ * 6 / 7 attention / MLP norm gain of `layer`, 8 final norm.  *total receives
+ * the size; host may be NULL (size query), else bytes must equal *total.
+ * Used to check the device generator against the host repack byte for byte. */
+ss_status ss_read_packed(ss_shard* s, int32_t layer, int32_t which, void* host, size_t bytes, size_t* total);
+
+/* One W4A16 GEMM of linear `which` (0 QKV, 1 O, 2 gate/up, 3 down) of `layer`
+ * on caller activations: d_x device float [T][K_local] (rounded to fp16 like
+ * the step's activations), d_y device float [T][N_pad] = the shard's output
+ * rows in packed row order (QKV: local q | k | v heads; gate/up: per 128-row
+ * tile-group 64 gate then 64 up columns; N_pad = N_local rounded up to 128).
+ * allreduce != 0 (O / down): d_y = the fused tensor-parallel all-reduce of
+ * every rank's partial (collective: all ranks call it; same T).  The same
+ * kernel as the step (integer-valued inputs give bit-exact sums: SURVEY 8(c)).
+ * Asynchronous on `stream`. */
+ss_status ss_debug_gemm(ss_shard* s, int32_t layer, int32_t which, const float* d_x, int32_t T, float* d_y,
+                        int32_t allreduce, void* stream);
 
 #ifdef __cplusplus
 }

@@ -399,13 +399,13 @@ __device__ void accept_walk_dev(DevState* st) {
   // a13: post the verified path to the draft group's outbox (Alg. 1
   // "Send the verified tokens"; P:293 STOP at the end of generation): lines
   // 1..n = (node index, token), then line 0 = (n | -status << 16 | stop << 31,
-  // bonus).  A failed step posts n = 0 and its status; a timed-out inbox
-  // message is polled again by the next step (the sequence number does not
-  // advance).
+  // bonus).  A failed step posts n = 0 and its status; an inbox message that
+  // timed out gets no post and is polled again by the next step (the sequence
+  // number does not advance).
   if (st->mbox_mode) {
     const uint32_t seq = st->mbox_cur;
     const bool ok = res.status == SS_OK;
-    if (st->mbox_post && st->mbox_out) {
+    if (st->mbox_post && st->mbox_out && !st->mbox_tmo) {
       const int np = ok ? n : 0;
       for (int k = 0; k < np; ++k)
         ll_store(st->mbox_out + 1 + k, (uint32_t)res.accepted[k], (uint32_t)st->tokens[res.accepted[k]], seq);
@@ -413,7 +413,7 @@ __device__ void accept_walk_dev(DevState* st) {
       ll_store(st->mbox_out, (uint32_t)np | ((uint32_t)(-res.status) & 0xFFu) << 16 | (stop << 31),
                ok ? (uint32_t)res.bonus_token : 0u, seq);
     }
-    if (res.status != SS_ETIMEOUT) st->mbox_seq = seq;
+    if (!st->mbox_tmo) st->mbox_seq = seq;
   }
 }
 

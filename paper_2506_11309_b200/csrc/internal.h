@@ -43,7 +43,7 @@ struct DevState {
   int32_t max_written;       // highest KV row ever written + 1 (prefix, tree rows)
   uint4* mbox_out;           // draft group's outbox (peer-mapped), nullptr = none
   int32_t debug;             // SS_DEBUG_* flags (ss_set_debug)
-  int32_t pad2;
+  int32_t mbox_tmo;          // the current step's inbox message never (fully) arrived
 };
 
 // One packed linear (W4 format, see common.cuh) or bf16 matrix.

@@ -136,6 +136,9 @@ void launch_mailbox_post(void* inbox, const int32_t* tokens, const int32_t* pare
 void launch_mailbox_recv(const void* outbox, uint32_t seq, int32_t* dev_out, cudaStream_t st);
 // RMSNorm of the residual into frag activations (a2 / a7 / final)
 void launch_prep_norm(ss_shard* s, const uint16_t* gain, int NT, int split, cudaStream_t st);
+// ss_debug_gemm: caller fp32 activations -> W4 GEMM input layout
+void launch_debug_act(ss_shard* s, const float* x, int T, int K, uint8_t* act, int NT, int bump_epoch,
+                      cudaStream_t st);
 // KV compaction + commit (a12); chain from the device result or commit list
 void launch_commit(ss_shard* s, int from_result, cudaStream_t st);
 // device synthetic generator (same counter-based hash as synth/generators.py)

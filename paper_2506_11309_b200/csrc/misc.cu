@@ -29,10 +29,20 @@ SS_DEV float block_sum_256(float v, float* s_red) {
   return r;
 }
 
-// a13 inbox poll: spin on one LL line until its flag equals seq (bounded).
+// a13 inbox poll: spin on one LL line until its flag equals seq, for at most
+// kMailboxPollNs of device time (%globaltimer), then report a timeout.
+constexpr unsigned long long kMailboxPollNs = 2000000000ull;  // 2 s
+SS_DEV unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 SS_DEV bool ll_wait(const uint4* line, uint32_t seq, uint32_t& d1, uint32_t& d2) {
-  for (long spins = 0; spins < (1L << 26); ++spins)
-    if (ll_try_load(line, seq, d1, d2)) return true;
+  if (ll_try_load(line, seq, d1, d2)) return true;
+  const unsigned long long t0 = global_ns();
+  while (global_ns() - t0 < kMailboxPollNs)
+    for (int i = 0; i < 64; ++i)
+      if (ll_try_load(line, seq, d1, d2)) return true;
   return false;
 }
 
@@ -92,7 +102,10 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
   const int T = min(max(T_in, 1), cap);
   if (tid == 0) s_bad = (T_in < 1 || T_in > cap) ? 1 : 0;
   __syncthreads();
-  if (s_tmo && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) st->timeout = 1;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    st->mbox_tmo = s_tmo;
+    if (s_tmo) st->timeout = 1;
+  }
   if (tid < T) {
     int p = mbox_in ? (int)mpar : parents[tid], tk = mbox_in ? (int)mtok : tokens[tid];
     bool bad = (tid == 0) ? (p != -1) : (p < 0 || p >= tid);
@@ -617,6 +630,41 @@ void launch_synth_kv_key(uint16_t* cache, int layer, int Hkv_full, int Hkv_l, in
 }  // namespace ss
 
 namespace ss {
+// ---------------------------------------------------------------- test hook
+// ss_debug_gemm: caller activations x[T][K] (fp32, rounded to fp16 like the
+// step's own activations) -> the W4 GEMM input layout (fp16 fragments + the
+// per-(group, token) sums X); token slots [T, 8 NT) are zeroed.  Thread-block
+// t handles token t; block 0 also publishes T and (all-reduce mode) advances
+// the LL flag epoch exactly like the step's ingest kernel.
+__global__ void debug_act_kernel(DevState* st, const float* x, int T, int K, uint8_t* act, int NT, int bump_epoch,
+                                 int epoch_stride) {
+  const int t = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (t == 0 && threadIdx.x == 0) {
+    st->T = T;
+    if (bump_epoch) {
+      uint32_t e = st->epoch + (uint32_t)epoch_stride;
+      if (e < st->epoch || e + (uint32_t)epoch_stride < e) e = 1;
+      st->epoch = e;
+    }
+  }
+  // one warp per 128-column group: 4 columns per lane
+  for (int g = warp; g < K / 128; g += blockDim.x / 32) {
+    const int k = g * 128 + lane * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < T) v = *reinterpret_cast<const float4*>(x + (size_t)t * K + k);
+    const uint32_t p01 = pack_half2(v.x, v.y), p23 = pack_half2(v.z, v.w);
+    *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k, NT)) = p01;
+    *reinterpret_cast<uint32_t*>(act + act_frag_offset(t, k + 2, NT)) = p23;
+    const float xs = warp_sum(half2_sum(p01) + half2_sum(p23));
+    if (lane == 0) *reinterpret_cast<float*>(act + act_xsum_offset(t, g, NT)) = xs;
+  }
+}
+void launch_debug_act(ss_shard* s, const float* x, int T, int K, uint8_t* act, int NT, int bump_epoch,
+                      cudaStream_t st) {
+  debug_act_kernel<<<8 * NT, 256, 0, st>>>(s->dstate, x, T, K, act, NT, bump_epoch, 2 * s->cfg.n_layers + 2);
+}
+
 // Lazy module loading (the CUDA 12 default) loads a kernel at its first
 // launch, which can wait for running kernels: a producer whose kernel is
 // loaded only after a consumer already spins on its flags would deadlock.
@@ -628,5 +676,6 @@ void warm_misc_kernels() {
   cudaFuncGetAttributes(&a, commit_kernel);
   cudaFuncGetAttributes(&a, mailbox_post_kernel);
   cudaFuncGetAttributes(&a, mailbox_recv_kernel);
+  cudaFuncGetAttributes(&a, debug_act_kernel);
 }
 }  // namespace ss

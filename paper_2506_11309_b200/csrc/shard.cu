@@ -1225,3 +1225,89 @@ extern "C" ss_status ss_mailbox_recv_result(const void* outbox_dev, uint32_t seq
   CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
+
+// ------------------------------------------------------------ test / inspection hooks
+extern "C" ss_status ss_read_tree_meta(ss_shard* s, int32_t* T, int32_t* pos, uint64_t* anc, int32_t* tokens,
+                                       int32_t* parents) {
+  SCOPE(s);
+  if (!s || !T || !pos || !anc) FAIL(SS_EINVAL, "null argument");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(s->hstate, s->dstate, sizeof(DevState), cudaMemcpyDeviceToHost));
+  *T = s->hstate->T;
+  std::memcpy(pos, s->hstate->pos, sizeof(s->hstate->pos));
+  std::memcpy(anc, s->hstate->anc, sizeof(s->hstate->anc));
+  if (tokens) std::memcpy(tokens, s->hstate->tokens, sizeof(s->hstate->tokens));
+  if (parents) std::memcpy(parents, s->hstate->parents, sizeof(s->hstate->parents));
+  return SS_OK;
+}
+
+static ss_status packed_region(ss_shard* s, int32_t layer, int32_t which, const void** ptr, size_t* bytes) {
+  const ss_model_cfg& c = s->cfg;
+  if (which <= 3 || which == 6 || which == 7) {
+    if (layer < 0 || layer >= c.n_layers) FAIL(SS_EINVAL, "layer out of range");
+    LayerW& lw = s->layers[layer];
+    if (which <= 3) {
+      const PackedLinear& pl = which == 0 ? lw.qkv : which == 1 ? lw.o : which == 2 ? lw.gu : lw.down;
+      *ptr = pl.d;
+      *bytes = pl.bytes;
+    } else {
+      *ptr = which == 6 ? lw.attn_norm : lw.mlp_norm;
+      *bytes = (size_t)c.hidden * 2;
+    }
+    return SS_OK;
+  }
+  switch (which) {
+    case 4: *ptr = s->lm_head.d; *bytes = s->lm_head.bytes; return SS_OK;
+    case 5: *ptr = s->embed; *bytes = (size_t)c.vocab * c.hidden * 2; return SS_OK;
+    case 8: *ptr = s->final_norm; *bytes = (size_t)c.hidden * 2; return SS_OK;
+    default: FAIL(SS_EINVAL, "unknown packed region");
+  }
+}
+
+extern "C" ss_status ss_read_packed(ss_shard* s, int32_t layer, int32_t which, void* host, size_t bytes,
+                                    size_t* total) {
+  SCOPE(s);
+  if (!s || !total) FAIL(SS_EINVAL, "null argument");
+  const void* p = nullptr;
+  size_t n = 0;
+  ss_status r = packed_region(s, layer, which, &p, &n);
+  if (r != SS_OK) return r;
+  *total = n;
+  if (!host) return SS_OK;
+  if (bytes != n) FAIL(SS_EINVAL, "bytes must equal the region size (*total)");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(host, p, n, cudaMemcpyDeviceToHost));
+  return SS_OK;
+}
+
+extern "C" ss_status ss_debug_gemm(ss_shard* s, int32_t layer, int32_t which, const float* d_x, int32_t T, float* d_y,
+                                   int32_t allreduce, void* stream) {
+  SCOPE(s);
+  if (!s || !d_x || !d_y) FAIL(SS_EINVAL, "null argument");
+  if (layer < 0 || layer >= s->cfg.n_layers || which < 0 || which > 3) FAIL(SS_EINVAL, "layer / linear out of range");
+  if (T < 1 || T > SS_MAX_TREE) FAIL(SS_EINVAL, "T out of [1, 64]");
+  if (allreduce && (which == 0 || which == 2)) FAIL(SS_EINVAL, "all-reduce applies to the O / down projections");
+  if (allreduce && s->P > 1 && !s->peers_ready) FAIL(SS_ESTATE, "peers not imported (tp_size > 1)");
+  if (!weights_complete(s)) FAIL(SS_ESTATE, "weights not fully loaded");
+  cudaSetDevice(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  LayerW& lw = s->layers[layer];
+  PackedLinear& pl = which == 0 ? lw.qkv : which == 1 ? lw.o : which == 2 ? lw.gu : lw.down;
+  GemmScratch& sc = which == 0 ? s->sc_qkv : which == 1 ? s->sc_o : which == 2 ? s->sc_gu : s->sc_down;
+  uint8_t* act = which == 1 ? s->act_o : which == 3 ? s->act_d : s->act_h;
+  const int NT = nt_of(T);
+  CUDA_TRY(cudaMemsetAsync(d_y, 0, (size_t)T * pl.N * 4, st));
+  launch_debug_act(s, d_x, T, pl.K, act, NT, allreduce ? 1 : 0, st);
+  GemmArgs g = gemm_args(s, pl, act, sc, EPI_RESID, layer);
+  g.epi.x = d_y;           // x += y with x = 0: the raw GEMM rows (or the all-reduced sum)
+  g.epi.h = pl.N;
+  g.epi.P = allreduce ? s->P : 1;
+  g.epi.ar_seq = 0;
+  ss_pdl_off = s->P > 1 && s->launch_cap > 0 && !s->loopback;
+  launch_gemm(g, 0, NT, s->launch_cap, st);
+  ss_pdl_off = false;
+  CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}

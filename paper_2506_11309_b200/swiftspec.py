@@ -49,7 +49,7 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
-           "ss_set_debug"]
+           "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm"]
 SS_DEBUG_CONSISTENCY = 1
 
 
@@ -73,6 +73,9 @@ def lib():
         "ss_destroy": (i32, [vp]),
         "ss_last_error": (C.c_char_p, [vp]),
         "ss_set_debug": (i32, [vp, i32]),
+        "ss_read_tree_meta": (i32, [vp, vp, vp, vp, vp, vp]),
+        "ss_read_packed": (i32, [vp, i32, i32, vp, sz, C.POINTER(sz)]),
+        "ss_debug_gemm": (i32, [vp, i32, i32, vp, i32, vp, i32, vp]),
         "ss_load_weights": (i32, [vp, i32, i32, i32, vp, sz]),
         "ss_synth_weights": (i32, [vp, u64]),
         "ss_set_prefix_kv": (i32, [vp, i32, vp, vp, i32]),
@@ -255,6 +258,30 @@ class Shard:
 
     def verify_mailbox(self, auto_commit: bool = True, stream=None):
         self._ck(lib().ss_verify_tree_mailbox(self.h, 1 if auto_commit else 0, _stream_handle(stream)))
+
+    # ---- inspection / test hooks
+    def read_tree_meta(self):
+        """(T, pos[T], anc[T] as uint64 bitmasks, tokens[T], parents[T]) of the last step."""
+        T = C.c_int32(0)
+        pos = np.zeros(SS_MAX_TREE, dtype=np.int32)
+        anc = np.zeros(SS_MAX_TREE, dtype=np.uint64)
+        tok = np.zeros(SS_MAX_TREE, dtype=np.int32)
+        par = np.zeros(SS_MAX_TREE, dtype=np.int32)
+        self._ck(lib().ss_read_tree_meta(self.h, C.byref(T), _ptr(pos), _ptr(anc), _ptr(tok), _ptr(par)))
+        n = T.value
+        return n, pos[:n], anc[:n], tok[:n], par[:n]
+
+    def read_packed(self, layer: int, which: int) -> np.ndarray:
+        total = C.c_size_t(0)
+        self._ck(lib().ss_read_packed(self.h, layer, which, None, 0, C.byref(total)))
+        buf = np.zeros(total.value, dtype=np.uint8)
+        self._ck(lib().ss_read_packed(self.h, layer, which, _ptr(buf), total.value, C.byref(total)))
+        return buf
+
+    def debug_gemm(self, layer: int, which: int, d_x, T: int, d_y, allreduce: bool = False, stream=None):
+        """One W4 GEMM of the step's kernel on caller activations (torch CUDA tensors)."""
+        self._ck(lib().ss_debug_gemm(self.h, layer, which, d_x.data_ptr(), T, d_y.data_ptr(),
+                                     1 if allreduce else 0, _stream_handle(stream)))
 
     # ---- tensor parallel peers
     def export_handle(self) -> bytes:

@@ -135,6 +135,29 @@ def exchange_handles(blob: bytes, world: int):
     return out
 
 
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: relaunch this
+    script under torch.distributed.run with N local ranks (127.0.0.1
+    rendezvous), pass rank 0's JSON line through, return the worst exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def gather_objects(obj, world: int):
+    import torch.distributed as dist
+    if world == 1:
+        return [obj]
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
 def max_over_ranks(x: float, world: int, device=None) -> float:
     import torch
     import torch.distributed as dist
@@ -234,7 +257,7 @@ def run_ours(args, cfg):
 
     rank, world, local = dist_env()
     if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (run without torchrun to self-spawn)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -262,21 +285,31 @@ def run_ours(args, cfg):
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    # every rank must have walked the same path from the same argmax (TP:
+    # replicated accept + commit); all statuses SS_OK
+    wres = [ssp.parse_result(r, T) for r in d_res[:args.warmup].cpu().numpy()]
+    allw = gather_objects([(r["status"], r["accepted"], r["bonus"], r["argmax"]) for r in wres], world)
+    ranks_agree = all(a == allw[0] for a in allw)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for i in range(args.warmup, n_steps):
+        ev[0].record(stream)
+        for j, i in enumerate(range(args.warmup, n_steps)):
             step(i)
-        e1.record(stream)
+            ev[j + 1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    per_step = [ev[j].elapsed_time(ev[j + 1]) for j in range(args.steps)]
+    ms = ev[0].elapsed_time(ev[-1]) / args.steps
     ms = max_over_ranks(ms, world, dev)
+    p50 = max_over_ranks(float(np.percentile(per_step, 50)), world, dev)
+    p90 = max_over_ranks(float(np.percentile(per_step, 90)), world, dev)
     res = [ssp.parse_result(r, T) for r in d_res[args.warmup:].cpu().numpy()]
+    allt = gather_objects([(r["status"], r["accepted"], r["bonus"]) for r in res], world)
+    ranks_agree = ranks_agree and all(a == allt[0] for a in allt)
     emitted = float(np.mean([r["n_accepted"] for r in res]))  # (n-1) accepted + 1 bonus
     statuses = set(r["status"] for r in res)
     kps = sh.kernels_per_step(T, auto_commit=True)
@@ -327,8 +360,30 @@ def run_ours(args, cfg):
         "step_roofline_frac": bytes_step / (ms / 1e3) / 1e9 / peak,
         "step_bytes": bytes_step,
         "status_ok": statuses == {0},
+        "p50_us": p50 * 1e3, "p90_us": p90 * 1e3,
+        "ranks_agree": bool(ranks_agree),
     }
-    if isinstance(prof, dict) and "gate_up_swiglu" in prof:
+    if isinstance(prof, dict) and prof.get("step_kernel", (0, 0))[1] > 0:
+        # persistent step kernel: the whole step's weights + KV stream through it
+        sk_ms, sk_n = prof["step_kernel"]
+        tot = sum(v[0] for v in prof.values())
+        per = sk_ms / sk_n
+        ach = bytes_step / (per / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(f"{cfg.name}/tp{world}/T{T}/step_kernel")
+            except Exception:
+                traffic = None
+        line["roofline"] = {"kernel": "step_kernel (persistent: every layer's GEMMs, attention, all-reduces, "
+                                      "LM head, accept walk)", "bound": "hbm",
+                            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                            "traffic": traffic, "peak_source": peak_src,
+                            "algorithmic_bytes_per_launch": bytes_step,
+                            "avg_launch_us": per * 1e3, "share_of_step": sk_ms / tot if tot else None}
+        line["kernel_times_us"] = {k: {"total": v[0] * 1e3, "launches": v[1]} for k, v in prof.items() if v[1]}
+    elif isinstance(prof, dict) and "gate_up_swiglu" in prof:
         gu_ms, gu_n = prof["gate_up_swiglu"]
         tot = sum(v[0] for v in prof.values())
         per = gu_ms / max(gu_n, 1)
@@ -487,6 +542,8 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = synth.CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

@@ -246,13 +246,26 @@ ss_status ss_commit_accepted(ss_shard* s, void* stream);
 /* Number of kernels the verify (+ commit) launch sequence contains. */
 int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_commit);
 
+/* Kernel organisation of the step.  on != 0 (the default): trees of T <= 32
+ * run as ONE persistent kernel per step (every layer's GEMMs, attention,
+ * all-reduces, the LM head and the accept walk; phases hand over through
+ * device counters, weights stream ahead of their inputs).  on == 0: one
+ * kernel per phase (QKV, attention, O, gate/up, down per layer, LM head) --
+ * the path T > 32 always takes; kept selectable for A/B parity tests.
+ * Results agree to the logit tolerance; both are bit-exact where the method
+ * requires it.  ss_step_kernel_active returns 1 if a verify of T nodes uses
+ * the persistent kernel, 0 if not, -1 on bad arguments. */
+ss_status ss_set_step_kernel(ss_shard* s, int32_t on);
+int32_t ss_step_kernel_active(ss_shard* s, int32_t T);
+
 /* Measurement helper (bench.py's roofline): run one all-device step like
  * ss_verify_tree_dev(auto_commit=1) but launched eagerly with a CUDA event
  * pair around every kernel on `stream`; synchronises and writes the summed
  * device time (ms) and launch count per kernel kind to ms[SS_PROF_KINDS],
  * count[SS_PROF_KINDS].  Kinds: 0 embed+tree, 1 QKV, 2 attention, 3 O-proj,
- * 4 RMSNorm, 5 gate/up+SwiGLU, 6 down, 7 LM head+argmax+accept, 8 commit. */
-#define SS_PROF_KINDS 9
+ * 4 RMSNorm, 5 gate/up+SwiGLU, 6 down, 7 LM head+argmax+accept, 8 commit,
+ * 9 the persistent step kernel (all of 1-7 in one launch, T <= 32). */
+#define SS_PROF_KINDS 10
 ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
                           float* ms, int32_t* count, void* stream);
 

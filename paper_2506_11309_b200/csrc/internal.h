@@ -13,6 +13,8 @@
 namespace ss {
 
 constexpr int kMaxPeers = 8;
+constexpr int kCtrPerLayerH = 48;  // == kCtrPerLayer (step.h)
+constexpr int kCtrGlobalH = 8;     // == kCtrGlobal
 
 // Device-resident per-step state (read by every kernel through a pointer so
 // that captured CUDA graphs replay with new trees).
@@ -138,6 +140,19 @@ struct ss_shard {
 
   // a13 mailbox: this shard's inbox (written by the draft group)
   uint4* mbox_in = nullptr;
+
+  // persistent step kernel (step.cu) state
+  int* step_ctr = nullptr;         // phase counters [n_layers][kCtrPerLayerH] + [kCtrGlobalH]
+  float* step_ss = nullptr;        // [n_layers + 1][2][64]
+  uint16_t* qf = nullptr;          // q fragments hi | lo
+  uint16_t* klo = nullptr;         // tree K / V lo window [Hkv_l][128][d]
+  uint16_t* vlo = nullptr;
+  float* att_ws = nullptr;         // [max step CTAs][2][64][d]
+  float2* att_ml = nullptr;
+  void* layer_tab = nullptr;       // device LayerPtrs[n_layers]
+  void* step_args_dev = nullptr;   // device StepArgs x 2 (without / with the logits output)
+  int step_max_ctas = 0;
+  bool use_step = true;            // NT <= 4: persistent step kernel; else per-phase kernels
 
   // graphs: key = NT*4 + auto_commit*2 + logits
   std::map<int, ss::Graph> graphs;

@@ -121,6 +121,11 @@ struct AttnArgs {
 };
 
 int launch_gemm(const GemmArgs& g, int wfmt, int NT, int max_ctas, cudaStream_t st);
+// persistent step kernel (step.cu, NT <= 4)
+struct StepArgs;
+int launch_step(const StepArgs& a, const StepArgs* dev_args, int NT, int max_ctas, cudaStream_t st);
+int step_ctas(int NT, int d, int max_ctas);
+void warm_step_kernels();
 // force-load every kernel (lazy module loading vs cross-kernel flag waits)
 void warm_gemm_kernels();
 void warm_attention_kernels();
@@ -129,7 +134,7 @@ int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st);
 
 // embed + tree metadata (a0, a1) + first RMSNorm into the frag activation
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
-                       cudaStream_t st, bool from_mailbox = false);
+                       cudaStream_t st, bool from_mailbox = false, bool step_mode = false);
 // a13 mailbox helpers for the draft side (and tests)
 void launch_mailbox_post(void* inbox, const int32_t* tokens, const int32_t* parents, int T, uint32_t seq,
                          cudaStream_t st);

@@ -50,6 +50,42 @@ SS_DEV bool ll_wait(const uint4* line, uint32_t seq, uint32_t& d1, uint32_t& d2)
 // "a debug mode checksums the arguments across ranks"): every rank posts a
 // checksum of (T, tokens, parents) to every peer's receive buffer as an LL
 // line flagged with this step's epoch, then compares all P lines.
+// Step-kernel mode of the ingest kernel (step.cu): the first layer's QKV input
+// is x * g in fp16 hi + lo with group sums X (the RMSNorm scale is deferred to
+// the QKV epilogue, which reads the token's sum of squares ss[0][t]); every
+// per-step counter and sum is zeroed and the padded token slots [T, 8 NT) of
+// every activation buffer are cleared.
+struct StepIngest {
+  int on = 0;
+  int* ctr = nullptr;
+  int n_ctr = 0;
+  float* ss = nullptr;      // [n_layers + 1][2][64]
+  int n_ss = 0;
+  uint8_t* act_o = nullptr;
+  uint8_t* act_d = nullptr;
+  uint8_t* act_lm = nullptr;
+  int K_o = 0, K_d = 0;
+};
+SS_DEV uint32_t a2_off(int tt, int k, int NT, int lo) {
+  return (uint32_t)(k >> 8) * ((uint32_t)NT * 8192u + (uint32_t)NT * 64u) + (lo ? (uint32_t)NT * 4096u : 0u) +
+         frag_offset(tt, k & 255, NT);
+}
+SS_DEV uint32_t a2_x(int tt, int g, int NT) {
+  return (uint32_t)(g >> 1) * ((uint32_t)NT * 8192u + (uint32_t)NT * 64u) + (uint32_t)NT * 8192u +
+         (uint32_t)(((g & 1) * 8 * NT + tt) * 4);
+}
+// zero token slot t of an a2-layout buffer with K columns (columns split over kNormSplit CTAs)
+SS_DEV void zero_a2_slot(uint8_t* act, int t, int K, int NT, int part) {
+  for (int f = threadIdx.x; f < K / 4; f += 256)
+    if ((f % 4) == part)
+      for (int lo = 0; lo < 2; ++lo) {
+        *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f, NT, lo)) = 0u;
+        *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f + 2, NT, lo)) = 0u;
+      }
+  for (int g = threadIdx.x; g < K / 128; g += 256)
+    if ((g % 4) == part) *reinterpret_cast<float*>(act + a2_x(t, g, NT)) = 0.f;
+}
+
 struct ConsistencyArgs {
   uint4* recv = nullptr;                  // own receive buffer (consistency area)
   uint4* peer_recv[kMaxPeers] = {nullptr};  // every rank's consistency area
@@ -60,7 +96,8 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
                                                          const int32_t* parents, int T_in, const uint16_t* E,
                                                          int V, int h, float* x, const uint16_t* gain,
                                                          uint8_t* act, int NT, float eps, int epoch_stride,
-                                                         const uint4* mbox_in, int max_tree, ConsistencyArgs ca) {
+                                                         const uint4* mbox_in, int max_tree, ConsistencyArgs ca,
+                                                         StepIngest si) {
   __shared__ int s_tok[SS_MAX_TREE], s_par[SS_MAX_TREE];
   __shared__ int s_bad;
   __shared__ int s_T;
@@ -165,6 +202,25 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     }
   }
   const int nv = h / 4;  // 4-element vectors per row
+  if (si.on) {
+    // per-step counters and sums of squares (ss[0][t < T] is written below)
+    const int nb = gridDim.x * gridDim.y, bi = blockIdx.y * gridDim.x + blockIdx.x;
+    for (int i = bi * 256 + tid; i < si.n_ctr; i += nb * 256) si.ctr[i] = 0;
+    for (int i = bi * 256 + tid; i < si.n_ss; i += nb * 256)
+      if (i >= 64 || i >= T) si.ss[i] = 0.f;
+  }
+  if (t >= T && si.on) {  // padded token slot of every step-kernel input
+    zero_a2_slot(act, t, h, NT, part);
+    zero_a2_slot(si.act_o, t, si.K_o, NT, part);
+    zero_a2_slot(si.act_d, t, si.K_d, NT, part);
+    for (int f = tid; f < nv; f += 256)
+      if ((f % kNormSplit) == part)
+        for (int hl = 0; hl < 2; ++hl) {
+          *reinterpret_cast<uint32_t*>(si.act_lm + frag_offset(t + hl * 8 * NT, 4 * f, 2 * NT)) = 0u;
+          *reinterpret_cast<uint32_t*>(si.act_lm + frag_offset(t + hl * 8 * NT, 4 * f + 2, 2 * NT)) = 0u;
+        }
+    return;
+  }
   if (t >= T) {          // padded token slot: zero its activation column and group sums
     for (int f = tid; f < nv; f += 256)
       if ((f % kNormSplit) == part) {
@@ -188,6 +244,38 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     }
   }
   ss = block_sum_256(ss, s_red);
+  if (si.on) {
+    // x * g (fp16 hi + lo, X of hi + lo); the QKV epilogue applies rsqrt(ss / h + eps)
+    if (part == 0 && tid == 0) si.ss[t] = ss;
+    float4* xs4 = reinterpret_cast<float4*>(x + (size_t)t * h);
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int f = tid + 256 * i;
+      if (256 * i >= nv) continue;  // warp-uniform
+      float xs = 0.f;
+      if (f < nv) {
+        const uint2 gw = reinterpret_cast<const uint2*>(gain)[f];
+        const float y0 = v[i].x * bf16_lo(gw.x), y1 = v[i].y * bf16_hi(gw.x);
+        const float y2 = v[i].z * bf16_lo(gw.y), y3 = v[i].w * bf16_hi(gw.y);
+        const uint32_t h01 = pack_half2(y0, y1), h23 = pack_half2(y2, y3);
+        const __half2 a01 = *reinterpret_cast<const __half2*>(&h01), a23 = *reinterpret_cast<const __half2*>(&h23);
+        const uint32_t l01 = pack_half2(y0 - __low2float(a01), y1 - __high2float(a01));
+        const uint32_t l23 = pack_half2(y2 - __low2float(a23), y3 - __high2float(a23));
+        xs = (half2_sum(h01) + half2_sum(l01)) + (half2_sum(h23) + half2_sum(l23));
+        if ((f % kNormSplit) == part) {
+          xs4[f] = v[i];
+          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f, NT, 0)) = h01;
+          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f + 2, NT, 0)) = h23;
+          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f, NT, 1)) = l01;
+          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f + 2, NT, 1)) = l23;
+        }
+      }
+      xs = warp_sum(xs);  // the warp's 32 vectors are exactly one 128-group
+      const int g = f >> 5;
+      if ((tid & 31) == 0 && f < nv && (g % kNormSplit) == part) *reinterpret_cast<float*>(act + a2_x(t, g, NT)) = xs;
+    }
+    return;
+  }
   const float r = rsqrtf(ss / (float)h + eps);
   float4* xr = reinterpret_cast<float4*>(x + (size_t)t * h);
 #pragma unroll
@@ -215,7 +303,7 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
 }
 
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
-                       cudaStream_t st, bool from_mailbox) {
+                       cudaStream_t st, bool from_mailbox, bool step_mode) {
   const uint16_t* g0 = s->layers[0].attn_norm;
   ConsistencyArgs ca;
   ca.rank = s->rank;
@@ -228,10 +316,23 @@ void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parent
     for (int p = 0; p < s->P; ++p)
       ca.peer_recv[p] = s->peer_recv[p] ? reinterpret_cast<uint4*>(s->peer_recv[p]) + ofs : nullptr;
   }
+  StepIngest si;
+  if (step_mode) {
+    si.on = 1;
+    si.ctr = s->step_ctr;
+    si.n_ctr = s->cfg.n_layers * kCtrPerLayerH + kCtrGlobalH;
+    si.ss = s->step_ss;
+    si.n_ss = (s->cfg.n_layers + 1) * 2 * 64;
+    si.act_o = s->act_o;
+    si.act_d = s->act_d;
+    si.act_lm = s->act_lm;
+    si.K_o = s->Hq_l * s->cfg.head_dim;
+    si.K_d = s->I_l;
+  }
   launch_pdl(embed_meta_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, s->dstate, tokens, parents, T,
              (const uint16_t*)s->embed, s->cfg.vocab, s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
              2 * s->cfg.n_layers + 2, from_mailbox ? (const uint4*)s->mbox_in : (const uint4*)nullptr,
-             s->cfg.max_tree, ca);
+             s->cfg.max_tree, ca, si);
 }
 
 // ---------------------------------------------------------------- a13 draft-side helpers

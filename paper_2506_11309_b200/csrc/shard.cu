@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "kernels.h"
+#include "step.h"
 
 using namespace ss;
 
@@ -270,6 +271,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   warm_gemm_kernels();
   warm_attention_kernels();
   warm_misc_kernels();
+  warm_step_kernels();
   ss_shard* s = new ss_shard();
   s->cfg = c;
   s->rank = tp_rank;
@@ -358,6 +360,27 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
     return fail(SS_ECUDA);
   }
   A(s->logits_dev, (size_t)SS_MAX_TREE * s->V_l_pad * 4);
+  // persistent step kernel (step.cu)
+  s->step_max_ctas = s->n_sm * 2;
+  A(s->step_ctr, ((size_t)c.n_layers * kCtrPerLayer + kCtrGlobal) * 4);
+  A(s->step_ss, (size_t)(c.n_layers + 1) * 2 * 64 * 4);
+  A(s->qf, (size_t)2 * s->Hkv_l * G * 64 * d * 2);
+  A(s->klo, (size_t)s->Hkv_l * 128 * d * 2);
+  A(s->vlo, (size_t)s->Hkv_l * 128 * d * 2);
+  A(s->att_ws, (size_t)s->step_max_ctas * 2 * 64 * d * 4);
+  A(s->att_ml, (size_t)s->step_max_ctas * 2 * 64 * sizeof(float2));
+  A(s->layer_tab, (size_t)c.n_layers * sizeof(LayerPtrs));
+  A(s->step_args_dev, 6 * sizeof(StepArgs));  // [NT = 1, 2, 4][logits off / on]
+  {
+    std::vector<LayerPtrs> tab(c.n_layers);
+    for (int l = 0; l < c.n_layers; ++l)
+      tab[l] = LayerPtrs{s->layers[l].qkv.d, s->layers[l].o.d, s->layers[l].gu.d, s->layers[l].down.d,
+                         s->layers[l].attn_norm, s->layers[l].mlp_norm};
+    if (cudaMemcpy(s->layer_tab, tab.data(), tab.size() * sizeof(LayerPtrs), cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_err("layer table copy failed");
+      return fail(SS_ECUDA);
+    }
+  }
   A(s->dstate, sizeof(DevState));
   A(s->d_tree_in, 2 * SS_MAX_TREE * 4);
   if (cudaMallocHost((void**)&s->hstate, sizeof(DevState)) != cudaSuccess ||
@@ -412,7 +435,9 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
                   s->act_o, s->act_d, s->act_lm, s->qbuf, s->attn_ws, s->attn_ml, s->attn_bar, s->logits_dev, s->dstate,
                   s->d_tree_in, s->recv, s->mbox_in, s->sc_qkv.accum, s->sc_qkv.counters, s->sc_o.accum, s->sc_o.counters,
                   s->sc_gu.accum, s->sc_gu.counters, s->sc_down.accum, s->sc_down.counters, s->sc_lm.accum,
-                  s->sc_lm.counters, s->sc_o.ss, s->sc_o.nbar, s->sc_down.ss, s->sc_down.nbar};
+                  s->sc_lm.counters, s->sc_o.ss, s->sc_o.nbar, s->sc_down.ss, s->sc_down.nbar, s->step_ctr,
+                  s->step_ss, s->qf, s->klo, s->vlo, s->att_ws, s->att_ml, s->layer_tab, s->sc_qkv.ss,
+                  s->sc_qkv.nbar, s->sc_gu.ss, s->sc_gu.nbar, s->sc_lm.ss, s->sc_lm.nbar, s->step_args_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->hstate) cudaFreeHost(s->hstate);
@@ -799,10 +824,104 @@ static Prof* g_prof = nullptr;
 #define PROF_END() \
   if (g_prof) g_prof->end()
 
+// Whether the persistent step kernel runs this tree width: T <= 32 (NT <= 4)
+// and every attention (kv head, 64-row chunk) group fits the grid.
+static bool step_path(const ss_shard* s, int NT) {
+  if (!s->use_step || NT > 4) return false;
+  const int groups = s->Hkv_l * ((s->G * 8 * NT + 63) / 64);
+  return groups <= step_ctas(NT, s->cfg.head_dim, s->launch_cap);
+}
+
+static StepArgs step_args(ss_shard* s, int want_logits) {
+  const ss_model_cfg& c = s->cfg;
+  StepArgs a;
+  a.st = s->dstate;
+  a.layers = (const LayerPtrs*)s->layer_tab;
+  a.n_layers = c.n_layers;
+  a.h = c.hidden;
+  a.d = c.head_dim;
+  a.Hq_l = s->Hq_l;
+  a.Hkv_l = s->Hkv_l;
+  a.G = s->G;
+  a.I_l = s->I_l;
+  a.max_ctx_pad = s->max_ctx_pad;
+  const LayerW& l0 = s->layers[0];
+  a.qkv_tg = l0.qkv.n_tg; a.qkv_S = l0.qkv.S;
+  a.o_tg = l0.o.n_tg; a.o_S = l0.o.S;
+  a.gu_tg = l0.gu.n_tg; a.gu_S = l0.gu.S;
+  a.dn_tg = l0.down.n_tg; a.dn_S = l0.down.S;
+  a.lm_tg = s->lm_head.n_tg; a.lm_S = s->lm_head.S;
+  a.lm_w = s->lm_head.d;
+  a.final_norm = s->final_norm;
+  a.eps = c.rms_eps;
+  a.act_h = s->act_h;
+  a.act_o = s->act_o;
+  a.act_d = s->act_d;
+  a.act_lm = s->act_lm;
+  a.qf = s->qf;
+  a.kc = s->kcache;
+  a.vc = s->vcache;
+  a.klo = s->klo;
+  a.vlo = s->vlo;
+  a.rope_cs = s->rope_cs;
+  a.x = s->x;
+  GemmScratch* sc[5] = {&s->sc_qkv, &s->sc_o, &s->sc_gu, &s->sc_down, &s->sc_lm};
+  for (int i = 0; i < 5; ++i) {
+    a.acc[i] = sc[i]->accum;
+    a.arr[i] = sc[i]->counters;
+  }
+  a.ctr = s->step_ctr;
+  a.ss = s->step_ss;
+  a.att_ws = s->att_ws;
+  a.att_ml = s->att_ml;
+  a.rank = s->rank;
+  a.P = s->P;
+  a.loopback = s->loopback ? 1 : 0;
+  a.recv = s->recv;
+  for (int p = 0; p < s->P; ++p) a.peer_recv[p] = s->peer_recv[p];
+  a.V_l = s->V_l;
+  a.V_off = s->V_off;
+  a.logits_ld = s->V_l_pad;
+  a.logits = want_logits ? s->logits_dev : nullptr;
+  return a;
+}
+
+// The step kernel reads its arguments from device memory (one copy per
+// logits mode): written before graph capture / an eager profile launch.
+static int step_args_slot(int NT, int want_logits) { return (NT == 1 ? 0 : NT == 2 ? 1 : 2) * 2 + want_logits; }
+static ss_status write_step_args(ss_shard* s, int NT) {
+  if (!step_path(s, NT)) return SS_OK;
+  StepArgs h[2];
+  for (int w = 0; w < 2; ++w) {
+    h[w] = step_args(s, w);
+    h[w].n_ctas = step_ctas(NT, s->cfg.head_dim, s->launch_cap);
+  }
+  CUDA_TRY(cudaMemcpy(reinterpret_cast<StepArgs*>(s->step_args_dev) + step_args_slot(NT, 0), h, sizeof(h),
+                      cudaMemcpyHostToDevice));
+  return SS_OK;
+}
+
 // Enqueue everything after a0/a1 (the graph body).  Returns the kernel count.
 static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, cudaStream_t st) {
   const ss_model_cfg& c = s->cfg;
   int n = 0;
+  if (step_path(s, NT)) {
+    ss_pdl_off = s->P > 1 && s->launch_cap > 0 && !s->loopback;
+    StepArgs a = step_args(s, want_logits);
+    a.n_ctas = step_ctas(NT, c.head_dim, s->launch_cap);
+    PROF_BEGIN(9);
+    n += launch_step(a, reinterpret_cast<const StepArgs*>(s->step_args_dev) + step_args_slot(NT, want_logits), NT,
+                     s->launch_cap, st);
+    PROF_END();
+    ss_pdl_off = false;
+    if (auto_commit) {
+      PROF_BEGIN(8);
+      launch_commit(s, 1, st);
+      PROF_END();
+      ++n;
+    }
+    return n;
+  }
   // timing experiments only (results are wrong; experiment builds only, the
   // product library always runs every launch): SS_EXP_SKIP = bitmask of
   // launches to leave out, 1 qkv, 2 attention, 4 o, 8 gate/up, 16 down
@@ -897,6 +1016,8 @@ static ss_status get_graph(ss_shard* s, int NT, int auto_commit, int want_logits
     return SS_OK;
   }
   // warm the launch helpers (function attributes, occupancy) outside capture
+  ss_status ra = write_step_args(s, NT);
+  if (ra != SS_OK) return ra;
   Graph gr;
   cudaGraph_t graph;
   CUDA_TRY(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -928,7 +1049,7 @@ static ss_status run_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d
   Graph* gr;
   ss_status r = get_graph(s, NT, auto_commit, want_logits, &gr);
   if (r != SS_OK) return r;
-  launch_embed_meta(s, d_tokens, d_parents, T, NT, st, from_mailbox);
+  launch_embed_meta(s, d_tokens, d_parents, T, NT, st, from_mailbox, step_path(s, NT));
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaGraphLaunch(gr->exec, st));
   return SS_OK;
@@ -1045,6 +1166,23 @@ extern "C" ss_status ss_commit_accepted(ss_shard* s, void* stream) {
   return SS_OK;
 }
 
+extern "C" ss_status ss_set_step_kernel(ss_shard* s, int32_t on) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  s->use_step = on != 0;
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" int32_t ss_step_kernel_active(ss_shard* s, int32_t T) {
+  if (!s || T < 1 || T > SS_MAX_TREE) return -1;
+  return step_path(s, nt_of(T)) ? 1 : 0;
+}
+
 extern "C" ss_status ss_set_debug(ss_shard* s, int32_t flags) {
   SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
@@ -1155,7 +1293,7 @@ extern "C" ss_status ss_profile_step(ss_shard* s, const int32_t* d_tokens, const
   if (r != SS_OK) return r;
   g_prof = &prof;
   prof.begin(0);
-  launch_embed_meta(s, d_tokens, d_parents, T, NT, st);
+  launch_embed_meta(s, d_tokens, d_parents, T, NT, st, false, step_path(s, NT));
   prof.end();
   enqueue_body(s, NT, 1, 0, st);
   g_prof = nullptr;

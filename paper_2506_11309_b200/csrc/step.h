@@ -1,0 +1,68 @@
+// step.h -- arguments and layouts of the persistent step kernel (step.cu),
+// shared with the host (shard.cu).  Internal, not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace ss {
+
+// Per-layer weight pointers (device table, one entry per layer).
+struct LayerPtrs {
+  const uint8_t* qkv;
+  const uint8_t* o;
+  const uint8_t* gu;
+  const uint8_t* down;
+  const uint16_t* attn_norm;
+  const uint16_t* mlp_norm;
+};
+
+// Phase-completion counters, per layer (zeroed by the ingest kernel every step).
+constexpr int kCtrPerLayer = kCtrPerLayerH;
+enum { C_QKV = 0, C_ATT = 1, C_O = 2, C_GU = 3, C_DN = 4, C_MEET = 8 };  // C_MEET + kvh*Z + z (<= 32)
+constexpr int kCtrGlobal = kCtrGlobalH;  // after the per-layer blocks: [0] LM tile-groups finalised
+
+// W4 GEMM input of the step kernel: per 256-deep K stage, fp16 hi fragments
+// (NT*4 KB), fp16 lo fragments (x - hi, NT*4 KB), then the per-(128-group,
+// token) sums X of hi + lo in fp32 (DESIGN R18: hi + lo carries ~22 bits).
+__host__ __device__ constexpr uint32_t a2_stage_bytes(int NT) { return (uint32_t)NT * 8192u + (uint32_t)NT * 64u; }
+
+// Attention: keys per K/V tile (a 16 KB ring unit: K then V, 8 KB each).
+__host__ __device__ constexpr int att_tile_keys(int d) { return 8192 / (2 * d); }
+
+struct StepArgs {
+  DevState* st = nullptr;
+  const LayerPtrs* layers = nullptr;  // device [n_layers]
+  int n_layers = 0, h = 0, d = 128, Hq_l = 0, Hkv_l = 0, G = 1, I_l = 0, max_ctx_pad = 0;
+  int qkv_tg = 0, qkv_S = 0, o_tg = 0, o_S = 0, gu_tg = 0, gu_S = 0, dn_tg = 0, dn_S = 0, lm_tg = 0, lm_S = 0;
+  const uint8_t* lm_w = nullptr;
+  const uint16_t* final_norm = nullptr;
+  float eps = 1e-5f;
+  uint8_t* act_h = nullptr;   // QKV / gate-up input (a2 layout, K = h)
+  uint8_t* act_o = nullptr;   // O input (K = Hq_l * d)
+  uint8_t* act_d = nullptr;   // down input (K = I_l)
+  uint8_t* act_lm = nullptr;  // LM head input (bf16 hi / lo fragments, K = h)
+  uint16_t* qf = nullptr;     // q, mma A-fragment order: [hi|lo][Hkv_l][4G row blocks][d/16][32 lanes][8]
+  uint16_t* kc = nullptr;     // KV cache [layer][Hkv_l][max_ctx_pad][d] fp16, swizzled 64-row blocks
+  uint16_t* vc = nullptr;
+  uint16_t* klo = nullptr;    // tree rows' lo parts, window of 128 rows from (L & ~63): [Hkv_l][128][d]
+  uint16_t* vlo = nullptr;
+  const float2* rope_cs = nullptr;
+  float* x = nullptr;         // residual [64][h] fp32
+  float* acc[5] = {nullptr};  // split-K accumulators: qkv, o, gu, down, lm  [n_tg][128][8 NT]
+  int* arr[5] = {nullptr};    // arrival counters per tile-group (self-cleaning)
+  int* ctr = nullptr;         // [n_layers][kCtrPerLayer] + [kCtrGlobal]
+  float* ss = nullptr;        // [n_layers + 1][2][64] sums of squares (0: attn-norm input, 1: mlp-norm input)
+  float* att_ws = nullptr;    // [n_ctas][2 key halves][64 rows][d] unnormalised partial outputs
+  float2* att_ml = nullptr;   // [n_ctas][2][64] (running max, sum)
+  int rank = 0, P = 1, loopback = 0;
+  float* recv = nullptr;
+  float* peer_recv[kMaxPeers] = {nullptr};
+  int V_l = 0, V_off = 0, logits_ld = 0;
+  float* logits = nullptr;
+  int n_ctas = 0;
+  int att_min_tiles = 4;      // fewest K/V tiles per attention split
+};
+
+}  // namespace ss

@@ -49,7 +49,8 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
-           "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm"]
+           "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
+           "ss_step_kernel_active"]
 SS_DEBUG_CONSISTENCY = 1
 
 
@@ -73,6 +74,8 @@ def lib():
         "ss_destroy": (i32, [vp]),
         "ss_last_error": (C.c_char_p, [vp]),
         "ss_set_debug": (i32, [vp, i32]),
+        "ss_set_step_kernel": (i32, [vp, i32]),
+        "ss_step_kernel_active": (i32, [vp, i32]),
         "ss_read_tree_meta": (i32, [vp, vp, vp, vp, vp, vp]),
         "ss_read_packed": (i32, [vp, i32, i32, vp, sz, C.POINTER(sz)]),
         "ss_debug_gemm": (i32, [vp, i32, i32, vp, i32, vp, i32, vp]),
@@ -140,6 +143,13 @@ class Shard:
 
     def _ck(self, code: int):
         _check(code, self.h)
+
+    def set_step_kernel(self, on: bool):
+        """True (default): the persistent one-launch step for T <= 32; False: per-phase kernels."""
+        self._ck(lib().ss_set_step_kernel(self.h, 1 if on else 0))
+
+    def step_kernel_active(self, T: int) -> bool:
+        return lib().ss_step_kernel_active(self.h, T) == 1
 
     def set_debug(self, flags: int):
         """SS_DEBUG_CONSISTENCY: cross-rank checksum of every verify's tree."""
@@ -236,12 +246,12 @@ class Shard:
         return lib().ss_kernels_per_step(self.h, T, 1 if auto_commit else 0)
 
     PROF_KINDS = ["embed+tree", "qkv", "attention", "o_proj", "rmsnorm", "gate_up_swiglu", "down",
-                  "lm_head_argmax_accept", "commit"]
+                  "lm_head_argmax_accept", "commit", "step_kernel"]
 
     def profile_step(self, d_tokens, d_parents, T: int, stream=None):
         """Eager step with CUDA events around every kernel -> {kind: (ms, launches)}."""
-        ms = np.zeros(9, dtype=np.float32)
-        cnt = np.zeros(9, dtype=np.int32)
+        ms = np.zeros(len(self.PROF_KINDS), dtype=np.float32)
+        cnt = np.zeros(len(self.PROF_KINDS), dtype=np.int32)
         ptr = lambda x: x if isinstance(x, int) else x.data_ptr()
         self._ck(lib().ss_profile_step(self.h, ptr(d_tokens), ptr(d_parents), T, _ptr(ms), _ptr(cnt),
                                      _stream_handle(stream)))

@@ -258,6 +258,21 @@ int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_commit);
 ss_status ss_set_step_kernel(ss_shard* s, int32_t on);
 int32_t ss_step_kernel_active(ss_shard* s, int32_t T);
 
+/* Measurement hook: on != 0 makes every later persistent-step launch record a
+ * timeline -- per CTA (up to 512), per slot (layer * 5 + phase: 0 QKV,
+ * 1 attention, 2 O, 3 gate/up, 4 down; slot n_layers * 5 = LM head), three
+ * %globaltimer ns stamps (phase entry, first unit ready, phase exit; 0 = the
+ * CTA had no work there).  ss_read_step_trace copies it to `host` (n >= 512 *
+ * slots * 3 elements; *n_ctas = 512, *slots = n_layers * 5 + 1) after a device
+ * synchronize.  on == 2 keeps the timeline in mapped host memory, read
+ * without synchronising (diagnosis of a launch that does not finish).  Off by
+ * default; toggling drops the captured graphs. */
+ss_status ss_step_trace(ss_shard* s, int32_t on);
+ss_status ss_read_step_trace(ss_shard* s, uint64_t* host, size_t n, int32_t* n_ctas, int32_t* slots);
+/* The mapped host buffer of on == 2 (NULL otherwise): [512][slots][3] stamps,
+ * then [512 CTAs][16 warps] progress words; readable with no CUDA call. */
+void* ss_step_trace_host(ss_shard* s);
+
 /* Measurement helper (bench.py's roofline): run one all-device step like
  * ss_verify_tree_dev(auto_commit=1) but launched eagerly with a CUDA event
  * pair around every kernel on `stream`; synchronises and writes the summed

@@ -152,6 +152,9 @@ struct ss_shard {
   void* layer_tab = nullptr;       // device LayerPtrs[n_layers]
   void* step_args_dev = nullptr;   // device StepArgs x 2 (without / with the logits output)
   int step_max_ctas = 0;
+  unsigned long long* step_trace = nullptr;  // ss_step_trace timeline (null: off)
+  int step_trace_slots = 0;
+  unsigned long long* step_trace_host = nullptr;  // mapped host buffer (ss_step_trace(s, 2))
   bool use_step = true;            // NT <= 4: persistent step kernel; else per-phase kernels
 
   // graphs: key = NT*4 + auto_commit*2 + logits

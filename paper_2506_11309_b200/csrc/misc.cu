@@ -5,6 +5,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "kernels.h"
+#include "step.h"
 
 namespace ss {
 
@@ -66,24 +67,16 @@ struct StepIngest {
   uint8_t* act_lm = nullptr;
   int K_o = 0, K_d = 0;
 };
-SS_DEV uint32_t a2_off(int tt, int k, int NT, int lo) {
-  return (uint32_t)(k >> 8) * ((uint32_t)NT * 8192u + (uint32_t)NT * 64u) + (lo ? (uint32_t)NT * 4096u : 0u) +
-         frag_offset(tt, k & 255, NT);
-}
-SS_DEV uint32_t a2_x(int tt, int g, int NT) {
-  return (uint32_t)(g >> 1) * ((uint32_t)NT * 8192u + (uint32_t)NT * 64u) + (uint32_t)NT * 8192u +
-         (uint32_t)(((g & 1) * 8 * NT + tt) * 4);
-}
 // zero token slot t of an a2-layout buffer with K columns (columns split over kNormSplit CTAs)
 SS_DEV void zero_a2_slot(uint8_t* act, int t, int K, int NT, int part) {
   for (int f = threadIdx.x; f < K / 4; f += 256)
     if ((f % 4) == part)
       for (int lo = 0; lo < 2; ++lo) {
-        *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f, NT, lo)) = 0u;
-        *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f + 2, NT, lo)) = 0u;
+        *reinterpret_cast<uint32_t*>(act + a2_frag(t, 4 * f, NT, lo)) = 0u;
+        *reinterpret_cast<uint32_t*>(act + a2_frag(t, 4 * f + 2, NT, lo)) = 0u;
       }
   for (int g = threadIdx.x; g < K / 128; g += 256)
-    if ((g % 4) == part) *reinterpret_cast<float*>(act + a2_x(t, g, NT)) = 0.f;
+    if ((g % 4) == part) *reinterpret_cast<float*>(act + a2_xsum(t, g, NT)) = 0.f;
 }
 
 struct ConsistencyArgs {
@@ -264,15 +257,15 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
         xs = (half2_sum(h01) + half2_sum(l01)) + (half2_sum(h23) + half2_sum(l23));
         if ((f % kNormSplit) == part) {
           xs4[f] = v[i];
-          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f, NT, 0)) = h01;
-          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f + 2, NT, 0)) = h23;
-          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f, NT, 1)) = l01;
-          *reinterpret_cast<uint32_t*>(act + a2_off(t, 4 * f + 2, NT, 1)) = l23;
+          *reinterpret_cast<uint32_t*>(act + a2_frag(t, 4 * f, NT, 0)) = h01;
+          *reinterpret_cast<uint32_t*>(act + a2_frag(t, 4 * f + 2, NT, 0)) = h23;
+          *reinterpret_cast<uint32_t*>(act + a2_frag(t, 4 * f, NT, 1)) = l01;
+          *reinterpret_cast<uint32_t*>(act + a2_frag(t, 4 * f + 2, NT, 1)) = l23;
         }
       }
       xs = warp_sum(xs);  // the warp's 32 vectors are exactly one 128-group
       const int g = f >> 5;
-      if ((tid & 31) == 0 && f < nv && (g % kNormSplit) == part) *reinterpret_cast<float*>(act + a2_x(t, g, NT)) = xs;
+      if ((tid & 31) == 0 && f < nv && (g % kNormSplit) == part) *reinterpret_cast<float*>(act + a2_xsum(t, g, NT)) = xs;
     }
     return;
   }

@@ -438,6 +438,8 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
                   s->sc_lm.counters, s->sc_o.ss, s->sc_o.nbar, s->sc_down.ss, s->sc_down.nbar, s->step_ctr,
                   s->step_ss, s->qf, s->klo, s->vlo, s->att_ws, s->att_ml, s->layer_tab, s->sc_qkv.ss,
                   s->sc_qkv.nbar, s->sc_gu.ss, s->sc_gu.nbar, s->sc_lm.ss, s->sc_lm.nbar, s->step_args_dev};
+  if (s->step_trace_host) cudaFreeHost(s->step_trace_host);
+  else if (s->step_trace) cudaFree(s->step_trace);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->hstate) cudaFreeHost(s->hstate);
@@ -827,7 +829,7 @@ static Prof* g_prof = nullptr;
 // Whether the persistent step kernel runs this tree width: T <= 32 (NT <= 4)
 // and every attention (kv head, 64-row chunk) group fits the grid.
 static bool step_path(const ss_shard* s, int NT) {
-  if (!s->use_step || NT > 4) return false;
+  if (!s->use_step || NT > 4 || s->cfg.n_layers > kStepMaxLayers) return false;
   const int groups = s->Hkv_l * ((s->G * 8 * NT + 63) / 64);
   return groups <= step_ctas(NT, s->cfg.head_dim, s->launch_cap);
 }
@@ -883,6 +885,10 @@ static StepArgs step_args(ss_shard* s, int want_logits) {
   a.V_off = s->V_off;
   a.logits_ld = s->V_l_pad;
   a.logits = want_logits ? s->logits_dev : nullptr;
+  a.trace = s->step_trace;
+  a.trace_slots = s->step_trace_slots;
+  a.where = s->step_trace_host ? s->step_trace + (size_t)512 * s->step_trace_slots * 3 : nullptr;
+  a.utl = s->step_trace ? s->step_trace + (size_t)512 * s->step_trace_slots * 3 + 512 * 16 : nullptr;
   return a;
 }
 
@@ -1175,6 +1181,56 @@ extern "C" ss_status ss_set_step_kernel(ss_shard* s, int32_t on) {
   for (auto& kv : s->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" ss_status ss_step_trace(ss_shard* s, int32_t on) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (s->step_trace) {
+    if (s->step_trace_host) cudaFreeHost(s->step_trace_host);
+    else cudaFree(s->step_trace);
+  }
+  s->step_trace = nullptr;
+  s->step_trace_host = nullptr;
+  s->step_trace_slots = 0;
+  if (on) {
+    s->step_trace_slots = s->cfg.n_layers * 5 + 1;
+    const size_t n = (size_t)512 * s->step_trace_slots * 3 + 512 * 16 + 65536;
+    if (on == 2) {  // mapped host memory: readable while a launch is still running (hang diagnosis)
+      CUDA_TRY(cudaHostAlloc(&s->step_trace_host, n * 8, cudaHostAllocMapped));
+      memset(s->step_trace_host, 0, n * 8);
+      CUDA_TRY(cudaHostGetDevicePointer((void**)&s->step_trace, s->step_trace_host, 0));
+    } else {
+      CUDA_TRY(cudaMalloc(&s->step_trace, n * 8));
+      CUDA_TRY(cudaMemset(s->step_trace, 0, n * 8));
+    }
+  }
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" void* ss_step_trace_host(ss_shard* s) { return s ? (void*)s->step_trace_host : nullptr; }
+
+extern "C" ss_status ss_read_step_trace(ss_shard* s, uint64_t* host, size_t n, int32_t* n_ctas, int32_t* slots) {
+  SCOPE(s);
+  if (!s || !host) FAIL(SS_EINVAL, "null argument");
+  if (!s->step_trace) FAIL(SS_ESTATE, "trace not enabled");
+  const size_t need = (size_t)512 * s->step_trace_slots * 3 + 512 * 16 + 65536;
+  if (n < need) FAIL(SS_EINVAL, "buffer too small");
+  cudaSetDevice(s->device);
+  if (s->step_trace_host) {
+    memcpy(host, s->step_trace_host, need * 8);  // no synchronisation (on == 2)
+  } else {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(host, s->step_trace, need * 8, cudaMemcpyDeviceToHost));
+  }
+  if (n_ctas) *n_ctas = 512;
+  if (slots) *slots = s->step_trace_slots;
   return SS_OK;
 }
 

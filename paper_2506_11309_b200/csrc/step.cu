@@ -36,10 +36,17 @@ struct StepCfg {
   static constexpr int ABYTES = (int)a2_stage_bytes(NT);           // W4 input per unit (hi, lo, X)
   static constexpr int LM_ABYTES = (kBFKS / 16) * 2 * NT * 256;     // LM input per unit (bf16 hi, lo)
   static constexpr int SLOT = kW4UnitBytes + ABYTES;                // >= LM unit, >= one 16 KB K/V tile
-  static constexpr int CTAS_PER_SM = NT <= 2 ? 2 : 1;
-  static constexpr int STAGES = (CTAS_PER_SM == 2 ? 102400 : 204800) / SLOT;
-  static constexpr int SMEM = STAGES * SLOT;
-  static constexpr int THREADS = 288;  // 8 consumer warps + 1 producer warp
+  static constexpr int CTAS_PER_SM = 1;  // owns the SM's 512 TMEM columns
+  static constexpr int QBYTES = 32768;  // attention: the item's q fragments (64 rows x d <= 128, hi + lo)
+  static constexpr int STAGES = (204800 - QBYTES) / SLOT;
+  static constexpr int SMEM = STAGES * SLOT + QBYTES;
+  // 8 consumer warps (warpgroups 0, 1) + warpgroup 2: producer warp, MMA warp,
+  // two idle warps.  Launched at 168 registers (3 warps per SMSP); warpgroup 2
+  // gives registers back (setmaxnreg) so the consumers run with 208.
+  static constexpr int THREADS = 384;
+  static constexpr int REG_CONSUMER = 208, REG_AUX = 80;  // 8 x 208 + 4 x 80 <= 12 x 168 (the CTA pool)
+  static constexpr int TP = 8 * NT;    // token slots
+  static constexpr int N = 2 * TP;     // MMA N: hi and lo columns of every token slot
   static constexpr int NCT = 256;
   static_assert(SLOT >= kBFUnitBytes + LM_ABYTES && SLOT >= 16384 && STAGES >= 3, "slot");
 };
@@ -47,12 +54,6 @@ struct StepCfg {
 enum { PH_QKV = 0, PH_ATT = 1, PH_O = 2, PH_GU = 3, PH_DN = 4, PH_LM = 5, PH_END = 6 };
 enum { ACC_QKV = 0, ACC_O = 1, ACC_GU = 2, ACC_DN = 3, ACC_LM = 4 };
 
-SS_DEV uint32_t a2_frag(int tt, int k, int NT, int lo) {
-  return (uint32_t)(k >> 8) * a2_stage_bytes(NT) + (lo ? (uint32_t)NT * 4096u : 0u) + frag_offset(tt, k & 255, NT);
-}
-SS_DEV uint32_t a2_xsum(int tt, int g, int NT) {
-  return (uint32_t)(g >> 1) * a2_stage_bytes(NT) + (uint32_t)NT * 8192u + (uint32_t)(((g & 1) * 8 * NT + tt) * 4);
-}
 // fp16 hi + lo of a pair of values; returns (hi + lo) summed as floats
 SS_DEV float split16(float a, float b, uint32_t& hi, uint32_t& lo) {
   hi = pack_half2(a, b);
@@ -65,14 +66,21 @@ SS_DEV float split16(float a, float b, uint32_t& hi, uint32_t& lo) {
 
 // Watchdog: every wait of the persistent kernel is bounded; a protocol bug
 // traps (the launch fails with an error) instead of hanging the GPU.
-constexpr unsigned long long kWatchdogNs = 10000000000ull;  // 10 s
+// (clock64 based: %globaltimer reads are slow and sit on the producer's and
+// the waits' critical paths; 2e10 cycles = 10 s at 1.965 GHz)
+constexpr unsigned long long kWatchdogClk = 20000000000ull;
 SS_DEV unsigned long long now_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+SS_DEV unsigned long long clk64() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
 SS_DEV void watchdog(unsigned long long t0) {
-  if (now_ns() - t0 > kWatchdogNs) asm volatile("trap;");
+  if (clk64() - t0 > kWatchdogClk) asm volatile("trap;");
 }
 SS_DEV bool mbar_try_a(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -87,17 +95,76 @@ SS_DEV bool mbar_try_a(uint32_t bar, uint32_t parity) {
 }
 SS_DEV void mbar_wait_wd(uint32_t bar, uint32_t parity) {
   if (mbar_try_a(bar, parity)) return;
-  const unsigned long long t0 = now_ns();
+  const unsigned long long t0 = clk64();
   while (!mbar_try_a(bar, parity)) watchdog(t0);
 }
+SS_DEV int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Poll relaxed (ld.acquire.gpu invalidates the SM's L1 on every poll, hurting
+// every warp that reads cached global data), acquire once when satisfied.
 SS_DEV void spin_until_geq(const int* p, int target) {
   if (ld_acquire_gpu(p) >= target) return;
-  const unsigned long long t0 = now_ns();
-  while (ld_acquire_gpu(p) < target) {
+  const unsigned long long t0 = clk64();
+  while (ld_relaxed_gpu(p) < target) {
     __nanosleep(64);
     watchdog(t0);
   }
+  (void)ld_acquire_gpu(p);
 }
+
+SS_DEV void tmark(const StepArgs& a, int slot, int which) {
+  if (a.trace && threadIdx.x == 0) a.trace[((size_t)blockIdx.x * a.trace_slots + slot) * 3 + which] = now_ns();
+}
+
+// tcgen05 (5th-gen tensor cores, TMEM accumulators) ------------------------
+// TMEM map of the CTA (512 columns, lane = output row of the 128-row tile):
+//   [0, 256)   A operand, two buffers of one W4 unit (256 k = 128 fp16x2 columns)
+//   [256, 512) fp32 accumulators, [buffer 2][AWQ group 2][N columns]
+constexpr uint32_t kTmemCols = 512, kAccCol = 256;
+SS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SS_DEV void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+SS_DEV void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 16 TMEM lanes x 32 columns; register 4j + (0..3) of thread (g, q) = (lane g,
+// col 8j + 2q), (g, 8j + 2q + 1), (g + 8, 8j + 2q), (g + 8, 8j + 2q + 1)
+// (the mma.m16n8 fragment pattern, CuTe SM100_TMEM_STORE_16dp256b).
+SS_DEV void tc_st_16x256b_x4(uint32_t ta, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+// thread i <- TMEM lane (base lane + i), 16 consecutive columns
+SS_DEV void tc_ld_32x32b_x16(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta)
+      : "memory");
+}
+// Shared-memory matrix descriptor, K-major, no swizzle (sm100 version 1):
+// lbo = bytes between the two 8-deep k chunks, sbo = bytes between 8-row groups.
+SS_DEV uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// Instruction descriptor kind::f16: D f32, A / B f16, both K-major, N, M.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+SS_DEV void where(const StepArgs& a, uint32_t code) {
+  if (a.where && (threadIdx.x & 31) == 0)
+    *reinterpret_cast<volatile unsigned long long*>(a.where + blockIdx.x * 16 + (threadIdx.x >> 5)) =
+        ((unsigned long long)code << 32) | (now_ns() & 0xFFFFFFFFull);
+}
+SS_DEV int lane_id() { return threadIdx.x & 31; }
+#define WCODE(layer, ph, pt) (((uint32_t)(layer) << 16) | ((uint32_t)(ph) << 8) | (uint32_t)(pt))
 
 // Static schedule ------------------------------------------------------------
 // GEMM phases: the U units (tile-group major) are split in equal contiguous
@@ -153,8 +220,17 @@ SS_DEV void make_sched(const StepArgs& a, int b, int L, int T, int NT, Sched& s)
 SS_DEV bool tile_is_tree(const Sched& s, int tile) { return (tile + 1) * s.att_KT > s.L; }
 
 // Producer iterator over this CTA's unit sequence ---------------------------
+// Per-phase data (unit range, weight / activation bases, dependency) is cached
+// at each phase change, so advancing over a GEMM / LM-head unit is a handful
+// of integer ops: the single producer thread shares its SMSP with two busy
+// consumer warps, and its per-unit instruction count bounds the stream rate.
 struct UnitIt {
   int layer, ph, i, lo;
+  int i1, st, S;             // range end, stage i % S, stages per tile-group
+  const uint8_t* w;          // GEMM / LM head: unit 0's weights of this phase
+  const uint8_t* act;        // stage 0's activations
+  const int* dep;            // part-2 dependency
+  int target;
 };
 
 SS_DEV void range_of(const Sched& s, int ph, int& i0, int& i1) {
@@ -169,17 +245,48 @@ SS_DEV void range_of(const Sched& s, int ph, int& i0, int& i1) {
   }
 }
 
+// Cache the per-phase fields of it (it.ph, it.layer, it.i set).
+SS_DEV void it_cache(const StepArgs& a, const Sched& s, UnitIt& it) {
+  const int l = it.layer;
+  const int* ctr = a.ctr + (size_t)l * kCtrPerLayer;
+  it.dep = nullptr;
+  it.target = 0;
+  it.S = 1;
+  it.w = it.act = nullptr;
+  if (it.ph == PH_ATT || it.ph == PH_END) return;
+  if (it.ph == PH_LM) {
+    it.w = a.lm_w; it.act = a.act_lm; it.S = a.lm_S;
+    it.dep = a.ctr + (size_t)(a.n_layers - 1) * kCtrPerLayer + C_DN; it.target = a.dn_tg;
+  } else {
+    const LayerPtrs& lp = a.layers[l];
+    switch (it.ph) {
+      case PH_QKV:
+        it.w = lp.qkv; it.act = a.act_h; it.S = a.qkv_S;
+        if (l > 0) { it.dep = ctr - kCtrPerLayer + C_DN; it.target = a.dn_tg; }
+        break;
+      case PH_O: it.w = lp.o; it.act = a.act_o; it.S = a.o_S; it.dep = ctr + C_ATT; it.target = s.att_A; break;
+      case PH_GU: it.w = lp.gu; it.act = a.act_h; it.S = a.gu_S; it.dep = ctr + C_O; it.target = a.o_tg; break;
+      default: it.w = lp.down; it.act = a.act_d; it.S = a.dn_S; it.dep = ctr + C_GU; it.target = a.gu_tg; break;
+    }
+  }
+  it.st = it.i % it.S;
+}
+
 // Move to the first unit at or after (layer, ph, i).
-SS_DEV void it_settle(const Sched& s, int n_layers, UnitIt& it) {
+SS_DEV void it_settle(const StepArgs& a, const Sched& s, UnitIt& it) {
   while (it.ph != PH_END) {
     int i0, i1;
     range_of(s, it.ph, i0, i1);
     if (it.i < i0) it.i = i0;
-    if (it.i < i1) return;
+    if (it.i < i1) {
+      it.i1 = i1;
+      it_cache(a, s, it);
+      return;
+    }
     it.lo = 0;
     if (it.ph == PH_LM) { it.ph = PH_END; return; }
     if (it.ph == PH_DN) {
-      if (++it.layer == n_layers) it.ph = PH_LM;
+      if (++it.layer == a.n_layers) it.ph = PH_LM;
       else it.ph = PH_QKV;
     } else {
       ++it.ph;
@@ -188,14 +295,15 @@ SS_DEV void it_settle(const Sched& s, int n_layers, UnitIt& it) {
   }
 }
 
-SS_DEV void it_next(const Sched& s, int n_layers, UnitIt& it) {
+SS_DEV void it_next(const StepArgs& a, const Sched& s, UnitIt& it) {
   if (it.ph == PH_ATT && !it.lo && tile_is_tree(s, it.i)) {
     it.lo = 1;
     return;
   }
   it.lo = 0;
   ++it.i;
-  it_settle(s, n_layers, it);
+  if (++it.st == it.S) it.st = 0;
+  if (it.i >= it.i1) it_settle(a, s, it);
 }
 
 // Bytes and sources of one unit.
@@ -264,9 +372,9 @@ SS_DEV void unit_src(const StepArgs& a, const Sched& s, const UnitIt& it, UnitSr
   u.a = act + (size_t)(it.i % S) * C::ABYTES; u.abytes = C::ABYTES; u.a_off = kW4UnitBytes;
 }
 
-// The producer: lane 0 of warp 8.  Issues part 1 of unit w whenever its ring
-// slot is free and part 2 of the oldest unit still missing it whenever that
-// unit's dependency is met -- never blocking on one while the other could
+// The producer: lane 0 of warp 8.  Issues part 1 of every unit whose ring
+// slot is free and part 2 of every unit (in order) whose dependency is met --
+// as many as possible per pass, never blocking on one while the other could
 // make progress.
 template <int NT>
 __device__ __noinline__ void producer(const StepArgs* __restrict__ ap, const Sched* __restrict__ sp, uint32_t sm0,
@@ -275,23 +383,28 @@ __device__ __noinline__ void producer(const StepArgs* __restrict__ ap, const Sch
   const StepArgs& a = *ap;
   const Sched s = *sp;
   const uint64_t pol = policy_evict_first();
-  UnitIt wi{0, PH_QKV, -1, 0}, ai;
-  it_settle(s, a.n_layers, wi);
-  ai = wi;
+  UnitIt wi;
+  wi.layer = 0; wi.ph = PH_QKV; wi.i = -1; wi.lo = 0;
+  it_settle(a, s, wi);
+  UnitIt ai = wi;
   int wk = 0, ak = 0;        // units issued (part 1 / part 2)
   const int* ok_dep = nullptr;
   int ok_target = 0;
-  unsigned long long t_idle = now_ns();
+  unsigned long long t_idle = clk64();
   while (ai.ph != PH_END) {
     bool prog = false;
-    if (wi.ph != PH_END) {
+    // part 1: weights (or prefix K/V tiles) into every free slot
+    while (wi.ph != PH_END && wk - ak < C::STAGES) {
       const int slot = wk % C::STAGES;
-      const uint32_t par = (uint32_t)((wk / C::STAGES) & 1);
-      if (mbar_test_a(empty0 + 8 * slot, par ^ 1)) {
-        fence_proxy_async_smem();  // consumers' reads of the slot before the TMA overwrite
+      if (!mbar_test_a(empty0 + 8 * slot, (uint32_t)(((wk / C::STAGES) & 1) ^ 1))) break;
+      const uint32_t dst = sm0 + slot * C::SLOT, bar = full0 + 8 * slot;
+      if (wi.ph != PH_ATT) {
+        const uint32_t ub = wi.ph == PH_LM ? (uint32_t)kBFUnitBytes : (uint32_t)kW4UnitBytes;
+        mbar_expect_tx_noarrive_a(bar, ub);
+        bulk_g2s_a(dst, wi.w + (size_t)wi.i * ub, ub, bar, pol);
+      } else {
         UnitSrc u;
         unit_src<NT>(a, s, wi, u);
-        const uint32_t dst = sm0 + slot * C::SLOT, bar = full0 + 8 * slot;
         if (u.wbytes) {
           const uint32_t tot = u.wbytes + u.w2bytes;
           if (u.abytes) mbar_expect_tx_noarrive_a(bar, tot);
@@ -299,42 +412,54 @@ __device__ __noinline__ void producer(const StepArgs* __restrict__ ap, const Sch
           bulk_g2s_a(dst, u.w, u.wbytes, bar, pol);
           if (u.w2bytes) bulk_g2s_a(dst + u.w2_off, u.w2, u.w2bytes, bar, pol);
         }
-        ++wk;
-        it_next(s, a.n_layers, wi);
-        prog = true;
       }
+      ++wk;
+      it_next(a, s, wi);
+      prog = true;
     }
-    if (ak < wk) {
+    // part 2: activations (or tree K/V rows) once their producing phase is done
+    while (ak < wk) {
+      const int* dep;
+      int target;
       UnitSrc u;
-      unit_src<NT>(a, s, ai, u);
-      bool go = true;
-      if (u.abytes && u.dep && !(u.dep == ok_dep && u.target <= ok_target)) {
-        const int v = ld_acquire_gpu(u.dep);
-        go = v >= u.target;
-        if (go) {
-          ok_dep = u.dep;
-          ok_target = u.target;
-          fence_proxy_async_global();  // the producers' generic stores before our async-proxy reads
-        }
+      const bool att = ai.ph == PH_ATT;
+      if (att) {
+        unit_src<NT>(a, s, ai, u);
+        dep = u.dep;
+        target = u.target;
+      } else {
+        dep = ai.dep;
+        target = ai.target;
       }
-      if (go) {
-        if (u.abytes) {
-          const int slot = ak % C::STAGES;
-          const uint32_t dst = sm0 + slot * C::SLOT, bar = full0 + 8 * slot;
-          mbar_arrive_expect_tx_a(bar, u.abytes + u.a2bytes);
-          bulk_g2s_nohint_a(dst + u.a_off, u.a, u.abytes, bar);
-          if (u.a2bytes) bulk_g2s_nohint_a(dst + u.a2_off, u.a2, u.a2bytes, bar);
-        }
-        ++ak;
-        it_next(s, a.n_layers, ai);
-        prog = true;
+      if (dep && !(dep == ok_dep && target <= ok_target)) {
+        if (ld_relaxed_gpu(dep) < target) break;
+        (void)ld_acquire_gpu(dep);
+        ok_dep = dep;
+        ok_target = target;
+        fence_proxy_async_global();  // the producers' generic stores before our async-proxy reads
       }
+      const int slot = ak % C::STAGES;
+      const uint32_t dst = sm0 + slot * C::SLOT, bar = full0 + 8 * slot;
+      if (!att) {
+        const uint32_t abytes = ai.ph == PH_LM ? (uint32_t)C::LM_ABYTES : (uint32_t)C::ABYTES;
+        const uint32_t aoff = ai.ph == PH_LM ? (uint32_t)kBFUnitBytes : (uint32_t)kW4UnitBytes;
+        mbar_arrive_expect_tx_a(bar, abytes);
+        bulk_g2s_nohint_a(dst + aoff, ai.act + (size_t)ai.st * abytes, abytes, bar);
+      } else if (u.abytes) {
+        mbar_arrive_expect_tx_a(bar, u.abytes + u.a2bytes);
+        bulk_g2s_nohint_a(dst + u.a_off, u.a, u.abytes, bar);
+        if (u.a2bytes) bulk_g2s_nohint_a(dst + u.a2_off, u.a2, u.a2bytes, bar);
+      }
+      ++ak;
+      it_next(a, s, ai);
+      prog = true;
     }
     if (!prog) {
+      where(a, WCODE(ai.layer, 0x40 + ai.ph, wi.ph == PH_END ? 0xEE : 0x01));
       __nanosleep(32);
       watchdog(t_idle);
     } else {
-      t_idle = now_ns();
+      t_idle = clk64();
     }
   }
 }
@@ -360,74 +485,170 @@ SS_DEV void ring_release(Ring& r) {
   ++r.k;
 }
 
-SS_DEV void cbar() { named_bar_sync(1, 256); }  // the 8 consumer warps
+template <int NT>
+SS_DEV uint32_t ring_wait_at(const Ring& r, int k) {
+  using C = StepCfg<NT>;
+  const int slot = k % C::STAGES;
+  mbar_wait_wd(r.full0 + 8 * slot, (uint32_t)((k / C::STAGES) & 1));
+  return r.sm0 + slot * C::SLOT;
+}
+template <int NT>
+SS_DEV void ring_release_at(const Ring& r, int k) {
+  using C = StepCfg<NT>;
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_a(r.empty0 + 8 * (k % C::STAGES));
+}
+SS_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+// the 8 consumer warps; each warp converges first (a thread-0-only block
+// before a barrier must not let the warp's other lanes arrive without it)
+SS_DEV void cbar() {
+  __syncwarp();
+  named_bar_sync(1, 256);
+}
 
 SS_DEV void wait_counter(const int* p, int target) {
   if (threadIdx.x == 0) spin_until_geq(p, target);
   cbar();
 }
 
-// One W4 unit, PAIR mapping (gemm.cu): warp = two 16-row tiles x one 128-deep
-// group; B fragments (fp16 hi and lo) feed two MMAs each.
+// W4 units on tcgen05 -----------------------------------------------------------
+// A unit = 128 output rows x 256 k (gemm.cu layout: [16-row tile 8][64-deep
+// k block 4][lane 32][4 nibble words], each word one m16n8k16 A fragment).
+// Consumer warp w (quadrant qd = w % 4, half hh = w / 4) dequantises tile
+// 2 qd + hh -- TMEM lanes 32 qd + 16 hh .. + 15, the lanes its quadrant may
+// access -- with the lop3 trick into fp16 (1024 + q, or 1024 + 16 q on the
+// tile's rows 8..15) and stores the fragments with tcgen05.st.16x256b, whose
+// register pattern is the fragment pattern: column pair order within each k16
+// step becomes (0 4 1 5 2 6 3 7), matched by the activation layout (a2_frag).
+// The MMA warp runs the unit's 16 MMAs (M 128, N = 2 TP hi + lo columns, K 16)
+// into one fresh accumulator per AWQ group; then warp w reads group hh of
+// rows 32 qd + lane and applies the exact zero point / scale (R3, R19, R20):
+//   y[t] += s * ((acc_hi[t] + acc_lo[t]) - (1024 + z) * X[t]).
+struct Tc {
+  uint32_t tbase;    // TMEM base address
+  uint32_t ardy0;    // mbarrier[2]: the unit's A operand is in TMEM (8 warp arrivals)
+  uint32_t mdone0;   // mbarrier[2]: the unit's MMAs completed (tcgen05.commit)
+  uint32_t* slot;    // shared [2]: smem address of the unit's ring slot (0 = stop)
+};
+
 template <int NT>
-SS_DEV void w4_unit(uint32_t sst, int warp, int lane, float (&acc)[NT][4], float (&acc1)[NT][4]) {
-  const int tile = 2 * (warp & 3), grp = warp >> 2;
-  const int gq = lane >> 2, tq = lane & 3;
-  const uint32_t o_w = (uint32_t)(tile * 128 + lane) * 16;
-  const uint32_t o_sc = (uint32_t)(kW4Bytes + tile * 64 + gq * 4);
-  const uint32_t o_z = (uint32_t)(kW4Bytes + 512 + tile * 16 + gq);
-  const uint32_t o_b = (uint32_t)(kW4UnitBytes + lane * 16);
-  const uint32_t o_x = (uint32_t)(kW4UnitBytes + NT * 8192 + 8 * tq);
-  uint32_t wa[2][8];
+SS_DEV void tc_dequant(const Tc& tc, uint32_t sst, int b, int warp, int lane) {
+  const int qd = warp & 3, hh = warp >> 2;
+  const uint32_t wbase = sst + (uint32_t)(((2 * qd + hh) * 4) * 512 + lane * 16);
+  const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd + 16 * hh) << 16) + (uint32_t)(b * 128);
+  __syncwarp();  // tcgen05 .sync.aligned: the warp must be converged (lanes leave the ring wait apart)
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const uint4 w0 = lds128(sst + o_w + i * 2048 + (grp * 2) * 512);
-    const uint4 w1 = lds128(sst + o_w + i * 2048 + (grp * 2 + 1) * 512);
-    wa[i][0] = w0.x; wa[i][1] = w0.y; wa[i][2] = w0.z; wa[i][3] = w0.w;
-    wa[i][4] = w1.x; wa[i][5] = w1.y; wa[i][6] = w1.z; wa[i][7] = w1.w;
-  }
-  float cg[2][NT][4];
+  for (int kb = 0; kb < 4; ++kb) {
+    const uint4 w = lds128(wbase + kb * 512);
+    uint32_t r[16], af[4];
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int n = 0; n < NT; ++n) cg[i][n][0] = cg[i][n][1] = cg[i][n][2] = cg[i][n][3] = 0.f;
-#pragma unroll
-  for (int jp = 0; jp < 4; ++jp) {
-    uint4 bh[NT], bl[NT];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      bh[n] = lds128(sst + o_b + ((grp * 4 + jp) * NT + n) * 512);
-      bl[n] = lds128(sst + o_b + NT * 4096 + ((grp * 4 + jp) * NT + n) * 512);
+    for (int j = 0; j < 4; ++j) {
+      dequant8(wv[j], af);
+      r[4 * j + 0] = af[0];
+      r[4 * j + 1] = af[2];
+      r[4 * j + 2] = af[1];
+      r[4 * j + 3] = af[3];
     }
+    tc_st_16x256b_x4(ta + kb * 32, r);
+  }
+}
+// The unit's A operand is complete in TMEM: hand it to the MMA warp.
+SS_DEV void tc_signal(const Tc& tc, uint32_t sst, int b, int warp, int lane) {
+  tc_wait_st();
+  tc_fence_before();
+  __syncwarp();
+  if (warp == 0 && lane == 0) tc.slot[b] = sst;
+  if (lane == 0) mbar_arrive_a(tc.ardy0 + 8 * b);
+}
+
+template <int NT>
+SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, float (&y)[8 * NT]) {
+  constexpr int TP = 8 * NT, N = 16 * NT;
+  const int qd = warp & 3, hh = warp >> 2, b = k & 1;
+  mbar_wait_wd(tc.mdone0 + 8 * b, (uint32_t)((k >> 1) & 1));
+  __syncwarp();
+  tc_fence_after();
+  // metadata of row m = 32 qd + lane (tile m / 16, fragment row m % 16) in group hh
+  const int m = 32 * qd + lane, tile = m >> 4, r16 = m & 15, g8 = r16 & 7, up = r16 >> 3;
+  const uint32_t zb = lds8(sst + kW4Bytes + 512 + tile * 16 + hh * 8 + g8);
+  const uint32_t sp = lds32(sst + kW4Bytes + tile * 64 + hh * 32 + g8 * 4);
+  const float sc = up ? __uint_as_float(sp & 0xFFFF0000u) * 0.0625f : __uint_as_float(sp << 16);
+  const float cz = up ? 1024.f + 16.f * (float)(zb >> 4) : 1024.f + (float)(zb & 15u);
+  float X[TP];
+  const uint32_t xo = sst + kW4UnitBytes + NT * 8192 + hh * TP * 4;
 #pragma unroll
-    for (int js = 0; js < 2; ++js)
+  for (int t = 0; t < TP; t += 4) {
+    const uint4 v = lds128(xo + t * 4);
+    X[t] = __uint_as_float(v.x); X[t + 1] = __uint_as_float(v.y);
+    X[t + 2] = __uint_as_float(v.z); X[t + 3] = __uint_as_float(v.w);
+  }
+  const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccCol + (uint32_t)((b * 2 + hh) * N);
+  if constexpr (TP == 8) {
+    uint32_t r[16];
+    tc_ld_32x32b_x16(ta, r);
+    tc_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        uint32_t af[4];
-        dequant8(wa[i][jp * 2 + js], af);
+    for (int t = 0; t < 8; ++t)
+      y[t] = fmaf(sc, fmaf(-cz, X[t], __uint_as_float(r[t]) + __uint_as_float(r[8 + t])), y[t]);
+  } else {
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          mma_f16_16816(cg[i][n], af, js ? bh[n].z : bh[n].x, js ? bh[n].w : bh[n].y);
-          mma_f16_16816(cg[i][n], af, js ? bl[n].z : bl[n].x, js ? bl[n].w : bl[n].y);
-        }
+    for (int j = 0; j < TP / 16; ++j) {
+      uint32_t rh[16], rl[16];
+      tc_ld_32x32b_x16(ta + 16 * j, rh);
+      tc_ld_32x32b_x16(ta + TP + 16 * j, rl);
+      tc_wait_ld();
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        y[16 * j + t] = fmaf(sc, fmaf(-cz, X[16 * j + t], __uint_as_float(rh[t]) + __uint_as_float(rl[t])), y[16 * j + t]);
+    }
+  }
+  tc_fence_before();  // the TMEM reads before the next MMA into this accumulator
+}
+
+// The MMA warp: for every W4 unit of the CTA (in the consumers' order), wait
+// for its A operand, issue 2 groups x 8 MMAs (K 16 each; the first MMA of a
+// group overwrites its accumulator), commit to mdone.  Stops on slot == 0.
+template <int NT>
+__device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc) {
+  const StepArgs& a = *ap;
+  constexpr int N = 16 * NT;
+  constexpr uint32_t idesc = idesc_f16(128, N);
+  for (int k = 0;; ++k) {
+    const int b = k & 1;
+    where(a, WCODE(k & 0xFFFF, 0x20, 1));
+    mbar_wait_wd(tc.ardy0 + 8 * b, (uint32_t)((k >> 1) & 1));
+    if (a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2] = clk64();
+    __syncwarp();
+    const uint32_t sst = *reinterpret_cast<volatile uint32_t*>(tc.slot + b);
+    if (sst == 0) break;
+    tc_fence_after();
+    const uint64_t bd0 = smem_desc(sst + kW4UnitBytes, N * 16, 128);
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const uint32_t d = tc.tbase + kAccCol + (uint32_t)((b * 2 + g) * N);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int i = g * 8 + ks;
+        const uint32_t at = tc.tbase + (uint32_t)(b * 128 + i * 8);
+        const uint64_t bd = bd0 + (uint64_t)((i * 2 * N * 16) >> 4);
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+            "r"(at), "l"(bd), "r"(idesc), "r"(ks))
+            ;
       }
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const uint32_t zb = lds8(sst + o_z + i * 16 + grp * 8), sp = lds32(sst + o_sc + i * 64 + grp * 32);
-    const float c0 = __uint_as_float(0x44800000u | ((zb & 15u) << 13));
-    const float c8 = __uint_as_float(0x44800000u | ((zb >> 4) << 17));
-    const float s0 = __uint_as_float(sp << 16);
-    const float s8 = __uint_as_float(sp & 0xFFFF0000u) * 0.0625f;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const float2 X = lds64f(sst + o_x + (grp * 8 * NT + n * 8) * 4);
-      float* ac = i ? acc1[n] : acc[n];
-      ac[0] = fmaf(s0, fmaf(-c0, X.x, cg[i][n][0]), ac[0]);
-      ac[1] = fmaf(s0, fmaf(-c0, X.y, cg[i][n][1]), ac[1]);
-      ac[2] = fmaf(s8, fmaf(-c8, X.x, cg[i][n][2]), ac[2]);
-      ac[3] = fmaf(s8, fmaf(-c8, X.y, cg[i][n][3]), ac[3]);
     }
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(tc.mdone0 + 8 * b)
+        : "memory");
+    if (a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2 + 1] = clk64();
   }
 }
 
@@ -588,12 +809,19 @@ SS_DEV void resid_update(const StepArgs& a, int tg, const float* acc, int T, int
     uint32_t d1[kMaxPeers], d2[kMaxPeers];
     unsigned ready = 0;
     const unsigned all = (1u << a.P) - 1u;
-    long spins = 0;
+    unsigned spins = 0;
+    unsigned long long tw = 0;
     while (ready != all) {
 #pragma unroll
       for (int p = 0; p < kMaxPeers; ++p)
         if (p < a.P && !(ready & (1u << p)) && ll_try_load(src0 + p * pstride, flag, d1[p], d2[p])) ready |= 1u << p;
-      if (++spins > (1L << 24)) { a.st->timeout = 1; break; }
+      if ((++spins & 255u) == 0) {  // bounded: 2 s per line, or at once after another timeout
+        if (!tw) tw = now_ns();
+        if (now_ns() - tw > 2000000000ull || *reinterpret_cast<volatile int*>(&a.st->timeout)) {
+          a.st->timeout = 1;
+          break;
+        }
+      }
     }
     float s0 = 0.f, s1 = 0.f;
 #pragma unroll
@@ -668,8 +896,8 @@ SS_DEV void epi_argmax(const StepArgs& a, int tg, const float* acc, int T) {
 // (red.add), count arrivals, run the epilogues of the tile-groups completed
 // here.  Returns the number of tile-groups this CTA finalised.
 template <int NT, int PH>
-__device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sched* __restrict__ sp, int layer,
-                                       int u0, int u1, Ring ring, int* s_done, int* s_nd) {
+__device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const Sched* __restrict__ sp, int layer,
+                                        int u0, int u1, Ring ring, Tc tc, int tck, int* s_done, int* s_nd) {
   const StepArgs& a = *ap;
   const Sched& s = *sp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -680,19 +908,20 @@ __device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sc
   float* accb = a.acc[ai];
   int* arr = a.arr[ai];
   const int T = s.T;
-  float acc[NT][4], acc1[NT][4];
+  const int tslot = PH == PH_LM ? a.n_layers * 5 : layer * 5 + PH;
+  tmark(a, tslot, 0);
+  where(a, WCODE(layer, PH, 1));
+  if constexpr (PH == PH_LM) {
+    float acc[NT][4];
 #pragma unroll
-  for (int n = 0; n < NT; ++n)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[n][e] = acc1[n][e] = 0.f;
-  for (int u = u0; u < u1; ++u) {
-    const uint32_t sst = ring_wait<NT>(ring);
-    if constexpr (PH == PH_LM) lm_unit<NT>(sst, warp, lane, acc);
-    else w4_unit<NT>(sst, warp, lane, acc, acc1);
-    ring_release<NT>(ring);
-    const int tg = u / S;
-    if (u + 1 == u1 || (u + 1) / S != tg) {  // flush this tile-group's partial
-      if constexpr (PH == PH_LM) {
+    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+    for (int u = u0; u < u1; ++u) {
+      const uint32_t sst = ring_wait<NT>(ring);
+      if (u == u0) tmark(a, tslot, 1);
+      lm_unit<NT>(sst, warp, lane, acc);
+      ring_release<NT>(ring);
+      const int tg = u / S;
+      if (u + 1 == u1 || (u + 1) / S != tg) {  // flush this tile-group's partial
         float* base = accb + ((size_t)tg * 128 + warp * 16 + gq) * TP;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
@@ -700,20 +929,57 @@ __device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sc
           red_add_v2(base + 8 * TP + n * 8 + 2 * tq, acc[n][2], acc[n][3]);
           acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
         }
-      } else {
-        float* base = accb + ((size_t)tg * 128 + 2 * (warp & 3) * 16 + gq) * TP;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          red_add_v2(base + n * 8 + 2 * tq, acc[n][0], acc[n][1]);
-          red_add_v2(base + 8 * TP + n * 8 + 2 * tq, acc[n][2], acc[n][3]);
-          red_add_v2(base + 16 * TP + n * 8 + 2 * tq, acc1[n][0], acc1[n][1]);
-          red_add_v2(base + 24 * TP + n * 8 + 2 * tq, acc1[n][2], acc1[n][3]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[n][e] = acc1[n][e] = 0.f;
-        }
       }
     }
+  } else {
+    // software pipeline: dequant unit u into TMEM buffer (tck + u - u0) & 1
+    // while the MMAs of unit u - 1 run, then its epilogue; flush per tile-group
+    float y[8 * NT];
+#pragma unroll
+    for (int t = 0; t < 8 * NT; ++t) y[t] = 0.f;
+    const int k0 = ring.k;
+    uint32_t prev = 0;
+    unsigned long long* utl =
+        (a.utl && PH == PH_GU && layer == a.n_layers / 2 && blockIdx.x == 0 && threadIdx.x == 0) ? a.utl : nullptr;
+    if (utl) { utl[127 * 8 + 7] = (unsigned long long)tck; utl[127 * 8 + 6] = (unsigned long long)(u1 - u0); }
+    // per iteration: the TMEM stores of unit u are issued, then the epilogue of
+    // unit u - 1 runs while they drain, then unit u is handed to the MMA warp
+    for (int u = u0; u <= u1; ++u) {
+      uint32_t sst = 0;
+      if (u < u1) {
+        if (utl && u - u0 < 127) utl[(u - u0) * 8 + 0] = clk64();
+        sst = ring_wait_at<NT>(ring, k0 + (u - u0));
+        if (utl && u - u0 < 127) utl[(u - u0) * 8 + 1] = clk64();
+        if (u == u0) tmark(a, tslot, 1);
+        tc_dequant<NT>(tc, sst, (tck + (u - u0)) & 1, warp, lane);
+        if (utl && u - u0 < 127) utl[(u - u0) * 8 + 2] = clk64();
+      }
+      if (u > u0) {
+        const int v = u - 1;
+        where(a, WCODE(layer, PH, 3));
+        tc_epilogue<NT>(tc, prev, tck + (v - u0), warp, lane, y);
+        if (utl && v - u0 < 127) utl[(v - u0) * 8 + 3] = clk64();
+      }
+      if (u < u1) tc_signal(tc, sst, (tck + (u - u0)) & 1, warp, lane);
+      if (u > u0) {
+        const int v = u - 1;
+        ring_release_at<NT>(ring, k0 + (v - u0));
+        const int tg = v / S;
+        if (v + 1 == u1 || (v + 1) / S != tg) {  // flush: row 32 qd + lane, group half of the warp
+          float* row = accb + ((size_t)tg * 128 + 32 * (warp & 3) + lane) * TP;
+#pragma unroll
+          for (int t = 0; t < 8 * NT; t += 4) {
+            red_add_v4(row + t, y[t], y[t + 1], y[t + 2], y[t + 3]);
+            y[t] = y[t + 1] = y[t + 2] = y[t + 3] = 0.f;
+          }
+        }
+      }
+      prev = sst;
+    }
+    ring.k = k0 + (u1 - u0);
+    tck += u1 - u0;
   }
+  where(a, WCODE(layer, PH, 4));
   // arrivals: the barrier orders every warp's reductions before thread 0's
   // GPU-scope fence (cumulative) and arrival counts
   cbar();
@@ -729,9 +995,13 @@ __device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sc
     }
     *s_nd = nd;
   }
+  __syncwarp();
   cbar();
   const int nd = *s_nd;
-  if (nd == 0) return ring.k;
+  if (nd == 0) {
+    tmark(a, tslot, 2);
+    return make_int2(ring.k, tck);
+  }
   int* ctr = a.ctr + (size_t)layer * kCtrPerLayer;
   if constexpr (PH == PH_QKV || PH == PH_GU || PH == PH_LM) {
     for (int i = 0; i < nd; ++i) {
@@ -745,9 +1015,12 @@ __device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sc
     // residual phases: sends of every completed tile-group first, then the
     // receives (no rank waits on a tile-group it has not sent yet)
     const int ar_seq = 2 * layer + (PH == PH_DN ? 1 : 0);
+    where(a, WCODE(layer, PH, 6));
     if (a.P > 1)
       for (int i = 0; i < nd; ++i) ar_send<NT>(a, s_done[i], accb + (size_t)s_done[i] * 128 * TP, T, ar_seq);
+    where(a, WCODE(layer, PH, 7));
     for (int i = 0; i < nd; ++i) resid_update<NT>(a, s_done[i], accb + (size_t)s_done[i] * 128 * TP, T, ar_seq);
+    where(a, WCODE(layer, PH, 8));
     cbar();
     const bool last = PH == PH_DN && layer + 1 == a.n_layers;
     const uint16_t* gain = PH == PH_O ? a.layers[layer].mlp_norm
@@ -778,6 +1051,7 @@ __device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sc
       int* lmc = a.ctr + (size_t)a.n_layers * kCtrPerLayer;
       if (atomicAdd(lmc, nd) + nd == a.lm_tg) {
         fence_acq_rel_gpu();
+        where(a, WCODE(layer, PH, 0x10));
         if (a.P > 1) {
           const ArgmaxXArgs x{a.P, a.rank, a.loopback, 2 * a.n_layers, a.h / 128, a.recv, a.peer_recv};
           argmax_exchange(x, a.st);
@@ -789,28 +1063,32 @@ __device__ __noinline__ int gemm_phase(const StepArgs* __restrict__ ap, const Sc
       red_release_gpu_add(ctr + ci, nd);
     }
   }
-  return ring.k;
+  __syncwarp();
+  tmark(a, tslot, 2);
+  where(a, WCODE(layer, PH, 9));
+  return make_int2(ring.k, tck);
 }
 
 // Tree-masked attention (a5, R11) of one work item: (kv head,
-// 64-row chunk z, key split).  Warp w = (row block rb = w % 4, half h = w / 4):
-// it computes the scores of its 16 query rows against key half h of every
-// tile (q hi + lo fragments from global memory -- written by the QKV epilogue,
-// L1-resident -- times the K tile in the ring; tree tiles add q_hi K_lo),
-// the warp pair (rb, 0) / (rb, 1) exchanges row maxima and the fp16
-// probabilities P through shared memory, then each warp accumulates O for
-// d-half h over ALL keys of the tile (P V_hi + P V_lo on tree tiles): no
-// duplicated MMAs and a 16 x d/2 fp32 accumulator per warp.  The split's
-// unnormalised partial goes to the workspace; after the splits of the group
-// meet, each merges a slice of the rows by log-sum-exp into the O input.
+// 64-row chunk z, key split).  Two tile streams: warps 0-3 take the item's
+// even tiles, warps 4-7 the odd ones; warp (stream, rb) owns query rows
+// rb*16 .. rb*16+15 of the chunk over ALL keys of its tiles, so the scores
+// stay in registers: S = q K^T (q hi + lo fragments from global / L1 -- the
+// QKV epilogue wrote them -- times the K tile from the ring; tree tiles add
+// q_hi K_lo), online softmax on the S fragments, P (fp16) reused in place as
+// the A fragments of O += P V (+ P V_lo on tree tiles).  No shared-memory P
+// exchange, no barriers inside the tile loop.  Each stream's unnormalised
+// partial (m, l, O) goes to the workspace (2 partials per item); after the
+// group's items meet, the 2S partials are merged by log-sum-exp, several
+// warps per output row.
 template <int NT, int D>
-__device__ __noinline__ int attn_item(const StepArgs* __restrict__ ap, const Sched* __restrict__ sp, int layer,
-                                      Ring ring, float* s_rmax, uint16_t* s_p) {
+__device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const Sched* __restrict__ sp, int layer,
+                                      Ring ring, float* s_merge, uint8_t* s_q) {
   const StepArgs& a = *ap;
   const Sched& s = *sp;
-  constexpr int KT = 4096 / D, KH = KT / 2, NTK = KH / 8, DH = D / 2;
+  constexpr int KT = 4096 / D, NB = KT / 8, DB = D / 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rb = warp & 3, kh = warp >> 2;
+  const int rb = warp & 3, ws = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
   const int b = s.att_item;
   const int grp = b / s.att_S, split = b % s.att_S;
@@ -820,7 +1098,18 @@ __device__ __noinline__ int attn_item(const StepArgs* __restrict__ ap, const Sch
   const int rbmax = 4 * G;
   const size_t qlo = (size_t)a.Hkv_l * rbmax * (D / 16) * 32 * 8;
   int* ctr = a.ctr + (size_t)layer * kCtrPerLayer;
+  tmark(a, layer * 5 + PH_ATT, 0);
+  where(a, WCODE(layer, PH_ATT, 1));
+  unsigned long long* atl =
+      (a.utl && layer == a.n_layers / 2 && blockIdx.x == 0 && threadIdx.x == 0) ? a.utl + 28672 : nullptr;
+  if (atl) atl[0] = clk64();
+  if (threadIdx.x == 0) {
+    reinterpret_cast<volatile int*>(s_merge)[0] = ring.k - 1;
+    reinterpret_cast<volatile int*>(s_merge)[1] = ring.k - 1;
+  }
   wait_counter(ctr + C_QKV, a.qkv_tg);  // q, tree rows and their lo parts are written
+  if (atl) atl[1] = clk64();
+  where(a, WCODE(layer, PH_ATT, 2));
   const DevState* st = a.st;
   const int rbg = z * 4 + rb;
   const int ra = rb * 16 + gq, rbr = ra + 8;  // rows within the chunk
@@ -829,162 +1118,183 @@ __device__ __noinline__ int attn_item(const StepArgs* __restrict__ ap, const Sch
   const unsigned long long ancA = st->anc[tokA], ancB = st->anc[tokB];
   const bool okA = rowA < Mrows, okB = rowB < Mrows;
   const float sl2 = rsqrtf((float)D) * 1.4426950408889634f;
-  const uint4* qh = reinterpret_cast<const uint4*>(a.qf) + (((size_t)kvh * rbmax + rbg) * (D / 16)) * 32 + lane;
-  const uint4* ql = reinterpret_cast<const uint4*>(a.qf + qlo) + (((size_t)kvh * rbmax + rbg) * (D / 16)) * 32 + lane;
-  const int pair_bar = 2 + rb;                 // named barrier of warps rb and rb + 4
-  const uint32_t spb = smem_u32(s_p);           // P [64 rows][KT keys] fp16, 16-byte chunks swizzled by row
+  // the chunk's q fragments (4 row blocks x d/16 k-steps x 32 lanes x 16 B,
+  // hi then lo) -> shared memory once; the tile loop reads them with LDS
+  // (from global they were L2 round trips every tile: the ring leaves ~30 KB of L1)
+  {
+    constexpr int NQ = 4 * (D / 16) * 32;  // uint4 per part
+    const uint4* gh = reinterpret_cast<const uint4*>(a.qf) + ((size_t)kvh * rbmax + z * 4) * (D / 16) * 32;
+    const uint4* gl = reinterpret_cast<const uint4*>(a.qf + qlo) + ((size_t)kvh * rbmax + z * 4) * (D / 16) * 32;
+    uint4* sq = reinterpret_cast<uint4*>(s_q);
+    for (int i = threadIdx.x; i < NQ; i += 256) {
+      sq[i] = __ldcg(gh + i);
+      sq[NQ + i] = __ldcg(gl + i);
+    }
+    cbar();
+  }
+  const uint32_t qh = smem_u32(s_q) + (uint32_t)((rb * (D / 16)) * 32 + lane) * 16;
+  const uint32_t ql = qh + (uint32_t)(4 * (D / 16) * 32) * 16;
+  // ring position of tile it: one unit per tile, two for a tree tile (hi, lo)
+  const int t0 = s.att_t0, t1 = s.att_t1, ft = L / KT, k0 = ring.k;
+  auto ring_of = [&](int it) { return k0 + (it - t0) + max(0, it - max(t0, ft)); };
   float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
-  float o[DH / 8][4];
+  float o[DB][4];
 #pragma unroll
-  for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  const int kofs = kh * KH;
-  for (int it = s.att_t0; it < s.att_t1; ++it) {
-    const bool tree = tile_is_tree(s, it);
-    const uint32_t shi = ring_wait<NT>(ring);
-    Ring r2 = ring;
-    ++r2.k;
-    const uint32_t slo = tree ? ring_wait<NT>(r2) : shi;
-    float sc[NTK][4];
+  for (int n = 0; n < DB; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  // Each stream publishes the last ring index it has waited for; a stream may
+  // wait for index k only once the other stream has waited for k - STAGES
+  // (the slot's previous use): mbarrier parity waits must never run a full
+  // ring round ahead of the slot's phase.
+  volatile int* prog = reinterpret_cast<volatile int*>(s_merge);
+  constexpr int STG = StepCfg<NT>::STAGES;
+  for (int it = t0 + ws; it < t1; it += 2) {
+    const bool tree = it >= ft;
+    const int ri = ring_of(it);
+    if (lane == 0)
+      while (prog[ws ^ 1] < ri + (tree ? 1 : 0) - STG) __nanosleep(20);
+    __syncwarp();
+    const uint32_t shi = ring_wait_at<NT>(ring, ri);
+    const uint32_t slo = tree ? ring_wait_at<NT>(ring, ri + 1) : shi;
+    if (rb == 0 && lane == 0) prog[ws] = ri + (tree ? 1 : 0);
+    if (atl && it - t0 < 64) atl[16 + (it - t0) * 2] = clk64();
+    // S = q K^T: the k16 chains alternate between two accumulator sets
+    float sc[1][NB][4];
 #pragma unroll
-    for (int n = 0; n < NTK; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+    for (int n = 0; n < NB; ++n) sc[0][n][0] = sc[0][n][1] = sc[0][n][2] = sc[0][n][3] = 0.f;
 #pragma unroll 2
     for (int kk = 0; kk < D / 16; ++kk) {
-      const uint4 fh = qh[kk * 32], fl = ql[kk * 32];
+      const uint4 fh = lds128(qh + kk * 512), fl = lds128(ql + kk * 512);
       const uint32_t ah[4] = {fh.x, fh.y, fh.z, fh.w}, al[4] = {fl.x, fl.y, fl.z, fl.w};
+      float(&sk)[NB][4] = sc[0];
 #pragma unroll
-      for (int np = 0; np < NTK / 2; ++np) {
-        const int key = kofs + np * 16 + (lane & 7) + ((lane >> 4) << 3);
+      for (int np = 0; np < NB / 2; ++np) {
+        const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
         const int ch = kk * 2 + ((lane >> 3) & 1);
         const uint32_t koff = (uint32_t)(key * D + ((ch ^ (key & 7)) << 3)) * 2;
         uint32_t kb[4];
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                      : "=r"(kb[0]), "=r"(kb[1]), "=r"(kb[2]), "=r"(kb[3]) : "r"(shi + koff));
-        mma_f16_16816(sc[2 * np], ah, kb[0], kb[1]);
-        mma_f16_16816(sc[2 * np + 1], ah, kb[2], kb[3]);
-        mma_f16_16816(sc[2 * np], al, kb[0], kb[1]);
-        mma_f16_16816(sc[2 * np + 1], al, kb[2], kb[3]);
+        mma_f16_16816(sk[2 * np], ah, kb[0], kb[1]);
+        mma_f16_16816(sk[2 * np + 1], ah, kb[2], kb[3]);
+        mma_f16_16816(sk[2 * np], al, kb[0], kb[1]);
+        mma_f16_16816(sk[2 * np + 1], al, kb[2], kb[3]);
         if (tree) {
           asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                        : "=r"(kb[0]), "=r"(kb[1]), "=r"(kb[2]), "=r"(kb[3]) : "r"(slo + koff));
-          mma_f16_16816(sc[2 * np], ah, kb[0], kb[1]);
-          mma_f16_16816(sc[2 * np + 1], ah, kb[2], kb[3]);
+          mma_f16_16816(sk[2 * np], ah, kb[0], kb[1]);
+          mma_f16_16816(sk[2 * np + 1], ah, kb[2], kb[3]);
         }
       }
     }
-    // mask: prefix always visible; tree rows by ancestor bit; beyond L+T never
-    const int kbase = it * KT + kofs;
+    if (atl && it - t0 < 8) atl[200 + (it - t0) * 4] = clk64();
+    // mask (prefix always visible; tree keys by ancestor bit; beyond L + T
+    // never), scale, tile row maxima over the quad
+    const int kbase = it * KT;
     float mxA = -INFINITY, mxB = -INFINITY;
 #pragma unroll
-    for (int n = 0; n < NTK; ++n)
+    for (int n = 0; n < NB; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int key = kbase + n * 8 + 2 * tq + (e & 1);
         const unsigned long long anc = (e < 2) ? ancA : ancB;
         const bool ok = (e < 2) ? okA : okB;
         const bool vis = ok && (key < L || (key < L + T && ((anc >> (key - L)) & 1ull)));
-        const float v = vis ? sc[n][e] * sl2 : -INFINITY;
-        sc[n][e] = v;
+        const float v = vis ? sc[0][n][e] * sl2 : -INFINITY;
+        sc[0][n][e] = v;
         if (e < 2) mxA = fmaxf(mxA, v); else mxB = fmaxf(mxB, v);
       }
     mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 1));
     mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 2));
     mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 1));
     mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 2));
-    // the pair's row maxima over the whole tile (both warps then hold the same running max)
-    if (tq == 0) {
-      s_rmax[kh * 64 + ra] = mxA;
-      s_rmax[kh * 64 + rbr] = mxB;
-    }
-    named_bar_sync(pair_bar, 64);
-    mxA = fmaxf(mxA, s_rmax[(kh ^ 1) * 64 + ra]);
-    mxB = fmaxf(mxB, s_rmax[(kh ^ 1) * 64 + rbr]);
     const float mnA = fmaxf(mA, mxA), mnB = fmaxf(mB, mxB);
     const float uA = (mnA == -INFINITY) ? 0.f : mnA, uB = (mnB == -INFINITY) ? 0.f : mnB;
     const float alA = exp2f(mA - uA), alB = exp2f(mB - uB);
-    float sumA = 0.f, sumB = 0.f;
-#pragma unroll
-    for (int n = 0; n < NTK; ++n) {
-      const float p0 = exp2f(sc[n][0] - uA), p1 = exp2f(sc[n][1] - uA);
-      const float p2 = exp2f(sc[n][2] - uB), p3 = exp2f(sc[n][3] - uB);
-      sumA += p0 + p1;
-      sumB += p2 + p3;
-      // P[row][key] fp16: row-major KT keys, 16-byte chunk index XOR row % 8
-      const int key = kofs + n * 8 + 2 * tq;
-      const uint32_t offA = (uint32_t)(ra * KT + ((((key >> 3) ^ (ra & 7))) << 3) + (key & 7)) * 2;
-      const uint32_t offB = (uint32_t)(rbr * KT + ((((key >> 3) ^ (rbr & 7))) << 3) + (key & 7)) * 2;
-      asm volatile("st.shared.b32 [%0], %1;" ::"r"(spb + offA), "r"(pack_half2(p0, p1)) : "memory");
-      asm volatile("st.shared.b32 [%0], %1;" ::"r"(spb + offB), "r"(pack_half2(p2, p3)) : "memory");
-    }
-    sumA += __shfl_xor_sync(0xffffffffu, sumA, 1);
-    sumA += __shfl_xor_sync(0xffffffffu, sumA, 2);
-    sumB += __shfl_xor_sync(0xffffffffu, sumB, 1);
-    sumB += __shfl_xor_sync(0xffffffffu, sumB, 2);
-    lA = lA * alA + sumA;  // this warp's keys only; the two halves are added at the end
-    lB = lB * alB + sumB;
     mA = mnA;
     mB = mnB;
+    // P = exp2(s - m) as fp16 A fragments (the C fragments of n-blocks 2j, 2j+1
+    // are the A fragment of keys 16j .. 16j+15)
+    uint32_t pf[NB / 2][4];
+    float sumA = 0.f, sumB = 0.f;
+#pragma unroll
+    for (int j = 0; j < NB / 2; ++j) {
+      const float p00 = exp2f(sc[0][2 * j][0] - uA), p01 = exp2f(sc[0][2 * j][1] - uA);
+      const float p02 = exp2f(sc[0][2 * j][2] - uB), p03 = exp2f(sc[0][2 * j][3] - uB);
+      const float p10 = exp2f(sc[0][2 * j + 1][0] - uA), p11 = exp2f(sc[0][2 * j + 1][1] - uA);
+      const float p12 = exp2f(sc[0][2 * j + 1][2] - uB), p13 = exp2f(sc[0][2 * j + 1][3] - uB);
+      sumA += (p00 + p01) + (p10 + p11);
+      sumB += (p02 + p03) + (p12 + p13);
+      pf[j][0] = pack_half2(p00, p01);
+      pf[j][1] = pack_half2(p02, p03);
+      pf[j][2] = pack_half2(p10, p11);
+      pf[j][3] = pack_half2(p12, p13);
+    }
+    lA = lA * alA + sumA;  // this thread's keys; the quad is summed at the end
+    lB = lB * alB + sumB;
     if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {
 #pragma unroll
-      for (int n = 0; n < DH / 8; ++n) {
+      for (int n = 0; n < DB; ++n) {
         o[n][0] *= alA; o[n][1] *= alA; o[n][2] *= alB; o[n][3] *= alB;
       }
     }
-    named_bar_sync(pair_bar, 64);  // P of both key halves is in shared memory
+    if (atl && it - t0 < 8) atl[200 + (it - t0) * 4 + 1] = clk64();
+    // O += P V (V hi; tree tiles also V lo)
     const uint32_t vh = shi + KT * D * 2, vl = slo + KT * D * 2;
 #pragma unroll
-    for (int kk = 0; kk < KT / 16; ++kk) {
-      uint32_t pa[4];
-      {  // A fragment of P: rows rb*16.., keys kk*16..
-        const int prow = rb * 16 + (lane & 15);
-        const int ch = kk * 2 + (lane >> 4);
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(pa[0]), "=r"(pa[1]), "=r"(pa[2]), "=r"(pa[3])
-                     
-                     : "r"(spb + (uint32_t)(prow * KT + ((ch ^ (prow & 7)) << 3)) * 2));
-      }
+    for (int j = 0; j < NB / 2; ++j) {
 #pragma unroll
-      for (int dp = 0; dp < DH / 16; ++dp) {
-        const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
-        const int ch = (kh * DH) / 8 + dp * 2 + (lane >> 4);
+      for (int dp = 0; dp < D / 16; ++dp) {
+        const int key = j * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int ch = dp * 2 + (lane >> 4);
         const uint32_t voff = (uint32_t)(key * D + ((ch ^ (key & 7)) << 3)) * 2;
         uint32_t vb[4];
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                      : "=r"(vb[0]), "=r"(vb[1]), "=r"(vb[2]), "=r"(vb[3]) : "r"(vh + voff));
-        mma_f16_16816(o[2 * dp], pa, vb[0], vb[1]);
-        mma_f16_16816(o[2 * dp + 1], pa, vb[2], vb[3]);
+        mma_f16_16816(o[2 * dp], pf[j], vb[0], vb[1]);
+        mma_f16_16816(o[2 * dp + 1], pf[j], vb[2], vb[3]);
         if (tree) {
           asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                        : "=r"(vb[0]), "=r"(vb[1]), "=r"(vb[2]), "=r"(vb[3]) : "r"(vl + voff));
-          mma_f16_16816(o[2 * dp], pa, vb[0], vb[1]);
-          mma_f16_16816(o[2 * dp + 1], pa, vb[2], vb[3]);
+          mma_f16_16816(o[2 * dp], pf[j], vb[0], vb[1]);
+          mma_f16_16816(o[2 * dp + 1], pf[j], vb[2], vb[3]);
         }
       }
     }
-    ring_release<NT>(ring);
-    if (tree) ring_release<NT>(ring);
-    named_bar_sync(pair_bar, 64);  // P reads done before the next tile's P writes
+    if (atl && it - t0 < 8) atl[200 + (it - t0) * 4 + 2] = clk64();
+    // this stream's 4 warps read each unit: 2 arrivals each (empty count 8)
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(ring.empty0 + 8 * (ri % StepCfg<NT>::STAGES))
+                   : "memory");
+      if (tree)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(ring.empty0 + 8 * ((ri + 1) % StepCfg<NT>::STAGES))
+                     : "memory");
+    }
+    if (atl && it - t0 < 64) atl[16 + (it - t0) * 2 + 1] = clk64();
   }
-  // the split's partial -> workspace: O (this warp's rows x d-half) and (m, l)
-  // with l summed over the two key halves
+  if (rb == 0 && lane == 0) prog[ws] = 0x7FFFFFFF;  // this stream is done with the ring
+  // this stream's partial -> workspace: O (16 rows x D per warp) and (m, l)
   {
-    float* ws = a.att_ws + (size_t)b * 64 * D;
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+    const size_t pidx = (size_t)b * 2 + ws;
+    float* wsp = a.att_ws + pidx * 64 * D;
 #pragma unroll
-    for (int n = 0; n < DH / 8; ++n) {
-      const int c = kh * DH + n * 8 + 2 * tq;
-      *reinterpret_cast<float2*>(ws + (size_t)ra * D + c) = make_float2(o[n][0], o[n][1]);
-      *reinterpret_cast<float2*>(ws + (size_t)rbr * D + c) = make_float2(o[n][2], o[n][3]);
+    for (int n = 0; n < DB; ++n) {
+      const int c = n * 8 + 2 * tq;
+      *reinterpret_cast<float2*>(wsp + (size_t)ra * D + c) = make_float2(o[n][0], o[n][1]);
+      *reinterpret_cast<float2*>(wsp + (size_t)rbr * D + c) = make_float2(o[n][2], o[n][3]);
     }
-    if (kh == 1 && tq == 0) {
-      s_rmax[ra] = lA;
-      s_rmax[rbr] = lB;
-    }
-    named_bar_sync(pair_bar, 64);
-    if (kh == 0 && tq == 0) {
-      a.att_ml[(size_t)b * 64 + ra] = make_float2(mA, lA + s_rmax[ra]);
-      a.att_ml[(size_t)b * 64 + rbr] = make_float2(mB, lB + s_rmax[rbr]);
+    if (tq == 0) {
+      a.att_ml[pidx * 64 + ra] = make_float2(mA, lA);
+      a.att_ml[pidx * 64 + rbr] = make_float2(mB, lB);
     }
   }
   // meet the other splits of this (kv head, row chunk)
+  where(a, WCODE(layer, PH_ATT, 4));
+  if (atl) atl[2] = clk64();
   cbar();
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
@@ -992,96 +1302,209 @@ __device__ __noinline__ int attn_item(const StepArgs* __restrict__ ap, const Sch
     spin_until_geq(ctr + C_MEET + grp, s.att_S);
   }
   cbar();
-  // merge a slice of the row groups (one 128-wide group of the O input: one
-  // head at d = 128, two at d = 64) across the S partials, R11 log-sum-exp
+  if (atl) atl[3] = clk64();
+  // merge this item's slice of the row groups (one 128-wide group of the O
+  // input: one head at d = 128, two at d = 64) over the group's 2S partials:
+  // W warps per row group, each summing every W-th partial, then combined
+  // through shared memory (R11 log-sum-exp)
   constexpr int RPG = 128 / D;             // rows per group
   constexpr int NRG = 64 / RPG;
   const int rg0 = split * NRG / s.att_S, rg1 = (split + 1) * NRG / s.att_S;
-  for (int rg = rg0 + warp; rg < rg1; rg += 8) {
+  const int nrg = rg1 - rg0;
+  const int P2 = 2 * s.att_S;
+  const size_t pb0 = (size_t)grp * P2;
+  const int W = nrg > 0 ? max(1, 8 / nrg) : 1;
+  for (int base = 0; base < nrg; base += 8 / W) {
+    const int rgl = base + warp / W, sub = warp % W;
+    const bool act = rgl < nrg && warp / W < 8 / W;
+    const int rg = rg0 + rgl;
     const int rr = rg * RPG + (RPG == 2 ? (lane >> 4) : 0);  // row within the chunk
     const int c4 = (RPG == 2 ? (lane & 15) : lane) * 4;       // 4 columns
-    const int m = z * 64 + rr;
-    const bool valid = m < Mrows;
-    float mx = -INFINITY;
-    for (int p = 0; p < s.att_S; ++p)
-      mx = fmaxf(mx, __ldcg(&a.att_ml[((size_t)grp * s.att_S + p) * 64 + rr].x));
-    float l = 0.f;
+    float mx = -INFINITY, l = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int p = 0; p < s.att_S; ++p) {
-      const size_t pb = (size_t)grp * s.att_S + p;
-      const float2 v = __ldcg(&a.att_ml[pb * 64 + rr]);
-      const float w = (v.x == -INFINITY) ? 0.f : exp2f(v.x - mx);
-      l += w * v.y;
-      const float4 ov = __ldcg(reinterpret_cast<const float4*>(a.att_ws + (pb * 64 + rr) * D + c4));
-      acc.x += w * ov.x;
-      acc.y += w * ov.y;
-      acc.z += w * ov.z;
-      acc.w += w * ov.w;
+    if (act) {
+      for (int p0 = sub; p0 < P2; p0 += 4 * W) {
+        float m8[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m8[j] = p0 + j * W < P2 ? __ldcg(&a.att_ml[(pb0 + p0 + j * W) * 64 + rr].x) : -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mx = fmaxf(mx, m8[j]);
+      }
+      for (int p0 = sub; p0 < P2; p0 += 4 * W) {
+        float2 v8[4];
+        float4 o8[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (p0 + j * W < P2) {
+            const size_t pp = pb0 + p0 + j * W;
+            v8[j] = __ldcg(&a.att_ml[pp * 64 + rr]);
+            o8[j] = __ldcg(reinterpret_cast<const float4*>(a.att_ws + (pp * 64 + rr) * D + c4));
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (p0 + j * W < P2) {
+            const float w = (v8[j].x == -INFINITY) ? 0.f : exp2f(v8[j].x - mx);
+            l += w * v8[j].y;
+            acc.x += w * o8[j].x;
+            acc.y += w * o8[j].y;
+            acc.z += w * o8[j].z;
+            acc.w += w * o8[j].w;
+          }
+      }
+      if (W > 1) {
+        float* sm = s_merge + warp * 132;
+        *reinterpret_cast<float4*>(sm + lane * 4) = acc;
+        if ((lane & 15) == 0) {
+          sm[128 + (lane >> 4) * 2] = mx;
+          sm[129 + (lane >> 4) * 2] = l;
+        }
+      }
     }
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-    const int t = m / G, hq = kvh * G + (m % G);
-    const int k = hq * D + c4;
-    uint32_t h01, l01, h23, l23;
-    float xs = split16(acc.x, acc.y, h01, l01) + split16(acc.z, acc.w, h23, l23);
-    if (valid) {
-      *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k, NT, 0)) = h01;
-      *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k + 2, NT, 0)) = h23;
-      *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k, NT, 1)) = l01;
-      *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k + 2, NT, 1)) = l23;
+    if (W > 1) cbar();
+    if (act && sub == 0) {
+      if (W > 1) {  // combine the W warps of this row group
+        float M = -INFINITY;
+        const int half = RPG == 2 ? (lane >> 4) : 0;
+        for (int v = 0; v < W; ++v) M = fmaxf(M, s_merge[(warp + v) * 132 + 128 + half * 2]);
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        float lt = 0.f;
+        for (int v = 0; v < W; ++v) {
+          const float* sm = s_merge + (warp + v) * 132;
+          const float mv = sm[128 + half * 2];
+          const float w = (mv == -INFINITY) ? 0.f : exp2f(mv - M);
+          lt += w * sm[129 + half * 2];
+          const float4 q4 = *reinterpret_cast<const float4*>(sm + lane * 4);
+          t.x += w * q4.x; t.y += w * q4.y; t.z += w * q4.z; t.w += w * q4.w;
+        }
+        acc = t;
+        l = lt;
+      }
+      const int m = z * 64 + rr;
+      const bool valid = m < Mrows;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      const int t = m / G, hq = kvh * G + (m % G);
+      const int k = hq * D + c4;
+      uint32_t h01, l01, h23, l23;
+      float xs = split16(acc.x, acc.y, h01, l01) + split16(acc.z, acc.w, h23, l23);
+      if (valid) {
+        *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k, NT, 0)) = h01;
+        *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k + 2, NT, 0)) = h23;
+        *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k, NT, 1)) = l01;
+        *reinterpret_cast<uint32_t*>(a.act_o + a2_frag(t, k + 2, NT, 1)) = l23;
+      }
+      // the warp's columns are exactly one 128-group of one token (at d = 64
+      // the two rows are consecutive heads of the same token: G is even)
+      xs = warp_sum(valid ? xs : 0.f);
+      if (lane == 0 && valid) *reinterpret_cast<float*>(a.act_o + a2_xsum(t, k >> 7, NT)) = xs;
     }
-    xs = warp_sum(valid ? xs : 0.f);
-    if (lane == 0 && valid) *reinterpret_cast<float*>(a.act_o + a2_xsum(t, k >> 7, NT)) = xs;
+    if (W > 1) cbar();
   }
   cbar();
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
     red_release_gpu_add(ctr + C_ATT, 1);
   }
-  return ring.k;
+  if (atl) { atl[4] = clk64(); atl[5] = (unsigned long long)(t1 - t0); atl[6] = (unsigned long long)s.att_S; }
+  tmark(a, layer * 5 + PH_ATT, 2);
+  where(a, WCODE(layer, PH_ATT, 9));
+  return ring_of(t1);
 }
 
 template <int NT, int D>
 __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM)
-    step_kernel(const StepArgs* __restrict__ ap) {
+    step_kernel(const StepArgs* __restrict__ ap_g) {
   using C = StepCfg<NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[2], mdone[2];
   __shared__ int s_done[128];
   __shared__ int s_nd;
   __shared__ float s_rmax[2 * 64];
   __shared__ Sched s_sched;
-  __shared__ __align__(16) uint16_t s_p[64 * (4096 / D)];
+  __shared__ __align__(16) float s_merge[8 * 132];
+  __shared__ uint32_t s_tmem, s_slot[2];
+  // the arguments and the per-layer pointer table live in shared memory: the
+  // producer's per-unit address arithmetic must not chase global pointers
+  __shared__ __align__(16) StepArgs s_args;
+  __shared__ __align__(16) LayerPtrs s_lp[kStepMaxLayers];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(ap_g);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(&s_args);
+    for (int i = threadIdx.x; i < (int)(sizeof(StepArgs) / 8); i += blockDim.x) dst[i] = src[i];
+    const uint64_t* lsrc = reinterpret_cast<const uint64_t*>(ap_g->layers);
+    uint64_t* ldst = reinterpret_cast<uint64_t*>(s_lp);
+    const int nl = ap_g->n_layers;
+    for (int i = threadIdx.x; i < nl * (int)(sizeof(LayerPtrs) / 8); i += blockDim.x) ldst[i] = lsrc[i];
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 8);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&ardy[i], 8);
+      mbar_init(&mdone[i], 1);
+    }
     fence_mbar_init();
   }
+  if (warp == 0) {  // the whole TMEM of the SM (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) s_args.layers = s_lp;
+  __syncthreads();
+  const StepArgs* __restrict__ ap = &s_args;
   const uint32_t sm0 = smem_u32(smem), full0 = smem_u32(full), empty0 = smem_u32(empty);
+  const Tc tc{s_tmem, smem_u32(ardy), smem_u32(mdone), s_slot};
   // everything below reads the ingest kernel's outputs (T, L, tree, counters)
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) make_sched(*ap, blockIdx.x, ap->st->L, ap->st->T, NT, s_sched);
   __syncthreads();
-  if (warp == 8) {
-    if (lane == 0) producer<NT>(ap, &s_sched, sm0, full0, empty0);
+  if (warp >= 8) {  // warpgroup 2: producer, MMA issuer, two idle warps
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_AUX));
+    if (warp == 8) {
+      if (lane == 0) producer<NT>(ap, &s_sched, sm0, full0, empty0);
+      where(*ap, WCODE(0xFFFF, 0x40, 0xFF));
+    } else if (warp == 9) {
+      mma_warp<NT>(ap, tc);
+      where(*ap, WCODE(0xFFFF, 0x20, 0xFF));
+    }
     return;
   }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_CONSUMER));
   Ring ring{sm0, full0, empty0, 0};
+  int tck = 0;  // W4 units consumed (TMEM buffer / barrier phase)
   const int n_layers = ap->n_layers;
   const bool att = s_sched.att_item >= 0;
+  int2 r;
   for (int l = 0; l < n_layers; ++l) {
-    ring.k = gemm_phase<NT, PH_QKV>(ap, &s_sched, l, s_sched.qkv0, s_sched.qkv1, ring, s_done, &s_nd);
-    if (att) ring.k = attn_item<NT, D>(ap, &s_sched, l, ring, s_rmax, s_p);
-    ring.k = gemm_phase<NT, PH_O>(ap, &s_sched, l, s_sched.o0, s_sched.o1, ring, s_done, &s_nd);
-    ring.k = gemm_phase<NT, PH_GU>(ap, &s_sched, l, s_sched.gu0, s_sched.gu1, ring, s_done, &s_nd);
-    ring.k = gemm_phase<NT, PH_DN>(ap, &s_sched, l, s_sched.dn0, s_sched.dn1, ring, s_done, &s_nd);
+    r = gemm_phase<NT, PH_QKV>(ap, &s_sched, l, s_sched.qkv0, s_sched.qkv1, ring, tc, tck, s_done, &s_nd);
+    ring.k = r.x; tck = r.y;
+    if (att) ring.k = attn_item<NT, D>(ap, &s_sched, l, ring, s_merge, smem + C::STAGES * C::SLOT);
+    r = gemm_phase<NT, PH_O>(ap, &s_sched, l, s_sched.o0, s_sched.o1, ring, tc, tck, s_done, &s_nd);
+    ring.k = r.x; tck = r.y;
+    r = gemm_phase<NT, PH_GU>(ap, &s_sched, l, s_sched.gu0, s_sched.gu1, ring, tc, tck, s_done, &s_nd);
+    ring.k = r.x; tck = r.y;
+    r = gemm_phase<NT, PH_DN>(ap, &s_sched, l, s_sched.dn0, s_sched.dn1, ring, tc, tck, s_done, &s_nd);
+    ring.k = r.x; tck = r.y;
   }
-  gemm_phase<NT, PH_LM>(ap, &s_sched, 0, s_sched.lm0, s_sched.lm1, ring, s_done, &s_nd);
+  // stop the MMA warp: an empty A buffer announcement (thread 0 writes the slot
+  // before its own arrival; every consumer warp's lane 0 arrives)
+  if (threadIdx.x == 0) s_slot[tck & 1] = 0;
+  if (lane == 0) mbar_arrive_a(tc.ardy0 + 8 * (tck & 1));
+  where(*ap, WCODE(0xFFFE, 0, 0));
+  gemm_phase<NT, PH_LM>(ap, &s_sched, 0, s_sched.lm0, s_sched.lm1, ring, tc, tck, s_done, &s_nd);
+  tc_fence_before();
+  cbar();
+  __syncwarp();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(kTmemCols));
+  where(*ap, WCODE(0xFFFF, 0xFF, 0xFF));
 }
 
 template <int NT, int D>

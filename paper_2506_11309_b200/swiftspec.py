@@ -76,6 +76,9 @@ def lib():
         "ss_set_debug": (i32, [vp, i32]),
         "ss_set_step_kernel": (i32, [vp, i32]),
         "ss_step_kernel_active": (i32, [vp, i32]),
+        "ss_step_trace": (i32, [vp, i32]),
+        "ss_read_step_trace": (i32, [vp, vp, sz, C.POINTER(i32), C.POINTER(i32)]),
+        "ss_step_trace_host": (vp, [vp]),
         "ss_read_tree_meta": (i32, [vp, vp, vp, vp, vp, vp]),
         "ss_read_packed": (i32, [vp, i32, i32, vp, sz, C.POINTER(sz)]),
         "ss_debug_gemm": (i32, [vp, i32, i32, vp, i32, vp, i32, vp]),
@@ -150,6 +153,37 @@ class Shard:
 
     def step_kernel_active(self, T: int) -> bool:
         return lib().ss_step_kernel_active(self.h, T) == 1
+
+    def step_trace(self, on: bool):
+        """Record a per-CTA phase timeline on later persistent-step launches (measurement hook;
+        on=2: mapped host memory, readable while a launch still runs)."""
+        self._ck(lib().ss_step_trace(self.h, int(on)))
+
+    def step_trace_where(self) -> np.ndarray:
+        """Progress words [512 CTAs][16 warps] straight from the mapped buffer (no CUDA call)."""
+        p = lib().ss_step_trace_host(self.h)
+        if not p:
+            raise RuntimeError("step_trace(2) not enabled")
+        slots = self.cfg.n_layers * 5 + 1
+        n = 512 * slots * 3 + 512 * 16 + 65536
+        arr = np.ctypeslib.as_array((C.c_uint64 * n).from_address(p))
+        return arr[512 * slots * 3:].reshape(512, 16).copy()
+
+    def read_step_trace(self, with_where: bool = False, with_units: bool = False):
+        """uint64 [512 CTAs][n_layers*5+1 slots][3 stamps] (entry, first unit ready, exit; ns);
+        with_where: also the per-(CTA, warp) progress words [512][16] (mapped mode);
+        with_units: also CTA 0's unit timeline (65536 words, clock64)."""
+        slots = self.cfg.n_layers * 5 + 1
+        nt = 512 * slots * 3
+        buf = np.zeros(nt + 512 * 16 + 65536, dtype=np.uint64)
+        nc, ns = C.c_int32(), C.c_int32()
+        self._ck(lib().ss_read_step_trace(self.h, _ptr(buf), buf.size, C.byref(nc), C.byref(ns)))
+        out = [buf[:nt].reshape(nc.value, ns.value, 3)]
+        if with_where:
+            out.append(buf[nt:nt + 512 * 16].reshape(512, 16))
+        if with_units:
+            out.append(buf[nt + 512 * 16:])
+        return out[0] if len(out) == 1 else tuple(out)
 
     def set_debug(self, flags: int):
         """SS_DEBUG_CONSISTENCY: cross-rank checksum of every verify's tree."""

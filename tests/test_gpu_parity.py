@@ -147,7 +147,14 @@ def test_tiny_commit_errors(tiny):
         sh.verify([1, 2], [0, 0])
     with pytest.raises(pkg.SwiftSpecError, match="SS_EINVAL"):
         sh.verify([1, cfg.vocab], [-1, 0])
-    # capacity: L + T > max_ctx is refused before any launch
+    # capacity: L + T > max_ctx is refused before any launch.  The
+    # committed length may only grow over rows actually written: write a longer
+    # prefix first (counter-indexed generator: its first 64 rows are unchanged)
+    with pytest.raises(pkg.SwiftSpecError, match="SS_EINVAL"):
+        sh.set_committed_len(sh.max_ctx - 64)
+    for l in range(cfg.n_layers):
+        k, v = synth.gen_prefix_kv(1, l, sh.max_ctx - 64, cfg.n_kv_heads, cfg.head_dim)
+        sh.set_prefix_kv(l, k, v)
     sh.set_committed_len(sh.max_ctx - 64)
     toks, pars = synth.tree_chain(8, cfg.vocab, np.random.default_rng(1))
     sh.verify(toks, pars)

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for tp in 1 8; do
+timeout 200 python tools/step_trace.py --T 8 --tp $tp --show 1 > gpurun_out/trace_att_tp$tp.log 2>&1; echo "rc=$?"; grep -A1 "CTA 0 attention" gpurun_out/trace_att_tp$tp.log; grep "mean critical" gpurun_out/trace_att_tp$tp.log
+done

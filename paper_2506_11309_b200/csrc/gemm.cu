@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
   bool done = false;
   // shared-window addresses, computed once: stage base + per-warp offsets
   const uint32_t sm0 = opaque(smem_u32(smem)), full0 = opaque(smem_u32(full)), empty0 = opaque(smem_u32(empty));
-  const uint32_t su0 = opaque(smem_u32(s_unit));
+  int uc = u0;  // next unit to consume
   const uint32_t o_w = opaque((uint32_t)(tile * 128 + lane) * 16);            // weight chunks
   const uint32_t o_sc = opaque((uint32_t)(kW4Bytes + tile * 64 + gq * 4));     // [grp][gq] scale pairs
   const uint32_t o_z = opaque((uint32_t)(kW4Bytes + 512 + tile * 16 + gq));    // [grp][gq] zero pairs
@@ -504,9 +504,12 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
     // consume consecutive units of one tile-group; stop at a tile-group change
     // (the new unit stays in its slot for the next round) or at end of work
     while (true) {
+      // the unit sequence is the static range [u0, u1): computed here, not
+      // read back from the producer's slot tags (no generic smem hand-off
+      // beside the TMA-completed barrier)
+      if (uc >= u1) { done = true; break; }
       mbar_wait_a(full0 + 8 * s, ph);
-      tg = (int)lds32(su0 + 4 * s);
-      if (tg < 0) { done = true; break; }
+      tg = uc / g.S;
       if (cur_tg >= 0 && tg != cur_tg) break;
       cur_tg = tg;
       ++nst;
@@ -647,6 +650,7 @@ __global__ void __launch_bounds__(GemmCfg<WFMT, NT>::THREADS, GemmCfg<WFMT, NT>:
       __syncwarp();
       if (lane == 0) mbar_arrive_a(empty0 + 8 * s);
       if (++s == C::STAGES) { s = 0; ph ^= 1; }
+      ++uc;
     }
     if (cur_tg < 0) break;  // no work at all
     TS(3);

@@ -37,11 +37,13 @@ struct StepCfg {
   static constexpr int LM_ABYTES = (kBFKS / 16) * 2 * NT * 256;     // LM input per unit (bf16 hi, lo)
   static constexpr int SLOT = kW4UnitBytes + ABYTES;                // >= LM unit, >= one 16 KB K/V tile
   static constexpr int CTAS_PER_SM = 1;  // owns the SM's 512 TMEM columns
-  static constexpr int QBYTES = 32768;  // attention: the item's q fragments (64 rows x d <= 128, hi + lo)
-  static constexpr int STAGES = (204800 - QBYTES) / SLOT;
+  // attention: the item's q fragments (64 rows x d <= 128, hi + lo, 32 KB);
+  // GEMM tails: the tile-group's accumulator block and new residual rows
+  static constexpr int QBYTES = 34816;
+  static constexpr int STAGES = (218112 - QBYTES) / SLOT;
   static constexpr int SMEM = STAGES * SLOT + QBYTES;
-  // 8 consumer warps (warpgroups 0, 1) + warpgroup 2: producer warp, MMA warp,
-  // two idle warps.  Launched at 168 registers (3 warps per SMSP); warpgroup 2
+  // 8 consumer warps (warpgroups 0, 1) + warpgroup 2: producer warp, two MMA
+  // warps (one per AWQ group of a unit), one idle warp.  Launched at 168 registers (3 warps per SMSP); warpgroup 2
   // gives registers back (setmaxnreg) so the consumers run with 208.
   static constexpr int THREADS = 384;
   static constexpr int REG_CONSUMER = 208, REG_AUX = 80;  // 8 x 208 + 4 x 80 <= 12 x 168 (the CTA pool)
@@ -393,10 +395,17 @@ __device__ __noinline__ void producer(const StepArgs* __restrict__ ap, const Sch
   unsigned long long t_idle = clk64();
   while (ai.ph != PH_END) {
     bool prog = false;
-    // part 1: weights (or prefix K/V tiles) into every free slot
+    // part 1: weights (or prefix K/V tiles) into every free slot; one proxy
+    // fence per batch orders the consumers' generic reads of the freed slots
+    // before the TMA overwrites
+    bool fenced = false;
     while (wi.ph != PH_END && wk - ak < C::STAGES) {
       const int slot = wk % C::STAGES;
       if (!mbar_test_a(empty0 + 8 * slot, (uint32_t)(((wk / C::STAGES) & 1) ^ 1))) break;
+      if (!fenced) {
+        fence_proxy_async_smem();
+        fenced = true;
+      }
       const uint32_t dst = sm0 + slot * C::SLOT, bar = full0 + 8 * slot;
       if (wi.ph != PH_ATT) {
         const uint32_t ub = wi.ph == PH_LM ? (uint32_t)kBFUnitBytes : (uint32_t)kW4UnitBytes;
@@ -530,7 +539,7 @@ SS_DEV void wait_counter(const int* p, int target) {
 struct Tc {
   uint32_t tbase;    // TMEM base address
   uint32_t ardy0;    // mbarrier[2]: the unit's A operand is in TMEM (8 warp arrivals)
-  uint32_t mdone0;   // mbarrier[2]: the unit's MMAs completed (tcgen05.commit)
+  uint32_t mdone0;   // mbarrier[2 buffers][2 groups]: the unit's MMAs of one AWQ group completed
   uint32_t* slot;    // shared [2]: smem address of the unit's ring slot (0 = stop)
 };
 
@@ -569,7 +578,10 @@ template <int NT>
 SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, float (&y)[8 * NT]) {
   constexpr int TP = 8 * NT, N = 16 * NT;
   const int qd = warp & 3, hh = warp >> 2, b = k & 1;
-  mbar_wait_wd(tc.mdone0 + 8 * b, (uint32_t)((k >> 1) & 1));
+  // both groups' MMAs (two issuers): this warp's next dequant overwrites the
+  // A columns of both groups
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b), (uint32_t)((k >> 1) & 1));
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b + 1), (uint32_t)((k >> 1) & 1));
   __syncwarp();
   tc_fence_after();
   // metadata of row m = 32 qd + lane (tile m / 16, fragment row m % 16) in group hh
@@ -609,11 +621,13 @@ SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, f
   tc_fence_before();  // the TMEM reads before the next MMA into this accumulator
 }
 
-// The MMA warp: for every W4 unit of the CTA (in the consumers' order), wait
-// for its A operand, issue 2 groups x 8 MMAs (K 16 each; the first MMA of a
-// group overwrites its accumulator), commit to mdone.  Stops on slot == 0.
+// The MMA warps (one per AWQ group g of the unit: a single issuing thread
+// sustains only one 128 x N x 16 MMA per ~70 cycles): for every W4 unit of the
+// CTA (in the consumers' order), wait for its A operand, issue the group's
+// 8 MMAs (K 16 each; the first overwrites the accumulator), commit to
+// mdone[b][g].  Stop on slot == 0.
 template <int NT>
-__device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc) {
+__device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc, int g) {
   const StepArgs& a = *ap;
   constexpr int N = 16 * NT;
   constexpr uint32_t idesc = idesc_f16(128, N);
@@ -621,14 +635,13 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc) {
     const int b = k & 1;
     where(a, WCODE(k & 0xFFFF, 0x20, 1));
     mbar_wait_wd(tc.ardy0 + 8 * b, (uint32_t)((k >> 1) & 1));
-    if (a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2] = clk64();
+    if (g == 0 && a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2] = clk64();
     __syncwarp();
     const uint32_t sst = *reinterpret_cast<volatile uint32_t*>(tc.slot + b);
     if (sst == 0) break;
     tc_fence_after();
     const uint64_t bd0 = smem_desc(sst + kW4UnitBytes, N * 16, 128);
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
+    {
       const uint32_t d = tc.tbase + kAccCol + (uint32_t)((b * 2 + g) * N);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
@@ -646,9 +659,9 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc) {
     }
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(tc.mdone0 + 8 * b)
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(tc.mdone0 + 8 * (2 * b + g))
         : "memory");
-    if (a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2 + 1] = clk64();
+    if (g == 0 && a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2 + 1] = clk64();
   }
 }
 
@@ -673,7 +686,42 @@ SS_DEV void lm_unit(uint32_t sst, int warp, int lane, float (&acc)[NT][4]) {
 }
 
 // Epilogues (256 consumer threads) --------------------------------------------
+// Tile-group tails are chains of dependent global accesses, so each first
+// stages what it reads -- the tile-group's fp32 accumulator block, the
+// per-token norm scales / positions -- into shared memory (the attention q
+// area, idle during GEMM phases) with all loads in flight at once, then
+// computes from shared memory.  New residual rows also stay there for the
+// next GEMM's input.
 SS_DEV float norm_scale(const float* ss, int t, int h, float eps) { return rsqrtf(__ldcg(ss + t) / (float)h + eps); }
+
+template <int NT>
+struct TailSm {
+  float* acc;  // [128][8 NT] accumulator block of the tile-group
+  float* xn;   // [8 NT][128] new residual rows of the tile-group
+  float* rs;   // [8 NT] per-token scale
+  int* pos;    // [8 NT] positions
+};
+template <int NT>
+SS_DEV TailSm<NT> tail_sm(uint8_t* base) {
+  constexpr int TP = 8 * NT;
+  TailSm<NT> t;
+  t.acc = reinterpret_cast<float*>(base);
+  t.xn = t.acc + 128 * TP;
+  t.rs = t.xn + 128 * TP;
+  t.pos = reinterpret_cast<int*>(t.rs + TP);
+  return t;
+}
+// acc block (128 x 8 NT fp32) -> shared memory; caller synchronises
+template <int NT>
+SS_DEV void stage_acc(const float* acc, float* sm) {
+  const float4* src = reinterpret_cast<const float4*>(acc);
+  float4* dst = reinterpret_cast<float4*>(sm);
+  float4 v[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) v[i] = __ldcg(src + threadIdx.x + i * 256);
+#pragma unroll
+  for (int i = 0; i < NT; ++i) dst[threadIdx.x + i * 256] = v[i];
+}
 
 SS_DEV uint32_t q_frag_index(int m, int j, int d, int rbmax, int kvh) {
   const int rb = m >> 4, r = m & 15, kk = j >> 4, c = j & 15;
@@ -685,24 +733,38 @@ SS_DEV uint32_t q_frag_index(int m, int j, int d, int rbmax, int kvh) {
 // a4: deferred attn-norm scale, RoPE (R2), q hi/lo in fragment order,
 // tree K/V rows: fp16 hi into the cache at L + t (R10), lo into the window.
 template <int NT>
-SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, const Sched& s) {
-  const int TP = NT * 8, T = s.T, L = s.L, d = a.d, half = d >> 1;
+SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, const Sched& s, const TailSm<NT>& ts) {
+  constexpr int TP = NT * 8, IT = 128 * TP / 256;
+  const int T = s.T, L = s.L, d = a.d, half = d >> 1;
   const int nq = a.Hq_l * d, nk = a.Hkv_l * d;
   const float* ssa = a.ss + (size_t)layer * 2 * 64;
   const int wb = L & ~63;
   const int rbmax = 4 * a.G;
   const size_t qlo = (size_t)a.Hkv_l * rbmax * (d / 16) * 32 * 8;
-  const int n = 128 * T;
-  for (int idx = threadIdx.x; idx < n; idx += 256) {
-    const int r = idx / T, t = idx - r * T;
+  stage_acc<NT>(acc, ts.acc);
+  if (threadIdx.x < T) {
+    ts.rs[threadIdx.x] = norm_scale(ssa, threadIdx.x, a.h, a.eps);
+    ts.pos[threadIdx.x] = a.st->pos[threadIdx.x];
+  }
+  cbar();
+  float2 cs[IT];
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {  // RoPE table entries first (independent loads)
+    const int idx = threadIdx.x + i * 256, r = idx / TP, t = idx % TP;
     const int row = tg * 128 + r, j = row % d;
-    const float rs = norm_scale(ssa, t, a.h, a.eps);
-    float x = __ldcg(acc + (size_t)r * TP + t) * rs;
+    cs[i] = (t < T && row < nq + nk) ? __ldg(&a.rope_cs[(size_t)ts.pos[t] * half + (j % half)]) : make_float2(1.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const int idx = threadIdx.x + i * 256, r = idx / TP, t = idx % TP;
+    if (t >= T) continue;
+    const int row = tg * 128 + r, j = row % d;
+    const float rs = ts.rs[t];
+    float x = ts.acc[r * TP + t] * rs;
     if (row < nq + nk) {
       const int pr = (j < half) ? r + half : r - half;
-      const float pv = __ldcg(acc + (size_t)pr * TP + t) * rs;
-      const float2 cs = a.rope_cs[(size_t)a.st->pos[t] * half + (j % half)];
-      x = (j < half) ? (x * cs.x - pv * cs.y) : (x * cs.x + pv * cs.y);
+      const float pv = ts.acc[pr * TP + t] * rs;
+      x = (j < half) ? (x * cs[i].x - pv * cs[i].y) : (x * cs[i].x + pv * cs[i].y);
     }
     const __half hh = __float2half_rn(x);
     const __half hl = __float2half_rn(x - __half2float(hh));
@@ -743,16 +805,19 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
 
 // a8: deferred mlp-norm scale + SwiGLU (R4) -> down input (hi/lo, X)
 template <int NT>
-SS_DEV void epi_swiglu(const StepArgs& a, int layer, int tg, const float* acc, int T) {
+SS_DEV void epi_swiglu(const StepArgs& a, int layer, int tg, const float* acc, int T, const TailSm<NT>& ts) {
   const int TP = NT * 8;
   const float* ssm = a.ss + (size_t)layer * 2 * 64 + 64;
+  stage_acc<NT>(acc, ts.acc);
+  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale(ssm, threadIdx.x, a.h, a.eps);
+  cbar();
   const int warp = threadIdx.x >> 5, cp = threadIdx.x & 31;
   for (int t = warp; t < T; t += 8) {
-    const float rs = norm_scale(ssm, t, a.h, a.eps);
-    const float g0 = __ldcg(acc + (size_t)(2 * cp) * TP + t) * rs;
-    const float g1 = __ldcg(acc + (size_t)(2 * cp + 1) * TP + t) * rs;
-    const float u0 = __ldcg(acc + (size_t)(64 + 2 * cp) * TP + t) * rs;
-    const float u1 = __ldcg(acc + (size_t)(64 + 2 * cp + 1) * TP + t) * rs;
+    const float rs = ts.rs[t];
+    const float g0 = ts.acc[(2 * cp) * TP + t] * rs;
+    const float g1 = ts.acc[(2 * cp + 1) * TP + t] * rs;
+    const float u0 = ts.acc[(64 + 2 * cp) * TP + t] * rs;
+    const float u1 = ts.acc[(64 + 2 * cp + 1) * TP + t] * rs;
     const float h0 = g0 / (1.f + __expf(-g0)) * u0;
     const float h1 = g1 / (1.f + __expf(-g1)) * u1;
     const int k = tg * 64 + 2 * cp;
@@ -765,17 +830,17 @@ SS_DEV void epi_swiglu(const StepArgs& a, int layer, int tg, const float* acc, i
   }
 }
 
-// TP > 1: this rank's fp32 partial of tile-group tg to every peer as LL lines
-// (data1, flag1, data2, flag2, R15), same layout as gemm.cu.
+// TP > 1: this rank's fp32 partial of tile-group tg (staged in shared memory)
+// to every peer as LL lines (data1, flag1, data2, flag2, R15).
 template <int NT>
-SS_DEV void ar_send(const StepArgs& a, int tg, const float* acc, int T, int ar_seq) {
+SS_DEV void ar_send(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<NT>& ts) {
   const int TP = NT * 8;
   const uint32_t flag = a.st->epoch + ar_seq;
   const int pairs = (T + 1) >> 1;
   const int ntg = a.h / 128;
   for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
     const int r = idx / pairs, tp = idx - r * pairs;
-    const float2 v = __ldcg(reinterpret_cast<const float2*>(acc + (size_t)r * TP + 2 * tp));
+    const float2 v = *reinterpret_cast<const float2*>(ts.acc + r * TP + 2 * tp);
     for (int p = 0; p < a.P; ++p) {
       const int slot = a.loopback ? p : a.rank;
       const size_t line = (((size_t)(ar_seq & 1) * a.P + slot) * ntg + tg) * 128 * (4 * NT) + (size_t)r * (4 * NT) + tp;
@@ -785,15 +850,27 @@ SS_DEV void ar_send(const StepArgs& a, int tg, const float* acc, int T, int ar_s
 }
 
 // Residual update of tile-group tg: x += acc (P == 1) or the rank-ordered sum
-// of every rank's partial (TP all-reduce receive).
+// of every rank's partial (TP all-reduce receive); the new rows also go to
+// ts.xn for the next GEMM's input.
 template <int NT>
-SS_DEV void resid_update(const StepArgs& a, int tg, const float* acc, int T, int ar_seq) {
-  const int TP = NT * 8;
+SS_DEV void resid_update(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<NT>& ts) {
+  constexpr int TP = NT * 8;
   if (a.P == 1) {
-    for (int idx = threadIdx.x; idx < 128 * T; idx += 256) {
-      const int t = idx >> 7, r = idx & 127;
-      float* xp = a.x + (size_t)t * a.h + tg * 128 + r;
-      *xp = __ldcg(xp) + __ldcg(acc + (size_t)r * TP + t);
+    constexpr int IT = 128 * TP / 256;
+    float xo[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int idx = threadIdx.x + i * 256, t = idx >> 7, r = idx & 127;
+      xo[i] = t < T ? __ldcg(a.x + (size_t)t * a.h + tg * 128 + r) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int idx = threadIdx.x + i * 256, t = idx >> 7, r = idx & 127;
+      if (t < T) {
+        const float v = xo[i] + ts.acc[r * TP + t];
+        a.x[(size_t)t * a.h + tg * 128 + r] = v;
+        ts.xn[t * 128 + r] = v;
+      }
     }
     return;
   }
@@ -801,11 +878,15 @@ SS_DEV void resid_update(const StepArgs& a, int tg, const float* acc, int T, int
   const uint32_t flag = a.st->epoch + ar_seq;
   const int pairs = (T + 1) >> 1;
   const int ntg = a.h / 128;
+  const size_t pstride = (size_t)ntg * 128 * PP;
+  const uint4* src0 = reinterpret_cast<const uint4*>(a.recv) + (((size_t)(ar_seq & 1) * a.P) * ntg + tg) * 128 * PP;
   for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
     const int tp = idx >> 7, r = idx & 127;
-    const uint4* src0 = reinterpret_cast<const uint4*>(a.recv) +
-                        (((size_t)(ar_seq & 1) * a.P) * ntg + tg) * 128 * PP + (size_t)r * PP + tp;
-    const size_t pstride = (size_t)ntg * 128 * PP;
+    const int t0 = 2 * tp;
+    const uint4* src = src0 + (size_t)r * PP + tp;
+    // the old residual values and every rank's line are requested together
+    const float x0 = __ldcg(a.x + (size_t)t0 * a.h + tg * 128 + r);
+    const float x1 = t0 + 1 < T ? __ldcg(a.x + (size_t)(t0 + 1) * a.h + tg * 128 + r) : 0.f;
     uint32_t d1[kMaxPeers], d2[kMaxPeers];
     unsigned ready = 0;
     const unsigned all = (1u << a.P) - 1u;
@@ -814,8 +895,8 @@ SS_DEV void resid_update(const StepArgs& a, int tg, const float* acc, int T, int
     while (ready != all) {
 #pragma unroll
       for (int p = 0; p < kMaxPeers; ++p)
-        if (p < a.P && !(ready & (1u << p)) && ll_try_load(src0 + p * pstride, flag, d1[p], d2[p])) ready |= 1u << p;
-      if ((++spins & 255u) == 0) {  // bounded: 2 s per line, or at once after another timeout
+        if (p < a.P && !(ready & (1u << p)) && ll_try_load(src + p * pstride, flag, d1[p], d2[p])) ready |= 1u << p;
+      if (ready != all && (++spins & 255u) == 0) {  // bounded: 2 s per line, or at once after another timeout
         if (!tw) tw = now_ns();
         if (now_ns() - tw > 2000000000ull || *reinterpret_cast<volatile int*>(&a.st->timeout)) {
           a.st->timeout = 1;
@@ -830,23 +911,27 @@ SS_DEV void resid_update(const StepArgs& a, int tg, const float* acc, int T, int
         s0 += __uint_as_float(d1[p]);
         s1 += __uint_as_float(d2[p]);
       }
-    const int t0 = 2 * tp;
-    float* x0 = a.x + (size_t)t0 * a.h + tg * 128 + r;
-    *x0 = __ldcg(x0) + s0;
-    if (t0 + 1 < T) x0[a.h] = __ldcg(x0 + a.h) + s1;
+    float* xp = a.x + (size_t)t0 * a.h + tg * 128 + r;
+    *xp = x0 + s0;
+    ts.xn[t0 * 128 + r] = x0 + s0;
+    if (t0 + 1 < T) {
+      xp[a.h] = x1 + s1;
+      ts.xn[(t0 + 1) * 128 + r] = x1 + s1;
+    }
   }
 }
 
-// After the residual of tile-group tg is final: the next GEMM's input for its
-// 128 columns (x * g, fp16 hi/lo + X; or bf16 hi/lo for the LM head) and the
-// token's sum of squares (the deferred RMSNorm scale, R5).
+// After the residual of tile-group tg is final (its rows in ts.xn): the next
+// GEMM's input for its 128 columns (x * g, fp16 hi/lo + X; or bf16 hi/lo for
+// the LM head) and the token's sum of squares (the deferred RMSNorm scale, R5).
 template <int NT>
-SS_DEV void next_input(const StepArgs& a, int tg, int T, const uint16_t* gain, float* ss, uint8_t* act, int lm) {
+SS_DEV void next_input(const StepArgs& a, int tg, int T, const uint16_t* gain, float* ss, uint8_t* act, int lm,
+                       const TailSm<NT>& ts) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = tg * 128 + lane * 4;
   const uint2 gw = *reinterpret_cast<const uint2*>(gain + k);
   for (int t = warp; t < T; t += 8) {
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x + (size_t)t * a.h + k));
+    const float4 v = *reinterpret_cast<const float4*>(ts.xn + t * 128 + lane * 4);
     const float q = warp_sum(v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w);
     if (lane == 0) atomicAdd(ss + t, q);
     const float y0 = v.x * bf16_lo(gw.x), y1 = v.y * bf16_hi(gw.x), y2 = v.z * bf16_lo(gw.y), y3 = v.w * bf16_hi(gw.y);
@@ -872,15 +957,17 @@ SS_DEV void next_input(const StepArgs& a, int tg, int T, const uint16_t* gain, f
 }
 
 template <int NT>
-SS_DEV void epi_argmax(const StepArgs& a, int tg, const float* acc, int T) {
+SS_DEV void epi_argmax(const StepArgs& a, int tg, const float* acc, int T, const TailSm<NT>& ts) {
   const int TP = NT * 8;
   const float* ssf = a.ss + (size_t)a.n_layers * 2 * 64;
+  stage_acc<NT>(acc, ts.acc);
+  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale(ssf, threadIdx.x, a.h, a.eps);
+  cbar();
   const int r = threadIdx.x & 127;
   const int v = tg * 128 + r;
   const bool valid = v < a.V_l;
   for (int t = threadIdx.x >> 7; t < T; t += 2) {
-    const float rs = norm_scale(ssf, t, a.h, a.eps);
-    const float val = valid ? __ldcg(acc + (size_t)r * TP + t) * rs : -INFINITY;
+    const float val = valid ? ts.acc[r * TP + t] * ts.rs[t] : -INFINITY;
     if (valid && a.logits) a.logits[(size_t)t * a.logits_ld + v] = val;
     unsigned long long key = valid ? argmax_key(val, (uint32_t)(a.V_off + v)) : 0ull;
 #pragma unroll
@@ -897,7 +984,8 @@ SS_DEV void epi_argmax(const StepArgs& a, int tg, const float* acc, int T) {
 // here.  Returns the number of tile-groups this CTA finalised.
 template <int NT, int PH>
 __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const Sched* __restrict__ sp, int layer,
-                                        int u0, int u1, Ring ring, Tc tc, int tck, int* s_done, int* s_nd) {
+                                        int u0, int u1, Ring ring, Tc tc, int tck, int* s_done, int* s_nd,
+                                        uint8_t* s_tail) {
   const StepArgs& a = *ap;
   const Sched& s = *sp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -982,6 +1070,7 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
   where(a, WCODE(layer, PH, 4));
   // arrivals: the barrier orders every warp's reductions before thread 0's
   // GPU-scope fence (cumulative) and arrival counts
+  const unsigned long long tl0 = clk64();
   cbar();
   if (threadIdx.x == 0) {
     int nd = 0;
@@ -998,18 +1087,24 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
   __syncwarp();
   cbar();
   const int nd = *s_nd;
+  // tail timeline (trace mode): the finaliser of tile-group 0, middle layer
+  unsigned long long* ttl = (a.utl && PH != PH_LM && layer == a.n_layers / 2 && nd > 0 && s_done[0] == 0 &&
+                             threadIdx.x == 0) ? a.utl + 30000 + PH * 16 : nullptr;
+  if (ttl) { ttl[0] = tl0; ttl[1] = clk64(); ttl[8] = (unsigned long long)nd; }
   if (nd == 0) {
     tmark(a, tslot, 2);
     return make_int2(ring.k, tck);
   }
   int* ctr = a.ctr + (size_t)layer * kCtrPerLayer;
+  const TailSm<NT> ts = tail_sm<NT>(s_tail);
   if constexpr (PH == PH_QKV || PH == PH_GU || PH == PH_LM) {
     for (int i = 0; i < nd; ++i) {
       const int tg = s_done[i];
       const float* accp = accb + (size_t)tg * 128 * TP;
-      if constexpr (PH == PH_QKV) epi_qkv<NT>(a, layer, tg, accp, s);
-      else if constexpr (PH == PH_GU) epi_swiglu<NT>(a, layer, tg, accp, T);
-      else epi_argmax<NT>(a, tg, accp, T);
+      if constexpr (PH == PH_QKV) epi_qkv<NT>(a, layer, tg, accp, s, ts);
+      else if constexpr (PH == PH_GU) epi_swiglu<NT>(a, layer, tg, accp, T, ts);
+      else epi_argmax<NT>(a, tg, accp, T, ts);
+      cbar();  // shared staging reused by the next tile-group
     }
   } else {
     // residual phases: sends of every completed tile-group first, then the
@@ -1017,17 +1112,31 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
     const int ar_seq = 2 * layer + (PH == PH_DN ? 1 : 0);
     where(a, WCODE(layer, PH, 6));
     if (a.P > 1)
-      for (int i = 0; i < nd; ++i) ar_send<NT>(a, s_done[i], accb + (size_t)s_done[i] * 128 * TP, T, ar_seq);
+      for (int i = 0; i < nd; ++i) {
+        stage_acc<NT>(accb + (size_t)s_done[i] * 128 * TP, ts.acc);
+        cbar();
+        ar_send<NT>(a, s_done[i], T, ar_seq, ts);
+        cbar();
+      }
+    if (ttl) ttl[2] = clk64();
     where(a, WCODE(layer, PH, 7));
-    for (int i = 0; i < nd; ++i) resid_update<NT>(a, s_done[i], accb + (size_t)s_done[i] * 128 * TP, T, ar_seq);
-    where(a, WCODE(layer, PH, 8));
-    cbar();
     const bool last = PH == PH_DN && layer + 1 == a.n_layers;
     const uint16_t* gain = PH == PH_O ? a.layers[layer].mlp_norm
                                       : (last ? a.final_norm : a.layers[layer + 1].attn_norm);
     float* ssn = a.ss + (size_t)(PH == PH_O ? layer * 2 + 1 : (layer + 1) * 2) * 64;
     uint8_t* act = last ? a.act_lm : a.act_h;
-    for (int i = 0; i < nd; ++i) next_input<NT>(a, s_done[i], T, gain, ssn, act, last ? 1 : 0);
+    for (int i = 0; i < nd; ++i) {
+      if (a.P == 1) {
+        stage_acc<NT>(accb + (size_t)s_done[i] * 128 * TP, ts.acc);
+        cbar();
+      }
+      resid_update<NT>(a, s_done[i], T, ar_seq, ts);
+      cbar();
+      if (ttl && i == 0) ttl[3] = clk64();
+      next_input<NT>(a, s_done[i], T, gain, ssn, act, last ? 1 : 0, ts);
+      cbar();
+    }
+    where(a, WCODE(layer, PH, 8));
     if constexpr (PH == PH_O) {
       // zero the down input's X slots (the SwiGLU epilogues of this layer add into them)
       const int ngrp = a.I_l / 128;
@@ -1037,6 +1146,7 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
             *reinterpret_cast<float*>(a.act_d + a2_xsum(t, g, NT)) = 0.f;
     }
   }
+  if (ttl) ttl[4] = clk64();
   cbar();
   // self-clean the accumulators and arrival counters for the next layer
   for (int i = 0; i < nd; ++i) {
@@ -1060,7 +1170,9 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
       }
     } else {
       const int ci = PH == PH_QKV ? C_QKV : PH == PH_O ? C_O : PH == PH_GU ? C_GU : C_DN;
+      if (ttl) ttl[5] = clk64();
       red_release_gpu_add(ctr + ci, nd);
+      if (ttl) ttl[6] = clk64();
     }
   }
   __syncwarp();
@@ -1103,10 +1215,6 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
   unsigned long long* atl =
       (a.utl && layer == a.n_layers / 2 && blockIdx.x == 0 && threadIdx.x == 0) ? a.utl + 28672 : nullptr;
   if (atl) atl[0] = clk64();
-  if (threadIdx.x == 0) {
-    reinterpret_cast<volatile int*>(s_merge)[0] = ring.k - 1;
-    reinterpret_cast<volatile int*>(s_merge)[1] = ring.k - 1;
-  }
   wait_counter(ctr + C_QKV, a.qkv_tg);  // q, tree rows and their lo parts are written
   if (atl) atl[1] = clk64();
   where(a, WCODE(layer, PH_ATT, 2));
@@ -1141,21 +1249,20 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
   float o[DB][4];
 #pragma unroll
   for (int n = 0; n < DB; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  // Each stream publishes the last ring index it has waited for; a stream may
-  // wait for index k only once the other stream has waited for k - STAGES
-  // (the slot's previous use): mbarrier parity waits must never run a full
-  // ring round ahead of the slot's phase.
-  volatile int* prog = reinterpret_cast<volatile int*>(s_merge);
+  // Tiles go in groups of two (one per stream) -- one when the pair would
+  // need more ring units than there are stages: both streams wait for their
+  // tile's units, compute, meet at a barrier, then every warp releases every
+  // unit of the group once (empty count 8).  Consumption stays in ring order.
   constexpr int STG = StepCfg<NT>::STAGES;
-  for (int it = t0 + ws; it < t1; it += 2) {
+  auto units_of = [&](int x) { return x >= ft ? 2 : 1; };
+  for (int g0 = t0; g0 < t1;) {
+    const int g1 = (g0 + 1 < t1 && units_of(g0) + units_of(g0 + 1) <= STG) ? g0 + 2 : g0 + 1;
+    const int it = g0 + ws;
+    if (it < g1) {
     const bool tree = it >= ft;
     const int ri = ring_of(it);
-    if (lane == 0)
-      while (prog[ws ^ 1] < ri + (tree ? 1 : 0) - STG) __nanosleep(20);
-    __syncwarp();
     const uint32_t shi = ring_wait_at<NT>(ring, ri);
     const uint32_t slo = tree ? ring_wait_at<NT>(ring, ri + 1) : shi;
-    if (rb == 0 && lane == 0) prog[ws] = ri + (tree ? 1 : 0);
     if (atl && it - t0 < 64) atl[16 + (it - t0) * 2] = clk64();
     // S = q K^T: the k16 chains alternate between two accumulator sets
     float sc[1][NB][4];
@@ -1261,18 +1368,17 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
       }
     }
     if (atl && it - t0 < 8) atl[200 + (it - t0) * 4 + 2] = clk64();
-    // this stream's 4 warps read each unit: 2 arrivals each (empty count 8)
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(ring.empty0 + 8 * (ri % StepCfg<NT>::STAGES))
-                   : "memory");
-      if (tree)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(ring.empty0 + 8 * ((ri + 1) % StepCfg<NT>::STAGES))
-                     : "memory");
-    }
     if (atl && it - t0 < 64) atl[16 + (it - t0) * 2 + 1] = clk64();
+    }
+    cbar();
+    if (lane == 0)
+      for (int x = g0; x < g1; ++x) {
+        const int rx = ring_of(x);
+        mbar_arrive_a(ring.empty0 + 8 * (rx % STG));
+        if (x >= ft) mbar_arrive_a(ring.empty0 + 8 * ((rx + 1) % STG));
+      }
+    g0 = g1;
   }
-  if (rb == 0 && lane == 0) prog[ws] = 0x7FFFFFFF;  // this stream is done with the ring
   // this stream's partial -> workspace: O (16 rows x D per warp) and (m, l)
   {
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
@@ -1416,7 +1522,7 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     step_kernel(const StepArgs* __restrict__ ap_g) {
   using C = StepCfg<NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[2], mdone[2];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[2], mdone[4];
   __shared__ int s_done[128];
   __shared__ int s_nd;
   __shared__ float s_rmax[2 * 64];
@@ -1442,10 +1548,8 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 8);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&ardy[i], 8);
-      mbar_init(&mdone[i], 1);
-    }
+    for (int i = 0; i < 2; ++i) mbar_init(&ardy[i], 8);
+    for (int i = 0; i < 4; ++i) mbar_init(&mdone[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) {  // the whole TMEM of the SM (one CTA per SM)
@@ -1471,27 +1575,28 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     if (warp == 8) {
       if (lane == 0) producer<NT>(ap, &s_sched, sm0, full0, empty0);
       where(*ap, WCODE(0xFFFF, 0x40, 0xFF));
-    } else if (warp == 9) {
-      mma_warp<NT>(ap, tc);
+    } else if (warp == 9 || warp == 10) {
+      mma_warp<NT>(ap, tc, warp - 9);
       where(*ap, WCODE(0xFFFF, 0x20, 0xFF));
     }
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_CONSUMER));
   Ring ring{sm0, full0, empty0, 0};
+  uint8_t* s_tail = smem + C::STAGES * C::SLOT;
   int tck = 0;  // W4 units consumed (TMEM buffer / barrier phase)
   const int n_layers = ap->n_layers;
   const bool att = s_sched.att_item >= 0;
   int2 r;
   for (int l = 0; l < n_layers; ++l) {
-    r = gemm_phase<NT, PH_QKV>(ap, &s_sched, l, s_sched.qkv0, s_sched.qkv1, ring, tc, tck, s_done, &s_nd);
+    r = gemm_phase<NT, PH_QKV>(ap, &s_sched, l, s_sched.qkv0, s_sched.qkv1, ring, tc, tck, s_done, &s_nd, s_tail);
     ring.k = r.x; tck = r.y;
     if (att) ring.k = attn_item<NT, D>(ap, &s_sched, l, ring, s_merge, smem + C::STAGES * C::SLOT);
-    r = gemm_phase<NT, PH_O>(ap, &s_sched, l, s_sched.o0, s_sched.o1, ring, tc, tck, s_done, &s_nd);
+    r = gemm_phase<NT, PH_O>(ap, &s_sched, l, s_sched.o0, s_sched.o1, ring, tc, tck, s_done, &s_nd, s_tail);
     ring.k = r.x; tck = r.y;
-    r = gemm_phase<NT, PH_GU>(ap, &s_sched, l, s_sched.gu0, s_sched.gu1, ring, tc, tck, s_done, &s_nd);
+    r = gemm_phase<NT, PH_GU>(ap, &s_sched, l, s_sched.gu0, s_sched.gu1, ring, tc, tck, s_done, &s_nd, s_tail);
     ring.k = r.x; tck = r.y;
-    r = gemm_phase<NT, PH_DN>(ap, &s_sched, l, s_sched.dn0, s_sched.dn1, ring, tc, tck, s_done, &s_nd);
+    r = gemm_phase<NT, PH_DN>(ap, &s_sched, l, s_sched.dn0, s_sched.dn1, ring, tc, tck, s_done, &s_nd, s_tail);
     ring.k = r.x; tck = r.y;
   }
   // stop the MMA warp: an empty A buffer announcement (thread 0 writes the slot
@@ -1499,7 +1604,7 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
   if (threadIdx.x == 0) s_slot[tck & 1] = 0;
   if (lane == 0) mbar_arrive_a(tc.ardy0 + 8 * (tck & 1));
   where(*ap, WCODE(0xFFFE, 0, 0));
-  gemm_phase<NT, PH_LM>(ap, &s_sched, 0, s_sched.lm0, s_sched.lm1, ring, tc, tck, s_done, &s_nd);
+  gemm_phase<NT, PH_LM>(ap, &s_sched, 0, s_sched.lm0, s_sched.lm1, ring, tc, tck, s_done, &s_nd, s_tail);
   tc_fence_before();
   cbar();
   __syncwarp();

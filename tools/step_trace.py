@@ -159,6 +159,13 @@ def main():
         print("  per tile (ready, done):", [(int(at[16 + 2 * j] - b), int(at[17 + 2 * j] - b)) for j in range(min(nt, 8))])
         print("  tile 0/2 (ready, S done, softmax done, PV done):",
               [(int(at[16 + 2 * j] - b), int(at[200 + 4 * j] - b), int(at[201 + 4 * j] - b), int(at[202 + 4 * j] - b)) for j in (0, 2) if j < nt])
+    for ph, name in ((0, "qkv"), (2, "o"), (3, "gu"), (4, "dn")):
+        tt = utl[30000 + ph * 16:30000 + ph * 16 + 9]
+        if tt[0]:
+            b = tt[0]
+            print(f"tail of {name} (finaliser of tile-group 0, layer {n_l // 2}, nd={tt[8]}): clk after loop end: "
+                  f"counted {tt[1]-b}, sent {tt[2]-b if tt[2] else '-'}, received {tt[3]-b if tt[3] else '-'}, "
+                  f"epilogue done {tt[4]-b}, cleaned+fence {tt[5]-b}, released {tt[6]-b}")
     if a.json:
         with open(a.json, "w") as f:
             json.dump(out, f)

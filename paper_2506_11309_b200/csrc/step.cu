@@ -117,6 +117,18 @@ SS_DEV void spin_until_geq(const int* p, int target) {
   (void)ld_acquire_gpu(p);
 }
 
+// GPU-scope atomics with release / acquire semantics: the release is
+// cumulative over the CTA's writes ordered before it by a CTA barrier, so no
+// separate fence.acq_rel.gpu is needed around the arrival counts.
+SS_DEV int atom_add_acqrel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+SS_DEV void atom_add_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 SS_DEV void tmark(const StepArgs& a, int slot, int which) {
   if (a.trace && threadIdx.x == 0) a.trace[((size_t)blockIdx.x * a.trace_slots + slot) * 3 + which] = now_ns();
 }
@@ -1075,12 +1087,11 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
   if (threadIdx.x == 0) {
     int nd = 0;
     if (u1 > u0) {
-      fence_acq_rel_gpu();
       for (int tg = u0 / S; tg <= (u1 - 1) / S; ++tg) {
         const int nst = min(u1, (tg + 1) * S) - max(u0, tg * S);
-        if (atomicAdd(&arr[tg], nst) + nst == S) s_done[nd++] = tg;
+        // release: this CTA's partials; acquire (last arriver): the others'
+        if (atom_add_acqrel_gpu(&arr[tg], nst) + nst == S) s_done[nd++] = tg;
       }
-      if (nd) fence_acq_rel_gpu();  // acquire side: the other CTAs' partials
     }
     *s_nd = nd;
   }
@@ -1156,11 +1167,11 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
   }
   cbar();
   if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();  // epilogue outputs (and the cleaning) before the completion count
+    // the completion counts carry release semantics (cumulative over the
+    // epilogue outputs and the cleaning, ordered by the barrier above)
     if constexpr (PH == PH_LM) {
       int* lmc = a.ctr + (size_t)a.n_layers * kCtrPerLayer;
-      if (atomicAdd(lmc, nd) + nd == a.lm_tg) {
-        fence_acq_rel_gpu();
+      if (atom_add_acqrel_gpu(lmc, nd) + nd == a.lm_tg) {
         where(a, WCODE(layer, PH, 0x10));
         if (a.P > 1) {
           const ArgmaxXArgs x{a.P, a.rank, a.loopback, 2 * a.n_layers, a.h / 128, a.recv, a.peer_recv};
@@ -1403,8 +1414,7 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
   if (atl) atl[2] = clk64();
   cbar();
   if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();
-    atomicAdd(ctr + C_MEET + grp, 1);
+    atom_add_release_gpu(ctr + C_MEET + grp, 1);
     spin_until_geq(ctr + C_MEET + grp, s.att_S);
   }
   cbar();
@@ -1507,10 +1517,7 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
     if (W > 1) cbar();
   }
   cbar();
-  if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();
-    red_release_gpu_add(ctr + C_ATT, 1);
-  }
+  if (threadIdx.x == 0) red_release_gpu_add(ctr + C_ATT, 1);
   if (atl) { atl[4] = clk64(); atl[5] = (unsigned long long)(t1 - t0); atl[6] = (unsigned long long)s.att_S; }
   tmark(a, layer * 5 + PH_ATT, 2);
   where(a, WCODE(layer, PH_ATT, 9));

@@ -401,6 +401,13 @@ def run_ours(args, cfg):
                             "algorithmic_bytes_per_launch": gateup_bytes(cfg, world),
                             "avg_launch_us": per * 1e3, "share_of_step": gu_ms / tot if tot else None}
         line["kernel_times_us"] = {k: {"total": v[0] * 1e3, "launches": v[1]} for k, v in prof.items()}
+    try:  # where the step's time goes (extra traced step, outside the timed region)
+        sm_mhz = line["clocks"].get("sm_mhz") or 1965.0
+        bd = phase_breakdown(sh, cfg, d_tok, d_par, T, n_steps - 2, stream, sm_mhz)
+        if bd:
+            line["breakdown"] = bd
+    except Exception as ex:  # pragma: no cover
+        line["breakdown"] = {"error": str(ex)}
     if world == 1 and not args.no_tp_emulate:
         line["decode_planted"] = decode_planted(sh, cfg, T, L)
         line["tp_emulated"] = tp_emulated(args, cfg, local, dev, peak)
@@ -486,6 +493,47 @@ def decode_planted(sh, cfg, T, L, n_steps=24, mean_emit=3.1, seed=5):
             "how": "host API (ss_verify_tree + ss_commit_accepted per step, wall clock), planted trees"}
 
 
+def phase_breakdown(sh, cfg, d_tok, d_par, T, i0, stream, sm_mhz=1965.0):
+    """One extra step with the persistent kernel's timeline on (ss_step_trace;
+    outside the timed region): the mean critical-path span of each phase over
+    the middle layers (exit of the phase's last CTA minus exit of the previous
+    phase's last CTA, us) and the all-reduce part of the O / down tails of the
+    middle layer (the finaliser of tile-group 0: LL sends + receives, us)."""
+    import torch
+    if not sh.step_kernel_active(T):
+        return None
+    sh.step_trace(True)
+    for i in (i0, i0 + 1):  # the first launch after enabling re-captures the graph
+        sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+    torch.cuda.synchronize()
+    tr, utl = sh.read_step_trace(with_units=True)
+    sh.step_trace(False)
+    tr = tr.astype(np.int64)
+    utl = utl.astype(np.int64)
+    n_l = cfg.n_layers
+    ex = np.where(tr[:, :, 2] > 0, tr[:, :, 2], 0).max(axis=0)  # per slot: exit of the last CTA (ns)
+    names = ["qkv", "attention", "o_allreduce", "gate_up", "down_allreduce"]
+    spans = {k: [] for k in names}
+    for l in range(max(1, n_l // 4), max(2, 3 * n_l // 4)):
+        for p in range(5):
+            prev = ex[l * 5 + p - 1] if p else ex[(l - 1) * 5 + 4]
+            cur = ex[l * 5 + p]
+            if prev > 0 and cur > 0:
+                spans[names[p]].append((cur - prev) / 1e3)
+    out = {"phase_us": {k: round(float(np.mean(v)), 2) for k, v in spans.items() if v},
+           "lm_head_us": round(float((ex[n_l * 5] - ex[(n_l - 1) * 5 + 4]) / 1e3), 2)}
+    ar = {}
+    for ph, name in ((2, "o"), (4, "down")):
+        tt = utl[30000 + ph * 16:30000 + ph * 16 + 9]
+        if tt[0] and tt[3]:
+            ar[name] = round(float((tt[3] - tt[1]) / sm_mhz), 2)  # clk -> us
+    if ar:
+        out["allreduce_us"] = ar
+        out["allreduce_how"] = ("persistent-kernel timeline, finaliser of tile-group 0 of the middle layer: "
+                                "LL sends to every rank + rank-ordered receive, clock64 at the SM clock")
+    return out
+
+
 def tp_emulated(args, cfg, local, dev, peak):
     """Per-GPU step latency of ONE rank of a TP = 2/4/8 group, emulated on this
     single GPU (ss_import_loopback: the rank's weight shard, KV heads and LL
@@ -522,6 +570,12 @@ def tp_emulated(args, cfg, local, dev, peak):
         status = ssp.parse_result(res.cpu().numpy(), T)["status"]  # -5 = a poll ran out of budget
         out[f"tp{P}"] = {"us": ms * 1e3, "bytes_per_gpu": b, "roofline_frac": b / (ms / 1e3) / 1e9 / peak,
                          "status_ok": status == 0}
+        try:
+            bd = phase_breakdown(sh, cfg, d_tok, d_par, T, n - 2, stream)
+            if bd:
+                out[f"tp{P}"].update(bd)
+        except Exception as e:  # measurement extra only
+            out[f"tp{P}"]["breakdown_error"] = str(e)
         sh.close()
     return out
 

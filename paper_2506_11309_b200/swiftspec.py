@@ -50,7 +50,7 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
            "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
-           "ss_step_kernel_active"]
+           "ss_step_kernel_active", "ss_step_trace", "ss_read_step_trace", "ss_step_trace_host"]
 SS_DEBUG_CONSISTENCY = 1
 
 

@@ -38,7 +38,7 @@ __all__ = [
     "bf16_to_f64", "tree_meta", "dequant", "rmsnorm", "silu", "rope", "softmax",
     "attend_node", "argmax_lowest", "accept_walk", "OracleModel", "KVCache",
     "layer_forward", "verify", "commit", "forced_decode", "greedy_decode",
-    "verify_sharded",
+    "verify_sharded", "tp_padded_dims",
 ]
 
 GROUP = 128  # AWQ group size, P:501 ("4-bit AWQ quantization with a group size of 128")
@@ -368,11 +368,52 @@ def greedy_decode(cfg, model, kv: KVCache, root: int, n_tokens: int):
 # two all-reduces per layer are plain sums of the ranks' partials in rank
 # order; argmax is taken over the concatenated vocab shards.
 # ---------------------------------------------------------------------------
+def tp_padded_dims(cfg, P: int):
+    """Arbitrary tensor parallelism by zero padding (SURVEY A13 /
+    NEXT-4): "we increase the number of attention heads so that it is divisible
+    by x" -- kv heads padded to a multiple of P, each with its G = Hq / Hkv query
+    heads -- "and zero-pad" the matrix dimension (intermediate) "so that they are
+    divisible by the number of GPUs x" and by the GEMM block (256 here).
+    Returns (Hq', Hkv', I')."""
+    G = cfg.n_heads // cfg.n_kv_heads
+    hkv = -(-cfg.n_kv_heads // P) * P
+    ip = -(-cfg.intermediate // (256 * P)) * 256 * P if cfg.intermediate % P or (cfg.intermediate // P) % 256 else cfg.intermediate
+    return hkv * G, hkv, ip
+
+
 def verify_sharded(cfg, model: OracleModel, kv: KVCache, tokens, parents, P: int):
-    Hq, Hkv, d, h, I, V = (cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden,
-                           cfg.intermediate, cfg.vocab)
-    if Hkv % P or I % P:
-        raise ValueError("TP size must divide n_kv_heads and intermediate")
+    """Tensor-parallel mode: each rank's partial sums computed separately and
+    added across ranks in rank order (Megatron split).  When P does
+    not divide the heads / intermediate size the weights are zero-padded as the
+    paper describes (padded Q/K/V columns, O rows, gate/up columns
+    and down rows are zero, so "the model output is equivalent of the
+    non-padded model"); tree_k / tree_v are returned for the real heads."""
+    Hq0, Hkv0, d, h, I0, V = (cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden,
+                              cfg.intermediate, cfg.vocab)
+    Hq, Hkv, I = tp_padded_dims(cfg, P)
+
+    def padc(W, n):  # zero columns up to n
+        return np.pad(W, ((0, 0), (0, n - W.shape[1])))
+
+    def padr(W, n):  # zero rows up to n
+        return np.pad(W, ((0, n - W.shape[0]), (0, 0)))
+
+    class _Padded:
+        def w(self, l, name):
+            W = model.w(l, name)
+            if name == "wq":
+                return padc(W, Hq * d)
+            if name in ("wk", "wv"):
+                return padc(W, Hkv * d)
+            if name == "wo":
+                return padr(W, Hq * d)
+            if name in ("wgate", "wup"):
+                return padc(W, I)
+            if name == "wdown":
+                return padr(W, I)
+            return W
+
+    pm = _Padded()
     tokens = np.asarray(tokens)
     L = kv.L
     depth, pos, anc = tree_meta(parents, L)
@@ -386,9 +427,9 @@ def verify_sharded(cfg, model: OracleModel, kv: KVCache, tokens, parents, P: int
         k_all = np.zeros((T, Hkv, d))
         v_all = np.zeros((T, Hkv, d))
         for r in range(P):
-            Wq = model.w(l, "wq")[:, r * hq * d:(r + 1) * hq * d]
-            Wk = model.w(l, "wk")[:, r * hk * d:(r + 1) * hk * d]
-            Wv = model.w(l, "wv")[:, r * hk * d:(r + 1) * hk * d]
+            Wq = pm.w(l, "wq")[:, r * hq * d:(r + 1) * hq * d]
+            Wk = pm.w(l, "wk")[:, r * hk * d:(r + 1) * hk * d]
+            Wv = pm.w(l, "wv")[:, r * hk * d:(r + 1) * hk * d]
             q = (xn @ Wq).reshape(T, hq, d)
             k = (xn @ Wk).reshape(T, hk, d)
             v = (xn @ Wv).reshape(T, hk, d)
@@ -397,14 +438,14 @@ def verify_sharded(cfg, model: OracleModel, kv: KVCache, tokens, parents, P: int
                 k[i] = rope(k[i], pos[i], cfg.rope_theta)
             k_all[:, r * hk:(r + 1) * hk] = k
             v_all[:, r * hk:(r + 1) * hk] = v
-            Kp = kv.K[l][:L, r * hk:(r + 1) * hk]
-            Vp = kv.V[l][:L, r * hk:(r + 1) * hk]
+            Kp = np.pad(kv.K[l][:L], ((0, 0), (0, Hkv - Hkv0), (0, 0)))[:, r * hk:(r + 1) * hk]
+            Vp = np.pad(kv.V[l][:L], ((0, 0), (0, Hkv - Hkv0), (0, 0)))[:, r * hk:(r + 1) * hk]
             attn = np.zeros((T, hq * d))
             for i in range(T):
                 sel = np.nonzero(anc[i])[0]
                 attn[i] = attend_node(q[i], np.concatenate([Kp, k[sel]]),
                                       np.concatenate([Vp, v[sel]]), hk).reshape(-1)
-            parts.append(attn @ model.w(l, "wo")[r * hq * d:(r + 1) * hq * d, :])
+            parts.append(attn @ pm.w(l, "wo")[r * hq * d:(r + 1) * hq * d, :])
         s = parts[0]
         for p_ in parts[1:]:
             s = s + p_
@@ -413,14 +454,14 @@ def verify_sharded(cfg, model: OracleModel, kv: KVCache, tokens, parents, P: int
         parts = []
         for r in range(P):
             sl = slice(r * ip, (r + 1) * ip)
-            hmid = silu(xn2 @ model.w(l, "wgate")[:, sl]) * (xn2 @ model.w(l, "wup")[:, sl])
-            parts.append(hmid @ model.w(l, "wdown")[sl, :])
+            hmid = silu(xn2 @ pm.w(l, "wgate")[:, sl]) * (xn2 @ pm.w(l, "wup")[:, sl])
+            parts.append(hmid @ pm.w(l, "wdown")[sl, :])
         s = parts[0]
         for p_ in parts[1:]:
             s = s + p_
         x = x + s
-        tk.append(k_all)
-        tv.append(v_all)
+        tk.append(k_all[:, :Hkv0])
+        tv.append(v_all[:, :Hkv0])
     xn = rmsnorm(x, model.canon["final_norm"], cfg.rms_eps)
     vp = -(-V // P)
     shards = []

@@ -321,6 +321,27 @@ def test_sharded_sum_equals_unsharded(tiny16):
     assert list(r2["argmax"]) == list(r1["argmax"])
 
 
+@pytest.mark.parametrize("P", [3, 5, 6])
+def test_sharded_zero_padding_equals_unsharded(tiny16, P):
+    """Arbitrary TP by zero padding: heads padded to a multiple of
+    P, intermediate to a multiple of 256 P, all padded weights zero; the
+    rank-ordered sum of the padded shards equals the unpadded, unsharded model
+    (the paper: "the model output is equivalent of the non-padded model")."""
+    cfg, m, kv = tiny16
+    Hq, Hkv, I = O.tp_padded_dims(cfg, P)
+    assert Hkv % P == 0 and Hq == Hkv * (cfg.n_heads // cfg.n_kv_heads) and Hkv >= cfg.n_kv_heads
+    assert I % P == 0 and (I // P) % 256 == 0 and I >= cfg.intermediate
+    rng = np.random.default_rng(23 + P)
+    toks, parents = synth.tree_random(8, cfg.vocab, rng)
+    r1 = O.verify(cfg, m, kv, toks, parents)
+    r2 = O.verify_sharded(cfg, m, kv, toks, parents, P=P)
+    np.testing.assert_allclose(r2["logits"], r1["logits"], rtol=1e-11, atol=1e-11)
+    for l in range(cfg.n_layers):
+        np.testing.assert_allclose(r2["tree_k"][l], r1["tree_k"][l], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(r2["tree_v"][l], r1["tree_v"][l], rtol=1e-12, atol=1e-12)
+    assert list(r2["argmax"]) == list(r1["argmax"])
+
+
 def _planted_tree(cfg, m, kv, depth, T, rng):
     """Tree whose root path of `depth` nodes below the root is the target's greedy
     continuation (computed with plain greedy decoding), plus random distractors."""

@@ -126,10 +126,18 @@ typedef enum {
 /* ---- lifecycle ---------------------------------------------------------- */
 
 /* Create the shard of TP rank tp_rank (0 <= tp_rank < tp_size, tp_size in
- * {1,2,4,8}) on CUDA device `device`: allocates weights, the KV cache
- * [n_layers][n_kv_heads/tp][max_ctx][head_dim] (fp16), workspaces and the
- * peer receive buffers.  *out receives the handle (owned by the caller, free
- * with ss_destroy).  Errors: SS_EINVAL (shape rules above), SS_ECUDA. */
+ * [1, 8]) on CUDA device `device`: allocates weights, the KV cache
+ * [n_layers][ceil(n_kv_heads/tp)][max_ctx][head_dim] (fp16), workspaces and
+ * the peer receive buffers.  *out receives the handle (owned by the caller,
+ * free with ss_destroy).
+ * Arbitrary TP: when tp_size does not divide n_kv_heads, the kv
+ * heads (each with its n_heads/n_kv_heads query heads) are zero-padded to a
+ * multiple of tp_size; when intermediate/tp_size is not a multiple of 256 the
+ * intermediate size is zero-padded to a multiple of 256 tp_size.  Padded
+ * weights and prefix K/V are zero (the loaders and generators fill them), so
+ * results equal the unpadded model's; padded kv heads read back as zeros.
+ * Errors: SS_EINVAL (shape rules above; padded n_heads*head_dim/tp must be a
+ * multiple of 256), SS_ECUDA. */
 ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
                         int32_t device, ss_shard** out);
 

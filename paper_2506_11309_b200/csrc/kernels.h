@@ -150,6 +150,9 @@ void launch_commit(ss_shard* s, int from_result, cudaStream_t st);
 struct LinMap {
   int mode;  // 0 QKV, 1 O, 2 GU, 3 DOWN
   int rank, Hq_l, Hkv_l, d, I_l, Kl, Nl_valid;
+  // unpadded sizes (arbitrary TP by zero padding): global indices
+  // at or beyond them are padding and map to zero weights
+  int q_full, kv_full, I_full, K_full;
 };
 struct SynthLinArgs {
   uint64_t keys[3][3];  // [part][qweight, qzeros, scales] stream keys

@@ -574,15 +574,18 @@ SS_DEV bool lin_map(const LinMap& m, int row, int k, int& part, int& n, int& kk)
     else if (row < nq + nk) { part = 1; n = m.rank * nk + row - nq; }
     else if (row < nq + 2 * nk) { part = 2; n = m.rank * nk + row - nq - nk; }
     else return false;
+    if (n >= (part == 0 ? m.q_full : m.kv_full)) return false;  // zero-padded head
   } else if (m.mode == 1) {
     part = 0; n = row; kk = m.rank * m.Kl + k;
+    if (kk >= m.K_full) return false;
   } else if (m.mode == 2) {
     int tg = row >> 7, r = row & 127;
     part = r < 64 ? 0 : 1;
     n = m.rank * m.I_l + tg * 64 + (r & 63);
-    if (tg * 64 + (r & 63) >= m.I_l) return false;
+    if (tg * 64 + (r & 63) >= m.I_l || n >= m.I_full) return false;
   } else {
     part = 0; n = row; kk = m.rank * m.Kl + k;
+    if (kk >= m.K_full) return false;
   }
   return true;
 }
@@ -709,8 +712,10 @@ __global__ void synth_kv_kernel(uint16_t* cache, int layer, int Hkv_full, int Hk
     int kvh = (int)(r / L);
     uint64_t idx = ((uint64_t)pos * Hkv_full + kv0 + kvh) * d + j;
     // canonical value = bf16(normal) (synth/generators.py); the cache holds it
-    // exactly as fp16
-    const float v = __uint_as_float((uint32_t)bf16_rne_bits(approx_normal(hash_u64(key, idx))) << 16);
+    // exactly as fp16.  Zero-padded heads (arbitrary TP) hold 0.
+    const float v = kv0 + kvh < Hkv_full
+                        ? __uint_as_float((uint32_t)bf16_rne_bits(approx_normal(hash_u64(key, idx))) << 16)
+                        : 0.f;
     size_t base = ((size_t)layer * Hkv_l + kvh) * max_ctx_pad * d;
     cache[base + kv_elem_offset(pos, j, d)] = f32_to_f16_bits(v);
   }

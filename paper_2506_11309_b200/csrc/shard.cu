@@ -150,13 +150,16 @@ static bool lin_map_h(const LinMap& m, int row, int k, int& part, int& n, int& k
     else if (row < nq + nk) { part = 1; n = m.rank * nk + row - nq; }
     else if (row < nq + 2 * nk) { part = 2; n = m.rank * nk + row - nq - nk; }
     else return false;
+    if (n >= (part == 0 ? m.q_full : m.kv_full)) return false;  // zero-padded head
   } else if (m.mode == 1 || m.mode == 3) {
     part = 0; n = row; kk = m.rank * m.Kl + k;
+    if (kk >= m.K_full) return false;  // zero-padded input rows
   } else {
     int tg = row >> 7, r = row & 127;
     part = r < 64 ? 0 : 1;
     if (tg * 64 + (r & 63) >= m.I_l) return false;
     n = m.rank * m.I_l + tg * 64 + (r & 63);
+    if (n >= m.I_full) return false;  // zero-padded intermediate columns
   }
   return true;
 }
@@ -170,6 +173,11 @@ static LinMap make_map(const ss_shard* s, int mode, int Kl) {
   m.d = s->cfg.head_dim;
   m.I_l = s->I_l;
   m.Kl = Kl;
+  const ss_model_cfg& c = s->cfg;
+  m.q_full = c.n_heads * c.head_dim;
+  m.kv_full = c.n_kv_heads * c.head_dim;
+  m.I_full = c.intermediate;
+  m.K_full = mode == 1 ? m.q_full : mode == 3 ? m.I_full : 1 << 30;
   return m;
 }
 
@@ -250,17 +258,25 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   if (!cfg || !out) FAIL(SS_EINVAL, "null argument");
   *out = nullptr;
   const ss_model_cfg& c = *cfg;
-  if (tp_size != 1 && tp_size != 2 && tp_size != 4 && tp_size != 8) FAIL(SS_EINVAL, "tp_size must be 1, 2, 4 or 8");
+  if (tp_size < 1 || tp_size > kMaxPeers) FAIL(SS_EINVAL, "tp_size must be in [1, 8]");
   if (tp_rank < 0 || tp_rank >= tp_size) FAIL(SS_EINVAL, "tp_rank out of range");
   if (c.group_size != SS_GROUP) FAIL(SS_EINVAL, "group_size must be 128");
   if (c.head_dim != 64 && c.head_dim != 128) FAIL(SS_EINVAL, "head_dim must be 64 or 128");
   if (c.n_layers < 1 || c.hidden < 256 || c.vocab < 2 || c.n_heads < 1 || c.n_kv_heads < 1)
     FAIL(SS_EINVAL, "bad model shape");
   if (c.n_heads % c.n_kv_heads) FAIL(SS_EINVAL, "n_heads must be a multiple of n_kv_heads");
-  if (c.n_kv_heads % tp_size || c.intermediate % tp_size) FAIL(SS_EINVAL, "tp_size must divide n_kv_heads and intermediate");
   if (c.hidden % kW4KS) FAIL(SS_EINVAL, "hidden must be a multiple of 256");
-  if ((c.n_heads / tp_size * c.head_dim) % kW4KS) FAIL(SS_EINVAL, "n_heads*head_dim/tp must be a multiple of 256");
-  if ((c.intermediate / tp_size) % kW4KS) FAIL(SS_EINVAL, "intermediate/tp must be a multiple of 256");
+  // Arbitrary TP by zero padding: kv heads (with their query
+  // heads) padded to a multiple of tp_size, the intermediate size to a
+  // multiple of 256 tp_size when tp_size does not split it into 256-multiples;
+  // padded weights are zero, so the padded model equals the unpadded one.
+  const int Hkv_pad = (c.n_kv_heads + tp_size - 1) / tp_size * tp_size;
+  const int Hq_pad = Hkv_pad * (c.n_heads / c.n_kv_heads);
+  const int I_pad = (c.intermediate % tp_size || (c.intermediate / tp_size) % kW4KS)
+                        ? (c.intermediate + kW4KS * tp_size - 1) / (kW4KS * tp_size) * (kW4KS * tp_size)
+                        : c.intermediate;
+  if ((Hq_pad / tp_size * c.head_dim) % kW4KS)
+    FAIL(SS_EINVAL, "padded n_heads*head_dim/tp must be a multiple of 256");
   if (c.hidden > 8192) FAIL(SS_EINVAL, "hidden must be <= 8192");
   if (c.max_tree < 1 || c.max_tree > SS_MAX_TREE) FAIL(SS_EINVAL, "max_tree must be in [1, 64]");
   if (c.max_ctx < c.max_tree) FAIL(SS_EINVAL, "max_ctx too small");
@@ -278,9 +294,9 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   s->P = tp_size;
   s->device = device;
   cudaDeviceGetAttribute(&s->n_sm, cudaDevAttrMultiProcessorCount, device);
-  s->Hq_l = c.n_heads / tp_size;
-  s->Hkv_l = c.n_kv_heads / tp_size;
-  s->I_l = c.intermediate / tp_size;
+  s->Hq_l = Hq_pad / tp_size;
+  s->Hkv_l = Hkv_pad / tp_size;
+  s->I_l = I_pad / tp_size;
   s->G = G;
   int vp = (c.vocab + tp_size - 1) / tp_size;
   s->V_off = tp_rank * vp;
@@ -669,7 +685,8 @@ extern "C" ss_status ss_set_prefix_kv(ss_shard* s, int32_t layer, const void* k,
       for (int pos = 0; pos < len; ++pos)
         for (int j = 0; j < d; ++j) {
           int r = pos & 63, cidx = (j >> 3) ^ (r & 7);
-          buf[(size_t)(pos - r) * d + r * d + cidx * 8 + (j & 7)] = bf16_to_f16(src[((size_t)pos * Hf + kv0 + kh) * d + j]);
+          buf[(size_t)(pos - r) * d + r * d + cidx * 8 + (j & 7)] =
+              kv0 + kh < Hf ? bf16_to_f16(src[((size_t)pos * Hf + kv0 + kh) * d + j]) : (uint16_t)0;  // padded head
         }
       size_t base = ((size_t)layer * s->Hkv_l + kh) * s->max_ctx_pad * d;
       CUDA_TRY(cudaMemcpy(cache + base, buf.data(), (size_t)rows * d * 2, cudaMemcpyHostToDevice));
@@ -919,13 +936,15 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
     n += launch_step(a, reinterpret_cast<const StepArgs*>(s->step_args_dev) + step_args_slot(NT, want_logits), NT,
                      s->launch_cap, st);
     PROF_END();
-    ss_pdl_off = false;
     if (auto_commit) {
+      // fake-peer shards: no PDL here either -- an early-launched commit grid
+      // holds an SM the next shard's persistent grid needs
       PROF_BEGIN(8);
       launch_commit(s, 1, st);
       PROF_END();
       ++n;
     }
+    ss_pdl_off = false;
     return n;
   }
   // timing experiments only (results are wrong; experiment builds only, the

@@ -142,7 +142,9 @@ class Shard:
         vp = -(-cfg.vocab // tp_size)
         self.v_off = tp_rank * vp
         self.v_l = max(0, min(cfg.vocab, (tp_rank + 1) * vp) - self.v_off)
-        self.hkv_l = cfg.n_kv_heads // tp_size
+        # kv heads per rank after the zero padding for tp_size not dividing
+        # n_kv_heads (padded heads read back as zeros)
+        self.hkv_l = -(-cfg.n_kv_heads // tp_size)
 
     def _ck(self, code: int):
         _check(code, self.h)

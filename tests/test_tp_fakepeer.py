@@ -94,6 +94,54 @@ def test_fakepeer_tp_parity(P):
         sh.close()
 
 
+@pytest.mark.parametrize("P", [3, 5, 6])
+def test_fakepeer_tp_zero_padding(P):
+    """Arbitrary TP by zero padding (the paper's 6+2
+    split): P does not divide the 4 kv heads / the intermediate size, the
+    library pads heads and columns with zero weights.  The ranks' logits equal
+    the unpadded model's (oracle: padded sharded == unsharded, pinned in
+    test_oracle), every rank walks the same path, each rank holds its real kv
+    heads of the tree rows and zeros for its padded ones, and 3 auto-commit
+    steps advance L identically."""
+    cfg = synth.CONFIGS["small-tp"]
+    L = 64
+    shards, m, kv = _setup(cfg, P, L)
+    hk = -(-cfg.n_kv_heads // P)
+    rng = np.random.default_rng(40 + P)
+    tokens, parents = synth.tree_paperlike(8, cfg.vocab, rng)
+    outs = _run(shards, tokens, parents)
+    ro = O.verify_sharded(cfg, m, kv, tokens, parents, P)
+    logits = np.concatenate([lg for _, lg in outs], axis=1)
+    err = np.abs(logits - ro["logits"])
+    assert np.all(err <= 2e-2 + 1e-2 * np.abs(ro["logits"])), err.max()
+    res0 = outs[0][0]
+    assert all(res["status"] == 0 for res, _ in outs)
+    for res, _ in outs[1:]:
+        assert res["argmax"] == res0["argmax"] and res["accepted"] == res0["accepted"] and res["bonus"] == res0["bonus"]
+    for i in range(len(tokens)):
+        a, b = res0["argmax"][i], int(ro["argmax"][i])
+        assert a == b or abs(ro["logits"][i][a] - ro["logits"][i][b]) < 2e-2
+    for sh in shards:
+        sh.set_committed_len(L)
+    for r, sh in enumerate(shards):
+        for l in range(cfg.n_layers):
+            k, v = sh.read_kv(l, L, len(tokens))
+            real = max(0, min(hk, cfg.n_kv_heads - r * hk))
+            np.testing.assert_allclose(k[:, :real], ro["tree_k"][l][:, r * hk:r * hk + real], atol=2e-2, rtol=1e-2)
+            np.testing.assert_allclose(v[:, :real], ro["tree_v"][l][:, r * hk:r * hk + real], atol=2e-2, rtol=1e-2)
+            assert np.all(k[:, real:] == 0) and np.all(v[:, real:] == 0)
+    total = 0
+    for step in range(3):
+        tokens, parents = synth.tree_random(8, cfg.vocab, rng)
+        outs = _run(shards, tokens, parents, auto_commit=True)
+        assert all(o[0]["status"] == 0 for o in outs), [o[0]["status"] for o in outs]
+        assert all(o[0]["accepted"] == outs[0][0]["accepted"] for o in outs)
+        total += outs[0][0]["n_accepted"]
+        assert [sh.L for sh in shards] == [L + total] * P, (step, [o[0]["n_accepted"] for o in outs])
+    for sh in shards:
+        sh.close()
+
+
 def test_fakepeer_tp_autocommit_many_steps():
     """Repeated steps exercise the LL flag epochs and both all-reduce buffer
     parities; the committed length advances identically on every rank."""

@@ -265,7 +265,7 @@ def run_ours(args, cfg):
     T, L = args.T, args.L
     n_steps = args.warmup + args.steps
     max_ctx = L + T * (3 * n_steps + 8) + 64
-    sh = pkg.Shard(cfg, rank, world, local, max_ctx=max_ctx, max_tree=max(T, 8))
+    sh = pkg.Shard(cfg, rank, world, local, max_ctx=max_ctx, max_tree=max(T, 32))
     sh.synth_weights(args.seed)
     sh.synth_prefix_kv(args.seed + 1, L)
     if world > 1:
@@ -408,6 +408,8 @@ def run_ours(args, cfg):
             line["breakdown"] = bd
     except Exception as ex:  # pragma: no cover
         line["breakdown"] = {"error": str(ex)}
+    if world == 1 and not args.no_extra:
+        line["other_configs"] = other_configs(args, sh, cfg, local, dev, peak)
     if world == 1 and not args.no_tp_emulate:
         line["decode_planted"] = decode_planted(sh, cfg, T, L)
         line["tp_emulated"] = tp_emulated(args, cfg, local, dev, peak)
@@ -523,7 +525,7 @@ def phase_breakdown(sh, cfg, d_tok, d_par, T, i0, stream, sm_mhz=1965.0):
     out = {"phase_us": {k: round(float(np.mean(v)), 2) for k, v in spans.items() if v},
            "lm_head_us": round(float((ex[n_l * 5] - ex[(n_l - 1) * 5 + 4]) / 1e3), 2)}
     ar = {}
-    for ph, name in ((2, "o"), (4, "down")):
+    for ph, name in (((2, "o"), (4, "down")) if sh.tp_size > 1 else ()):
         tt = utl[30000 + ph * 16:30000 + ph * 16 + 9]
         if tt[0] and tt[3]:
             ar[name] = round(float((tt[3] - tt[1]) / sm_mhz), 2)  # clk -> us
@@ -531,6 +533,51 @@ def phase_breakdown(sh, cfg, d_tok, d_par, T, i0, stream, sm_mhz=1965.0):
         out["allreduce_us"] = ar
         out["allreduce_how"] = ("persistent-kernel timeline, finaliser of tile-group 0 of the middle layer: "
                                 "LL sends to every rank + rank-ordered receive, clock64 at the SM clock")
+    return out
+
+
+def time_steps(sh, cfg, T, n_warm, n_time, dev, seed=13):
+    """Device time per auto-commit step (CUDA events on the launching stream)."""
+    import torch
+    trees = make_trees(cfg, T, n_warm + n_time, seed=seed)
+    d_tok = torch.tensor(np.stack([t for t, _ in trees]), dtype=torch.int32, device=dev)
+    d_par = torch.tensor(np.stack([p for _, p in trees]), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for i in range(n_warm):
+        sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(n_warm, n_warm + n_time):
+        sh.verify_dev(d_tok[i], d_par[i], T, auto_commit=True, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n_time
+
+
+def other_configs(args, sh70, cfg70, local, dev, peak):
+    """The other BASELINE.json TP = 1 workloads on this GPU, same step (whole hot
+    path, auto-commit): 70B-shaped at T = 16 / 32 (the main shard, its prefix
+    rewound to L), Llama3-1B-shaped (T = 16, 1K KV) and 8B-shaped (T = 16, 4K KV).
+    Device time per step, HBM roofline fraction of the step's algorithmic bytes."""
+    import paper_2506_11309_b200 as pkg
+    out = {}
+    L = args.L
+    for T in (16, 32):
+        sh70.set_committed_len(L)
+        ms = time_steps(sh70, cfg70, T, 3, 8, dev)
+        b = step_bytes(cfg70, T, L + 1, 1)
+        out[f"{cfg70.name}/T{T}/L{L}"] = {"us": ms * 1e3, "roofline_frac": b / (ms / 1e3) / 1e9 / peak}
+    for name, T, Lx in (("llama3-1b", 16, 1024), ("llama3-8b", 16, 4096)):
+        c = synth.CONFIGS[name]
+        sh = pkg.Shard(c, 0, 1, local, max_ctx=Lx + 16 * 40 + 64, max_tree=16)
+        sh.synth_weights(args.seed)
+        sh.synth_prefix_kv(args.seed + 1, Lx)
+        ms = time_steps(sh, c, T, 3, 10, dev)
+        b = step_bytes(c, T, Lx + 1, 1)
+        out[f"{name}/T{T}/L{Lx}"] = {"us": ms * 1e3, "roofline_frac": b / (ms / 1e3) / 1e9 / peak}
+        sh.close()
+    out["how"] = "TP 1, paper-like trees, auto-commit steps, CUDA events; weights random (device generator)"
     return out
 
 
@@ -592,6 +639,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tp-emulate", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs (70B T16/32, 1B, 8B)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

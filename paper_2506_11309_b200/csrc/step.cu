@@ -136,8 +136,12 @@ SS_DEV void tmark(const StepArgs& a, int slot, int which) {
 // tcgen05 (5th-gen tensor cores, TMEM accumulators) ------------------------
 // TMEM map of the CTA (512 columns, lane = output row of the 128-row tile):
 //   [0, 256)   A operand, two buffers of one W4 unit (256 k = 128 fp16x2 columns)
-//   [256, 512) fp32 accumulators, [buffer 2][AWQ group 2][N columns]
+//   [256, 512) fp32 accumulators, [slot kNacc][AWQ group 2][N columns]
 constexpr uint32_t kTmemCols = 512, kAccCol = 256;
+// accumulator slots [kNacc][AWQ group 2][N]: 4 at T <= 16 (the two warp sets
+// alternate two each, so a unit's MMAs never write the accumulator the
+// previous unit's epilogue is reading), 2 at T <= 32
+template <int NT> constexpr int kNacc = NT <= 2 ? 4 : 2;
 SS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 SS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 SS_DEV void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -586,6 +590,87 @@ SS_DEV void tc_signal(const Tc& tc, uint32_t sst, int b, int warp, int lane) {
   if (lane == 0) mbar_arrive_a(tc.ardy0 + 8 * b);
 }
 
+// Two-set variant (T <= 16): warps 4 s .. 4 s + 3 (set s) take every other
+// unit; warp (quadrant qd, set s) dequantises BOTH 16-row tiles of its
+// quadrant (rows 32 qd .. 32 qd + 31) -- so each unit is handled by one set
+// while the other set's dequant / store drain / epilogue overlap it.
+SS_DEV void tc_dequant_q(const Tc& tc, uint32_t sst, int b, int qd, int lane) {
+  __syncwarp();  // tcgen05 .sync.aligned: the warp must be converged
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t wbase = sst + (uint32_t)(((2 * qd + h) * 4) * 512 + lane * 16);
+    const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd + 16 * h) << 16) + (uint32_t)(b * 128);
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      const uint4 w = lds128(wbase + kb * 512);
+      uint32_t r[16], af[4];
+      const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dequant8(wv[j], af);
+        r[4 * j + 0] = af[0];
+        r[4 * j + 1] = af[2];
+        r[4 * j + 2] = af[1];
+        r[4 * j + 3] = af[3];
+      }
+      tc_st_16x256b_x4(ta + kb * 32, r);
+    }
+  }
+}
+// The set's 4 warps arrive with count 2 each (ardy count 8); the set's
+// quadrant-0 warp publishes the slot address first.
+SS_DEV void tc_signal_q(const Tc& tc, uint32_t sst, int b, int qd, int lane) {
+  tc_wait_st();
+  tc_fence_before();
+  __syncwarp();
+  if (qd == 0 && lane == 0) tc.slot[b] = sst;
+  if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(tc.ardy0 + 8 * b) : "memory");
+}
+// Epilogue of unit k for rows 32 qd + lane, both AWQ groups.
+template <int NT>
+SS_DEV void tc_epilogue_q(const Tc& tc, uint32_t sst, int k, int qd, int lane, float (&y)[8 * NT]) {
+  constexpr int TP = 8 * NT, N = 16 * NT;
+  const int b = k & 1;
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b), (uint32_t)((k >> 1) & 1));
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b + 1), (uint32_t)((k >> 1) & 1));
+  __syncwarp();
+  tc_fence_after();
+  const int m = 32 * qd + lane, tile = m >> 4, r16 = m & 15, g8 = r16 & 7, up = r16 >> 3;
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const uint32_t zb = lds8(sst + kW4Bytes + 512 + tile * 16 + hh * 8 + g8);
+    const uint32_t sp = lds32(sst + kW4Bytes + tile * 64 + hh * 32 + g8 * 4);
+    const float sc = up ? __uint_as_float(sp & 0xFFFF0000u) * 0.0625f : __uint_as_float(sp << 16);
+    const float cz = up ? 1024.f + 16.f * (float)(zb >> 4) : 1024.f + (float)(zb & 15u);
+    float X[TP];
+    const uint32_t xo = sst + kW4UnitBytes + NT * 8192 + hh * TP * 4;
+#pragma unroll
+    for (int t = 0; t < TP; t += 4) {
+      const uint4 v = lds128(xo + t * 4);
+      X[t] = __uint_as_float(v.x); X[t + 1] = __uint_as_float(v.y);
+      X[t + 2] = __uint_as_float(v.z); X[t + 3] = __uint_as_float(v.w);
+    }
+    const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccCol + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + hh) * N);
+#pragma unroll
+    for (int j = 0; j < (TP + 15) / 16; ++j) {
+      uint32_t rh[16], rl[16];
+      if constexpr (TP == 8) {
+        tc_ld_32x32b_x16(ta, rh);
+      } else {
+        tc_ld_32x32b_x16(ta + 16 * j, rh);
+        tc_ld_32x32b_x16(ta + TP + 16 * j, rl);
+      }
+      tc_wait_ld();
+#pragma unroll
+      for (int t = 0; t < (TP == 8 ? 8 : 16); ++t) {
+        const float hi = __uint_as_float(rh[t]), lo = __uint_as_float(TP == 8 ? rh[8 + t] : rl[t]);
+        y[16 * j + t] = fmaf(sc, fmaf(-cz, X[16 * j + t], hi + lo), y[16 * j + t]);
+      }
+    }
+  }
+  tc_fence_before();
+}
+
 template <int NT>
 SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, float (&y)[8 * NT]) {
   constexpr int TP = 8 * NT, N = 16 * NT;
@@ -610,7 +695,7 @@ SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, f
     X[t] = __uint_as_float(v.x); X[t + 1] = __uint_as_float(v.y);
     X[t + 2] = __uint_as_float(v.z); X[t + 3] = __uint_as_float(v.w);
   }
-  const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccCol + (uint32_t)((b * 2 + hh) * N);
+  const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccCol + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + hh) * N);
   if constexpr (TP == 8) {
     uint32_t r[16];
     tc_ld_32x32b_x16(ta, r);
@@ -654,7 +739,7 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc, in
     tc_fence_after();
     const uint64_t bd0 = smem_desc(sst + kW4UnitBytes, N * 16, 128);
     {
-      const uint32_t d = tc.tbase + kAccCol + (uint32_t)((b * 2 + g) * N);
+      const uint32_t d = tc.tbase + kAccCol + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + g) * N);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int i = g * 8 + ks;
@@ -1031,6 +1116,81 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
         }
       }
     }
+  } else if constexpr (NT <= 2) {
+    // two warp sets on alternating units, in lockstep pairs (p, p + 1): set s
+    // dequantises unit p + s, runs the epilogue of its previous unit, hands the
+    // new one to the MMA warps; after a barrier every warp releases the
+    // previous pair's ring slots (once each: empty count 8)
+    float y[8 * NT];
+#pragma unroll
+    for (int t = 0; t < 8 * NT; ++t) y[t] = 0.f;
+    const int k0 = ring.k;
+    const int ws = warp >> 2, qd = warp & 3;
+    unsigned long long* utl =
+        (a.utl && PH == PH_GU && layer == a.n_layers / 2 && blockIdx.x == 0 && threadIdx.x == 0) ? a.utl : nullptr;
+    if (utl) { utl[127 * 8 + 7] = (unsigned long long)tck; utl[127 * 8 + 6] = (unsigned long long)(u1 - u0); }
+    uint32_t sst_prev = 0;
+    int u_prev = -1;
+    auto release_pair = [&](int q0) {
+      __syncwarp();
+      if (lane == 0)
+        for (int v = q0; v < q0 + 2 && v < u1; ++v) mbar_arrive_a(ring.empty0 + 8 * ((k0 + v - u0) % StepCfg<NT>::STAGES));
+    };
+    auto flush_prev = [&](int v) {
+      const int tg = v / S;
+      if (v + 2 >= u1 || (v + 2) / S != tg) {  // this set's next unit starts another tile-group
+        float* row = accb + ((size_t)tg * 128 + 32 * qd + lane) * TP;
+#pragma unroll
+        for (int t = 0; t < 8 * NT; t += 4) {
+          red_add_v4(row + t, y[t], y[t + 1], y[t + 2], y[t + 3]);
+          y[t] = y[t + 1] = y[t + 2] = y[t + 3] = 0.f;
+        }
+      }
+    };
+    for (int p = u0; p < u1; p += 2) {
+      const int um = p + ws;
+      const bool have = um < u1;
+      uint32_t sst = 0;
+      if (u_prev >= 0) {
+        // the set's previous unit used the same TMEM A buffer: its MMAs must
+        // be complete before the dequant below overwrites it
+        const int kp = tck + (u_prev - u0);
+        mbar_wait_wd(tc.mdone0 + 8 * (2 * (kp & 1)), (uint32_t)((kp >> 1) & 1));
+        mbar_wait_wd(tc.mdone0 + 8 * (2 * (kp & 1) + 1), (uint32_t)((kp >> 1) & 1));
+      }
+      if (have) {
+        if (utl && um - u0 < 127) utl[(um - u0) * 8 + 0] = clk64();
+        sst = ring_wait_at<NT>(ring, k0 + (um - u0));
+        if (utl && um - u0 < 127) utl[(um - u0) * 8 + 1] = clk64();
+        if (p == u0) tmark(a, tslot, 1);
+        tc_dequant_q(tc, sst, (tck + (um - u0)) & 1, qd, lane);
+        if (utl && um - u0 < 127) utl[(um - u0) * 8 + 2] = clk64();
+      }
+      // hand the new unit to the MMA warps first: its MMAs then run during
+      // the previous unit's epilogue and are done before this set's next dequant
+      if (have) tc_signal_q(tc, sst, (tck + (um - u0)) & 1, qd, lane);
+      if (u_prev >= 0) {
+        where(a, WCODE(layer, PH, 3));
+        tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y);
+        if (utl && u_prev - u0 < 127) utl[(u_prev - u0) * 8 + 3] = clk64();
+        flush_prev(u_prev);
+      }
+      cbar();
+      if (p > u0) release_pair(p - 2);
+      u_prev = have ? um : -1;
+      sst_prev = sst;
+    }
+    if (u_prev >= 0) {
+      tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y);
+      if (utl && u_prev - u0 < 127) utl[(u_prev - u0) * 8 + 3] = clk64();
+      flush_prev(u_prev);
+    }
+    if (u1 > u0) {
+      cbar();
+      release_pair(u0 + ((u1 - 1 - u0) & ~1));
+    }
+    ring.k = k0 + (u1 - u0);
+    tck += u1 - u0;
   } else {
     // software pipeline: dequant unit u into TMEM buffer (tck + u - u0) & 1
     // while the MMAs of unit u - 1 run, then its epilogue; flush per tile-group

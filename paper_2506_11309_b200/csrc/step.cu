@@ -201,11 +201,28 @@ struct Sched {
   int L, T;
 };
 
+// Tile-group-aligned split: c = n_ctas / n_tg CTAs per tile-group, each a
+// contiguous chunk of one tile-group, so no CTA finalises two tile-groups
+// (their tails -- all-reduce, RoPE / KV writes -- would run back to back).
+// Used when it does not lengthen the longest range by more than one unit.
+SS_DEV void gemm_range_tg(int n_tg, int S, int n_ctas, int b, int& u0, int& u1) {
+  const int U = n_tg * S;
+  const int c = n_ctas / n_tg;
+  if (c >= 2 && (S + c - 1) / c <= (U + n_ctas - 1) / n_ctas + 1) {
+    if (b >= n_tg * c) { u0 = u1 = 0; return; }
+    const int tg = b / c, j = b % c;
+    u0 = tg * S + j * S / c;
+    u1 = tg * S + (j + 1) * S / c;
+    return;
+  }
+  gemm_range(U, n_ctas, b, u0, u1);
+}
+
 SS_DEV void make_sched(const StepArgs& a, int b, int L, int T, int NT, Sched& s) {
-  gemm_range(a.qkv_tg * a.qkv_S, a.n_ctas, b, s.qkv0, s.qkv1);
-  gemm_range(a.o_tg * a.o_S, a.n_ctas, b, s.o0, s.o1);
-  gemm_range(a.gu_tg * a.gu_S, a.n_ctas, b, s.gu0, s.gu1);
-  gemm_range(a.dn_tg * a.dn_S, a.n_ctas, b, s.dn0, s.dn1);
+  gemm_range_tg(a.qkv_tg, a.qkv_S, a.n_ctas, b, s.qkv0, s.qkv1);
+  gemm_range_tg(a.o_tg, a.o_S, a.n_ctas, b, s.o0, s.o1);
+  gemm_range_tg(a.gu_tg, a.gu_S, a.n_ctas, b, s.gu0, s.gu1);
+  gemm_range_tg(a.dn_tg, a.dn_S, a.n_ctas, b, s.dn0, s.dn1);
   gemm_range(a.lm_tg * a.lm_S, a.n_ctas, b, s.lm0, s.lm1);
   const int KT = att_tile_keys(a.d);
   const int ntiles = (L + T + KT - 1) / KT;

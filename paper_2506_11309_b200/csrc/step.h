@@ -86,7 +86,7 @@ struct StepArgs {
   int V_l = 0, V_off = 0, logits_ld = 0;
   float* logits = nullptr;
   int n_ctas = 0;
-  int att_min_tiles = 4;      // fewest K/V tiles per attention split
+  int att_min_tiles = 2;      // fewest K/V tiles per attention split
   // optional timeline (ss_step_trace): per CTA, per (layer, phase) slot, three
   // %globaltimer stamps: phase entry, first unit ready, phase exit
   unsigned long long* trace = nullptr;

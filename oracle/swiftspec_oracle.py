@@ -38,7 +38,8 @@ __all__ = [
     "bf16_to_f64", "tree_meta", "dequant", "rmsnorm", "silu", "rope", "softmax",
     "attend_node", "argmax_lowest", "accept_walk", "OracleModel", "KVCache",
     "layer_forward", "verify", "commit", "forced_decode", "greedy_decode",
-    "verify_sharded", "tp_padded_dims",
+    "verify_sharded", "tp_padded_dims", "nonsquare_mask", "layer_forward_nonsquare",
+    "forward_nonsquare",
 ]
 
 GROUP = 128  # AWQ group size, P:501 ("4-bit AWQ quantization with a group size of 128")
@@ -321,7 +322,97 @@ def verify(cfg, model: OracleModel, kv: KVCache, tokens, parents, want_logits: b
     am = np.array([argmax_lowest(r) for r in logits], dtype=np.int64)
     acc, bonus = accept_walk(tokens, parents, am)                         # a11
     return dict(logits=logits if want_logits else None, argmax=am, accepted=acc,
-                bonus=bonus, tree_k=tk, tree_v=tv, depth=depth, pos=pos, anc=anc)
+                bonus=bonus, tree_k=tk, tree_v=tv, depth=depth, pos=pos, anc=anc,
+                tokens=tokens, parents=np.asarray(parents))
+
+
+# ---------------------------------------------------------------------------
+# Non-square mask: "for the draft model ... with a
+# current tree of size 6, and we want to calculate the logits of 4 probable
+# leaves, then regarding the tree cache, we only calculate the attention of
+# each leave with its ancestor on the tree (and also all the data that is in
+# the prefix cache). In this case, we need a mask of at least size (4, 10)".
+# The tree cache holds nodes [0, T0) whose K/V earlier calls computed (P:339
+# "the KV states of the tree are stored right after the prefix"); the w leaves
+# [T0, T0 + w) are computed now, each against the prefix, its cached ancestors
+# and its new ancestors-or-self.
+# ---------------------------------------------------------------------------
+def nonsquare_mask(parents_all, T0: int, L: int):
+    """Returns (pos int[w], mask bool[w][T0 + w]) of the leaves [T0, T0 + w) of
+    the tree `parents_all` (every node, root first): mask[i][j] = node j is an
+    ancestor-or-self of leaf T0 + i (brute-force parent walk)."""
+    parents_all = [int(p) for p in parents_all]
+    T = len(parents_all)
+    if not (0 <= T0 < T):
+        raise ValueError("need 0 <= T0 < T (at least one leaf)")
+    depth, pos, anc = tree_meta(parents_all, L)
+    return pos[T0:], anc[T0:, :]
+
+
+def layer_forward_nonsquare(cfg, model: OracleModel, layer: int, x, kv: KVCache, L: int, pos, mask,
+                            tree_k, tree_v):
+    """One decoder layer over the w leaves only (a2-a9), float64.  x [w][h]:
+    the leaves' residual streams; tree_k / tree_v [T0][Hkv][d]: this layer's
+    cached tree K/V; mask [w][T0 + w] (nonsquare_mask).  Returns (x', leaf K
+    [w][Hkv][d], leaf V)."""
+    w = x.shape[0]
+    Hq, Hkv, d = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+    xn = rmsnorm(x, model.norm(layer, "attn_norm"), cfg.rms_eps)          # a2
+    q = model.matmul(layer, "wq", xn).reshape(w, Hq, d)                   # a3
+    k = model.matmul(layer, "wk", xn).reshape(w, Hkv, d)
+    v = model.matmul(layer, "wv", xn).reshape(w, Hkv, d)
+    for i in range(w):                                                    # a4: RoPE at L + depth
+        q[i] = rope(q[i], pos[i], cfg.rope_theta)
+        k[i] = rope(k[i], pos[i], cfg.rope_theta)
+    Kt = np.concatenate([tree_k, k], axis=0)                              # tree cache + leaves
+    Vt = np.concatenate([tree_v, v], axis=0)
+    attn = np.zeros((w, Hq * d))
+    Kp, Vp = kv.K[layer][:L], kv.V[layer][:L]
+    for i in range(w):                                                    # a5: non-square mask row i
+        sel = np.nonzero(mask[i])[0]
+        keys = np.concatenate([Kp, Kt[sel]], axis=0)
+        vals = np.concatenate([Vp, Vt[sel]], axis=0)
+        attn[i] = attend_node(q[i], keys, vals, Hkv).reshape(-1)
+    x = x + model.matmul(layer, "wo", attn)                               # a6
+    xn2 = rmsnorm(x, model.norm(layer, "mlp_norm"), cfg.rms_eps)          # a7
+    hmid = silu(model.matmul(layer, "wgate", xn2)) * model.matmul(layer, "wup", xn2)  # a8
+    x = x + model.matmul(layer, "wdown", hmid)                            # a9
+    return x, k, v
+
+
+def forward_nonsquare(cfg, model: OracleModel, kv: KVCache, tree, tokens_new, parents_new,
+                      want_logits: bool = True):
+    """Forward of w new leaves on top of a tree cache (P:321 non-square mask).
+
+    tree: None (empty cache, T0 = 0) or the dict a previous verify /
+    forward_nonsquare returned for the same committed cache (tokens, parents,
+    tree_k, tree_v, argmax of its T0 nodes).  parents_new[i] indexes the whole
+    tree (< T0 + i; -1 only for node 0).  Returns the grown tree's dict:
+    logits [w][V] of the leaves, argmax of all T0 + w nodes (the cached nodes'
+    from `tree`), tree_k / tree_v of all nodes, pos / mask of the leaves, and
+    the greedy accept walk (a11) over the whole grown tree."""
+    L = kv.L
+    T0 = 0 if tree is None else len(tree["tokens"])
+    toks_all = np.concatenate([np.asarray(tree["tokens"] if tree else [], dtype=np.int64),
+                               np.asarray(tokens_new, dtype=np.int64)])
+    par_all = [int(p) for p in (list(tree["parents"]) if tree else [])] + [int(p) for p in parents_new]
+    pos, mask = nonsquare_mask(par_all, T0, L)                            # a0 (leaves)
+    x = model.embed_rows(np.asarray(tokens_new))                          # a1
+    tk, tv = [], []
+    for l in range(cfg.n_layers):
+        ck = tree["tree_k"][l] if tree else np.zeros((0, cfg.n_kv_heads, cfg.head_dim))
+        cv = tree["tree_v"][l] if tree else np.zeros((0, cfg.n_kv_heads, cfg.head_dim))
+        x, k, v = layer_forward_nonsquare(cfg, model, l, x, kv, L, pos, mask, ck, cv)
+        tk.append(np.concatenate([ck, k], axis=0))
+        tv.append(np.concatenate([cv, v], axis=0))
+    xn = rmsnorm(x, model.canon["final_norm"], cfg.rms_eps)              # a10
+    logits = model.logits(xn)
+    am_new = np.array([argmax_lowest(r) for r in logits], dtype=np.int64)
+    am = np.concatenate([np.asarray(tree["argmax"] if tree else [], dtype=np.int64), am_new])
+    acc, bonus = accept_walk(toks_all, par_all, am)                       # a11 over the grown tree
+    return dict(logits=logits if want_logits else None, argmax=am, accepted=acc, bonus=bonus,
+                tree_k=tk, tree_v=tv, tokens=toks_all, parents=np.array(par_all, dtype=np.int64),
+                pos=pos, mask=mask)
 
 
 def commit(kv: KVCache, res: dict, accepted) -> KVCache:

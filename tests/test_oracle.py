@@ -426,3 +426,76 @@ def test_streamed_weights_equal_dense():
     b = O.verify(cfg, streamed, kv, toks, par)
     np.testing.assert_allclose(b["logits"], a["logits"], rtol=1e-12, atol=1e-12)
     assert list(a["argmax"]) == list(b["argmax"])
+
+
+# ---------------------------------------------------------------- non-square mask (NEXT-3)
+def test_nonsquare_mask_shape_and_rows_fig():
+    """a current tree of size 6 and 4 leaves to compute need a mask of
+    size (4, 10); each row is the leaf's ancestors-or-self (brute force: walk
+    the parents by hand), the prefix is not part of the mask."""
+    parents = [-1, 0, 0, 1, 1, 2, 3, 5, 4, 0]   # nodes 0..5 cached, leaves 6..9
+    pos, mask = O.nonsquare_mask(parents, 6, L=20)
+    assert mask.shape == (4, 10)
+    want = {6: {6, 3, 1, 0}, 7: {7, 5, 2, 0}, 8: {8, 4, 1, 0}, 9: {9, 0}}
+    for i, leaf in enumerate(range(6, 10)):
+        assert set(np.nonzero(mask[i])[0]) == want[leaf]
+    assert list(pos) == [20 + 3, 20 + 3, 20 + 3, 20 + 1]
+
+
+def _split_tree(toks, parents, T0):
+    return list(toks[:T0]), list(parents[:T0]), list(toks[T0:]), list(parents[T0:])
+
+
+def test_forward_nonsquare_empty_cache_equals_verify(tiny16):
+    """T0 = 0: the non-square forward of the whole tree is the square verify."""
+    cfg, m, kv = tiny16
+    toks, parents = synth.tree_paperlike(8, cfg.vocab, np.random.default_rng(31))
+    r1 = O.verify(cfg, m, kv, toks, parents)
+    r2 = O.forward_nonsquare(cfg, m, kv, None, toks, parents)
+    np.testing.assert_allclose(r2["logits"], r1["logits"], rtol=1e-12, atol=1e-12)
+    assert list(r2["argmax"]) == list(r1["argmax"]) and r2["accepted"] == r1["accepted"]
+
+
+@pytest.mark.parametrize("cuts", [(5,), (3, 7), (1, 2, 4, 9)])
+def test_forward_nonsquare_growth_equals_square_verify(tiny16, cuts):
+    """Growing a tree by non-square forwards (the draft's expansions, P:321,
+    Alg. 1) gives every node the logits and K/V of the square verify of
+    the whole tree, and the accept walk over the grown tree is the same."""
+    cfg, m, kv = tiny16
+    toks, parents = synth.tree_random(12, cfg.vocab, np.random.default_rng(32))
+    full = O.verify(cfg, m, kv, toks, parents)
+    bounds = [0, *cuts, 12]
+    tree = None
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        tree = O.forward_nonsquare(cfg, m, kv, tree, toks[a:b], parents[a:b])
+        np.testing.assert_allclose(tree["logits"], full["logits"][a:b], rtol=1e-10, atol=1e-10)
+        assert tree["mask"].shape == (b - a, b)
+    for l in range(cfg.n_layers):
+        np.testing.assert_allclose(tree["tree_k"][l], full["tree_k"][l], rtol=1e-11, atol=1e-11)
+        np.testing.assert_allclose(tree["tree_v"][l], full["tree_v"][l], rtol=1e-11, atol=1e-11)
+    assert list(tree["argmax"]) == list(full["argmax"])
+    assert tree["accepted"] == full["accepted"] and tree["bonus"] == full["bonus"]
+
+
+def test_forward_nonsquare_chain_one_leaf_at_a_time_is_sequential_decode(tiny16):
+    """A chain grown one leaf per call is plain sequential decoding:
+    leaf i's logits equal forced single-token decoding of the chain prefix."""
+    cfg, m, kv = tiny16
+    chain = [11, 250, 3, 4000, 17]
+    seq = O.forced_decode(cfg, m, kv.copy(), chain)
+    tree = None
+    for i, t in enumerate(chain):
+        tree = O.forward_nonsquare(cfg, m, kv, tree, [t], [i - 1])
+        np.testing.assert_allclose(tree["logits"][0], seq[i], rtol=1e-10, atol=1e-10)
+    kv_seq = kv.copy()
+    O.forced_decode(cfg, m, kv_seq, chain)
+    kv_tree = O.commit(kv.copy(), tree, list(range(len(chain))))
+    for l in range(cfg.n_layers):
+        np.testing.assert_allclose(kv_tree.K[l][:kv_tree.L], kv_seq.K[l][:kv_seq.L], rtol=1e-12, atol=1e-12)
+
+
+def test_nonsquare_mask_rejects_bad_split():
+    with pytest.raises(ValueError):
+        O.nonsquare_mask([-1, 0, 1], 3, 0)   # no leaf
+    with pytest.raises(ValueError):
+        O.nonsquare_mask([-1, 0, 2], 1, 0)   # parent not earlier

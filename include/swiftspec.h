@@ -241,6 +241,31 @@ ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t
                              int32_t T, ss_verify_result* d_result, float* d_logits,
                              int32_t auto_commit, void* stream);
 
+/* Non-square forward ("Non-square mask support"):
+ * grow the pending tree by w new nodes and compute only them.  The pending
+ * tree's first T0 nodes (from the last ss_verify_tree / ss_extend_tree since
+ * the last commit; T0 <= its size, nodes >= T0 are discarded) keep their K/V
+ * rows [L, L+T0) -- "the KV states of the tree are stored right after the
+ * prefix".  New node T0+i (token tokens[i], parent parents[i] in
+ * [0, T0+i), or -1 only when T0+i == 0) attends to the L prefix rows, its
+ * cached ancestors and its new ancestors-or-self: a w x (T0+w) mask, e.g.
+ * (4, 10) for a tree of 6 and 4 leaves.  Its K/V go to row L+T0+i;
+ * cached rows enter as fp16 (like committed rows, R18).  T0 = 0 is
+ * ss_verify_tree.  The step replays the graph of ceil(w/8) (graphs
+ * per width; the tree offset is device state).
+ * out: argmax[j] for every node j < T0+w (cached nodes keep the argmax of the
+ * call that computed them) and the greedy accept walk over the whole grown
+ * tree; logits_out: nullable float[w][vocab_shard], the new nodes only.
+ * The tree stays pending: commit any root-anchored chain of its T0+w nodes
+ * with ss_commit_kv / ss_commit_accepted, or discard it.
+ * Errors: SS_EINVAL (w out of [1, 32], T0+w > max_tree, bad parents /
+ * tokens, T0 > 0 with a tp_size whose step cannot run the persistent
+ * kernel), SS_ESTATE (T0 > 0 without a pending tree of >= T0 nodes, T0 == 0
+ * with one; weights / peers missing), SS_ECAPACITY (L+T0+w > max_ctx),
+ * SS_ECUDA; device failures as ss_verify_tree. */
+ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0, int32_t w,
+                         ss_verify_result* out, float* logits_out, void* stream);
+
 /* Commit a root-anchored chain of tree nodes from the last verify:
  * accepted[0] == 0 and accepted[k] a child of accepted[k-1] (any such chain,
  * not only the accepted one: chain prefill, EOS truncation).  K/V rows

@@ -43,13 +43,18 @@ __device__ inline void argmax_exchange(const ArgmaxXArgs& e, DevState* st) {
 }
 
 // Greedy accept walk (a11; R6, R7) on the device.
+// A non-square forward (T0 > 0, ss_extend_tree) computed slots t = nodes
+// T0 + t; the cached nodes keep the argmax of the call that computed them, and
+// the walk runs over the whole grown tree of T0 + T nodes.
 __device__ inline void accept_walk_dev(DevState* st) {
-  int T = st->T;
+  const int T0 = st->T0;
+  const int T = T0 + st->T;
   ss_verify_result& res = st->result;
   for (int i = 0; i < SS_MAX_TREE; ++i) {
-    unsigned long long k = i < T ? __ldcg(&st->argmax_key[i]) : 0ull;
-    res.argmax[i] = i < T ? (int)argmax_key_index(k) : 0;
-    st->argmax_key[i] = 0ull;
+    const int t = i - T0;  // slot of node i
+    unsigned long long k = (t >= 0 && t < st->T) ? __ldcg(&st->argmax_key[t]) : 0ull;
+    if (i >= T0) res.argmax[i] = i < T ? (int)argmax_key_index(k) : 0;
+    if (i < SS_MAX_TREE) st->argmax_key[i] = 0ull;
   }
   int cur = 0, n = 1;
   res.accepted[0] = 0;

@@ -56,6 +56,35 @@ inline ss_status check_verify(const CallState& c, int32_t T, std::string& err) {
   return SS_OK;
 }
 
+// A non-square forward (ss_extend_tree): w new nodes on the first T0 nodes of
+// the pending tree.  Parents index the whole tree.
+inline ss_status check_extend(const CallState& c, const int32_t* tokens, const int32_t* parents, int32_t T0,
+                              int32_t w, std::string& err) {
+  if (!tokens || !parents) { err = "null tree"; return SS_EINVAL; }
+  if (w < 1 || w > 32) { err = "w out of [1, 32]"; return SS_EINVAL; }
+  if (T0 < 0 || T0 + w > c.max_tree) { err = "T0 + w out of [1, max_tree]"; return SS_EINVAL; }
+  for (int i = 0; i < w; ++i) {
+    const int node = T0 + i;
+    if (node == 0 ? parents[i] != -1 : (parents[i] < 0 || parents[i] >= node)) {
+      err = "parents[i] must be in [0, T0 + i) (-1 only for node 0)";
+      return SS_EINVAL;
+    }
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) { err = "token out of vocab"; return SS_EINVAL; }
+  }
+  if (!c.weights_ready) { err = "weights not fully loaded"; return SS_ESTATE; }
+  if (!c.peers_ready) { err = "peers not imported (tp_size > 1)"; return SS_ESTATE; }
+  if (T0 > 0 && (!c.have_verify || T0 > c.last_T)) {
+    err = "T0 > 0 needs a pending tree of at least T0 nodes";
+    return SS_ESTATE;
+  }
+  if (T0 == 0 && c.have_verify) {
+    err = "a verify is pending: commit or discard it, or extend it (T0 > 0)";
+    return SS_ESTATE;
+  }
+  if ((int64_t)c.L + T0 + w > c.max_ctx) { err = "L + T0 + w exceeds max_ctx"; return SS_ECAPACITY; }
+  return SS_OK;
+}
+
 // A commit of a root-anchored chain of the last verified tree.
 inline ss_status check_commit(const CallState& c, const int32_t* accepted, int32_t n, std::string& err) {
   if (!accepted) { err = "null argument"; return SS_EINVAL; }
@@ -89,6 +118,12 @@ inline void on_verify(CallState& c, int32_t T, const int32_t* parents, bool auto
   } else {
     c.have_verify = true;
   }
+}
+inline void on_extend(CallState& c, int32_t T0, int32_t w, const int32_t* parents) {
+  for (int i = 0; i < w && T0 + i < SS_MAX_TREE; ++i) c.last_parents[T0 + i] = parents[i];
+  c.last_T = T0 + w;
+  if (c.L_known && c.L + T0 + w > c.max_written) c.max_written = c.L + T0 + w;
+  c.have_verify = true;
 }
 inline void on_commit(CallState& c, int32_t n) {
   c.L += n;

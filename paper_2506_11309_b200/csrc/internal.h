@@ -46,6 +46,10 @@ struct DevState {
   uint4* mbox_out;           // draft group's outbox (peer-mapped), nullptr = none
   int32_t debug;             // SS_DEBUG_* flags (ss_set_debug)
   int32_t mbox_tmo;          // the current step's inbox message never (fully) arrived
+  // non-square forward (ss_extend_tree): the step computes nodes
+  // [T0, T0 + T) of a tree whose nodes [0, T0) are cached at rows [L, L + T0);
+  // token slot t is node T0 + t.  0 for a square verify.
+  int32_t T0;
 };
 
 // One packed linear (W4 format, see common.cuh) or bf16 matrix.

@@ -134,7 +134,7 @@ int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st);
 
 // embed + tree metadata (a0, a1) + first RMSNorm into the frag activation
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
-                       cudaStream_t st, bool from_mailbox = false, bool step_mode = false);
+                       cudaStream_t st, bool from_mailbox = false, bool step_mode = false, int T0 = 0);
 // a13 mailbox helpers for the draft side (and tests)
 void launch_mailbox_post(void* inbox, const int32_t* tokens, const int32_t* parents, int T, uint32_t seq,
                          cudaStream_t st);

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
                                                          int V, int h, float* x, const uint16_t* gain,
                                                          uint8_t* act, int NT, float eps, int epoch_stride,
                                                          const uint4* mbox_in, int max_tree, ConsistencyArgs ca,
-                                                         StepIngest si) {
+                                                         StepIngest si, int T0) {
   __shared__ int s_tok[SS_MAX_TREE], s_par[SS_MAX_TREE];
   __shared__ int s_bad;
   __shared__ int s_T;
@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
   const int tid = threadIdx.x;
   // graph capacity: the step was captured for 8*NT token slots (and the KV /
   // RoPE capacity checks assumed max_tree): larger trees are refused
-  const int cap = min(8 * NT, max_tree);
+  // non-square forward (ss_extend_tree): slots are nodes [T0, T0 + T)
+  // of a tree whose nodes [0, T0) are cached; the mailbox carries whole trees
+  if (mbox_in) T0 = 0;
+  const int cap = max(0, min(8 * NT, max_tree - T0));
   if (tid == 0) s_tmo = 0;
   // a13: the tree arrives in the inbox as LL lines ("sends a
   // sub-graph ... to the target worker"): line 0 = (T, seq), line 1+i =
@@ -138,27 +141,37 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
   }
   if (tid < T) {
     int p = mbox_in ? (int)mpar : parents[tid], tk = mbox_in ? (int)mtok : tokens[tid];
-    bool bad = (tid == 0) ? (p != -1) : (p < 0 || p >= tid);
+    const int node = T0 + tid;  // parents index the whole tree
+    bool bad = (node == 0) ? (p != -1) : (p < 0 || p >= node);
     bad = bad || tk < 0 || tk >= V;
     if (bad) atomicOr(&s_bad, 1);
-    s_par[tid] = (tid == 0) ? -1 : ((p < 0 || p >= tid) ? 0 : p);
+    s_par[tid] = (node == 0) ? -1 : ((p < 0 || p >= node) ? 0 : p);
     s_tok[tid] = (tk < 0 || tk >= V) ? 0 : tk;
   }
   __syncthreads();
   const int t = blockIdx.x, part = blockIdx.y;
   if (t == 0 && part == 0 && tid < SS_MAX_TREE) {
-    if (tid < T) {
+    if (tid >= T0 && tid < T0 + T) {
+      // walk the new nodes' parents; a cached ancestor contributes its stored
+      // ancestor mask and depth (pos - L)
       unsigned long long anc = 0;
-      int dep = -1;
-      for (int j = tid; j != -1; j = s_par[j]) {
+      int dep = 0, j = tid;
+      while (j >= T0) {
         anc |= 1ull << j;
+        j = s_par[j - T0];
         ++dep;
+      }
+      if (j >= 0) {
+        anc |= st->anc[j];
+        dep += st->pos[j] - st->L;
+      } else {
+        dep -= 1;
       }
       st->anc[tid] = anc;
       st->pos[tid] = st->L + dep;
-      st->tokens[tid] = s_tok[tid];
-      st->parents[tid] = s_par[tid];
-    } else {
+      st->tokens[tid] = s_tok[tid - T0];
+      st->parents[tid] = s_par[tid - T0];
+    } else if (tid >= T0) {
       st->anc[tid] = 0ull;
       st->pos[tid] = st->L;
       st->tokens[tid] = -1;
@@ -166,15 +179,16 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     }
     if (tid == 0) {
       st->T = T;
+      st->T0 = T0;
       int status = s_bad ? SS_EINVAL : SS_OK;
       // LL flag epoch of this step: flags epoch + [0, epoch_stride) are used
       // by the all-reduces and the argmax exchange; 0 is never a live flag.
       uint32_t e = st->epoch + (uint32_t)epoch_stride;
       if (e < st->epoch || e + (uint32_t)epoch_stride < e) e = 1;
       st->epoch = e;
-      st->max_written = max(st->max_written, st->L + T);
+      st->max_written = max(st->max_written, st->L + T0 + T);
       if ((st->debug & SS_DEBUG_CONSISTENCY) && ca.P > 1) {
-        uint32_t hsh = 2166136261u ^ (uint32_t)T_in;
+        uint32_t hsh = (2166136261u ^ (uint32_t)T_in) * 16777619u ^ (uint32_t)T0;
         for (int i = 0; i < T; ++i) {
           hsh = (hsh ^ (uint32_t)s_tok[i]) * 16777619u;
           hsh = (hsh ^ (uint32_t)s_par[i]) * 16777619u;
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
 }
 
 void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parents, int T, int NT,
-                       cudaStream_t st, bool from_mailbox, bool step_mode) {
+                       cudaStream_t st, bool from_mailbox, bool step_mode, int T0) {
   const uint16_t* g0 = s->layers[0].attn_norm;
   ConsistencyArgs ca;
   ca.rank = s->rank;
@@ -325,7 +339,7 @@ void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parent
   launch_pdl(embed_meta_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, s->dstate, tokens, parents, T,
              (const uint16_t*)s->embed, s->cfg.vocab, s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
              2 * s->cfg.n_layers + 2, from_mailbox ? (const uint4*)s->mbox_in : (const uint4*)nullptr,
-             s->cfg.max_tree, ca, si);
+             s->cfg.max_tree, ca, si, T0);
 }
 
 // ---------------------------------------------------------------- a13 draft-side helpers

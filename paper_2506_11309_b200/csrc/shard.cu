@@ -1069,12 +1069,12 @@ static ss_status check_ready(ss_shard* s, int T) {
 }
 
 static ss_status run_step(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int T, int auto_commit,
-                          int want_logits, cudaStream_t st, bool from_mailbox = false) {
+                          int want_logits, cudaStream_t st, bool from_mailbox = false, int T0 = 0) {
   const int NT = nt_of(T);
   Graph* gr;
   ss_status r = get_graph(s, NT, auto_commit, want_logits, &gr);
   if (r != SS_OK) return r;
-  launch_embed_meta(s, d_tokens, d_parents, T, NT, st, from_mailbox, step_path(s, NT));
+  launch_embed_meta(s, d_tokens, d_parents, T, NT, st, from_mailbox, step_path(s, NT), T0);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaGraphLaunch(gr->exec, st));
   return SS_OK;
@@ -1118,6 +1118,42 @@ extern "C" ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const in
   return SS_OK;
 }
 
+extern "C" ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0,
+                                    int32_t w, ss_verify_result* out, float* logits_out, void* stream) {
+  SCOPE(s);
+  if (!s || !out) FAIL(SS_EINVAL, "null argument");
+  s->hs.weights_ready = weights_complete(s);
+  s->hs.peers_ready = s->P == 1 || s->peers_ready;
+  if (!s->hs.L_known) {
+    ss_status r = sync_L(s);
+    if (r != SS_OK) return r;
+  }
+  HOST_CHECK(check_extend, s->hs, tokens, parents, T0, w);
+  // the cached-tree offset is handled by the persistent step kernel only
+  if (T0 > 0 && !step_path(s, nt_of(w))) FAIL(SS_EINVAL, "T0 > 0 needs the persistent step kernel (w <= 32)");
+  cudaSetDevice(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::memcpy(s->h_tree_in, tokens, w * 4);
+  std::memcpy(s->h_tree_in + SS_MAX_TREE, parents, w * 4);
+  CUDA_TRY(cudaMemcpyAsync(s->d_tree_in, s->h_tree_in, 2 * SS_MAX_TREE * 4, cudaMemcpyHostToDevice, st));
+  ss_status r = run_step(s, s->d_tree_in, s->d_tree_in + SS_MAX_TREE, w, 0, logits_out != nullptr, st, false, T0);
+  if (r != SS_OK) return r;
+  CUDA_TRY(cudaMemcpyAsync(&s->hstate->result, &s->dstate->result, sizeof(ss_verify_result), cudaMemcpyDeviceToHost,
+                           st));
+  if (logits_out)
+    CUDA_TRY(cudaMemcpy2DAsync(logits_out, (size_t)s->V_l * 4, s->logits_dev, (size_t)s->V_l_pad * 4,
+                               (size_t)s->V_l * 4, w, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::memcpy(out, &s->hstate->result, sizeof(ss_verify_result));
+  if (out->status != SS_OK) {
+    s->hs.max_written = std::max(s->hs.max_written, s->hs.L + T0 + w);
+    s->hs.have_verify = false;  // the tree is no longer usable
+    FAIL((ss_status)out->status, status_msg(out->status));
+  }
+  ss::host::on_extend(s->hs, T0, w, parents);
+  return SS_OK;
+}
+
 extern "C" ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t* d_parents, int32_t T,
                                         ss_verify_result* d_result, float* d_logits, int32_t auto_commit,
                                         void* stream) {
@@ -1146,9 +1182,10 @@ static ss_status read_last_tree(ss_shard* s, cudaStream_t st, int32_t* status) {
                            cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&s->hstate->result.status, &s->dstate->result.status, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&s->hstate->T, &s->dstate->T, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&s->hstate->T0, &s->dstate->T0, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   *status = s->hstate->result.status;
-  s->hs.last_T = s->hstate->T;
+  s->hs.last_T = s->hstate->T0 + s->hstate->T;  // nodes of the pending tree
   return SS_OK;
 }
 
@@ -1447,7 +1484,7 @@ extern "C" ss_status ss_read_tree_meta(ss_shard* s, int32_t* T, int32_t* pos, ui
   cudaSetDevice(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(s->hstate, s->dstate, sizeof(DevState), cudaMemcpyDeviceToHost));
-  *T = s->hstate->T;
+  *T = s->hstate->T0 + s->hstate->T;  // nodes of the tree (cached + this step's)
   std::memcpy(pos, s->hstate->pos, sizeof(s->hstate->pos));
   std::memcpy(anc, s->hstate->anc, sizeof(s->hstate->anc));
   if (tokens) std::memcpy(tokens, s->hstate->tokens, sizeof(s->hstate->tokens));

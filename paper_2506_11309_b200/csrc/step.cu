@@ -198,7 +198,7 @@ struct Sched {
   int qkv0, qkv1, o0, o1, gu0, gu1, dn0, dn1, lm0, lm1;
   // attention: item of this CTA (grp = kvh * Z + z, split), tiles [t0, t1)
   int att_item, att_S, att_Z, att_A, att_t0, att_t1, att_KT;
-  int L, T;
+  int L, T, T0;  // committed length, token slots, cached tree nodes (slot t = node T0 + t)
 };
 
 // Tile-group-aligned split: c = n_ctas / n_tg CTAs per tile-group, each a
@@ -218,14 +218,14 @@ SS_DEV void gemm_range_tg(int n_tg, int S, int n_ctas, int b, int& u0, int& u1) 
   gemm_range(U, n_ctas, b, u0, u1);
 }
 
-SS_DEV void make_sched(const StepArgs& a, int b, int L, int T, int NT, Sched& s) {
+SS_DEV void make_sched(const StepArgs& a, int b, int L, int T, int T0, int NT, Sched& s) {
   gemm_range_tg(a.qkv_tg, a.qkv_S, a.n_ctas, b, s.qkv0, s.qkv1);
   gemm_range_tg(a.o_tg, a.o_S, a.n_ctas, b, s.o0, s.o1);
   gemm_range_tg(a.gu_tg, a.gu_S, a.n_ctas, b, s.gu0, s.gu1);
   gemm_range_tg(a.dn_tg, a.dn_S, a.n_ctas, b, s.dn0, s.dn1);
   gemm_range(a.lm_tg * a.lm_S, a.n_ctas, b, s.lm0, s.lm1);
   const int KT = att_tile_keys(a.d);
-  const int ntiles = (L + T + KT - 1) / KT;
+  const int ntiles = (L + T0 + T + KT - 1) / KT;  // prefix + cached tree rows + new rows
   const int Z = (a.G * 8 * NT + 63) / 64;           // 64-row chunks of the G x T rows per kv head
   const int groups = a.Hkv_l * Z;
   int S = a.n_ctas / groups;
@@ -248,6 +248,7 @@ SS_DEV void make_sched(const StepArgs& a, int b, int L, int T, int NT, Sched& s)
   }
   s.L = L;
   s.T = T;
+  s.T0 = T0;
 }
 
 // A tile whose rows reach the tree rows [L, L+T) waits for the QKV epilogue
@@ -850,6 +851,7 @@ template <int NT>
 SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, const Sched& s, const TailSm<NT>& ts) {
   constexpr int TP = NT * 8, IT = 128 * TP / 256;
   const int T = s.T, L = s.L, d = a.d, half = d >> 1;
+  const int R = L + s.T0;  // row of slot 0 (a non-square forward appends after the cached tree rows)
   const int nq = a.Hq_l * d, nk = a.Hkv_l * d;
   const float* ssa = a.ss + (size_t)layer * 2 * 64;
   const int wb = L & ~63;
@@ -858,7 +860,7 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
   stage_acc<NT>(acc, ts.acc);
   if (threadIdx.x < T) {
     ts.rs[threadIdx.x] = norm_scale(ssa, threadIdx.x, a.h, a.eps);
-    ts.pos[threadIdx.x] = a.st->pos[threadIdx.x];
+    ts.pos[threadIdx.x] = a.st->pos[s.T0 + threadIdx.x];
   }
   cbar();
   float2 cs[IT];
@@ -893,12 +895,13 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
       uint16_t* c = isk ? a.kc : a.vc;
       uint16_t* lo = isk ? a.klo : a.vlo;
       const size_t base = ((size_t)layer * a.Hkv_l + kvh) * a.max_ctx_pad * d;
-      c[base + kv_elem_offset(L + t, j, d)] = __half_as_ushort(hh);
-      lo[(size_t)kvh * 128 * d + kv_elem_offset(L + t - wb, j, d)] = __half_as_ushort(hl);
+      c[base + kv_elem_offset(R + t, j, d)] = __half_as_ushort(hh);
+      lo[(size_t)kvh * 128 * d + kv_elem_offset(R + t - wb, j, d)] = __half_as_ushort(hl);
     }
   }
-  // zero the lo window rows outside the tree of this tile-group's K / V heads
-  // (a tree tile's prefix rows add q . 0)
+  // zero the lo window rows outside this step's new rows of this tile-group's
+  // K / V heads (a tree tile's prefix rows -- and the cached tree rows of a
+  // non-square forward, fp16 like committed rows -- add q . 0)
   const int row0 = tg * 128;
   if (row0 + 127 >= nq && row0 < nq + 2 * nk) {
     for (int hd = 0; hd < 128 / d; ++hd) {
@@ -910,7 +913,7 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
       for (int i = threadIdx.x; i < 128 * d / 8; i += 256) {
         const int w = i / (d / 8);
         const int pos = wb + w;
-        if (pos >= L && pos < L + T) continue;
+        if (pos >= R && pos < R + T) continue;
         *reinterpret_cast<uint4*>(lo + (size_t)w * d + (i % (d / 8)) * 8) = make_uint4(0, 0, 0, 0);
       }
     }
@@ -1410,7 +1413,7 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
   const int rbg = z * 4 + rb;
   const int ra = rb * 16 + gq, rbr = ra + 8;  // rows within the chunk
   const int rowA = z * 64 + ra, rowB = z * 64 + rbr;
-  const int tokA = min(rowA / G, SS_MAX_TREE - 1), tokB = min(rowB / G, SS_MAX_TREE - 1);
+  const int tokA = min(s.T0 + rowA / G, SS_MAX_TREE - 1), tokB = min(s.T0 + rowB / G, SS_MAX_TREE - 1);
   const unsigned long long ancA = st->anc[tokA], ancB = st->anc[tokB];
   const bool okA = rowA < Mrows, okB = rowB < Mrows;
   const float sl2 = rsqrtf((float)D) * 1.4426950408889634f;
@@ -1482,8 +1485,9 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
       }
     }
     if (atl && it - t0 < 8) atl[200 + (it - t0) * 4] = clk64();
-    // mask (prefix always visible; tree keys by ancestor bit; beyond L + T
-    // never), scale, tile row maxima over the quad
+    // mask (prefix always visible; tree keys -- cached and new -- by ancestor
+    // bit, the non-square mask of P:321; beyond L + T0 + T never), scale, tile
+    // row maxima over the quad
     const int kbase = it * KT;
     float mxA = -INFINITY, mxB = -INFINITY;
 #pragma unroll
@@ -1493,7 +1497,7 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
         const int key = kbase + n * 8 + 2 * tq + (e & 1);
         const unsigned long long anc = (e < 2) ? ancA : ancB;
         const bool ok = (e < 2) ? okA : okB;
-        const bool vis = ok && (key < L || (key < L + T && ((anc >> (key - L)) & 1ull)));
+        const bool vis = ok && (key < L || (key < L + s.T0 + T && ((anc >> (key - L)) & 1ull)));
         const float v = vis ? sc[0][n][e] * sl2 : -INFINITY;
         sc[0][n][e] = v;
         if (e < 2) mxA = fmaxf(mxA, v); else mxB = fmaxf(mxB, v);
@@ -1752,7 +1756,7 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
   // everything below reads the ingest kernel's outputs (T, L, tree, counters)
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x == 0) make_sched(*ap, blockIdx.x, ap->st->L, ap->st->T, NT, s_sched);
+  if (threadIdx.x == 0) make_sched(*ap, blockIdx.x, ap->st->L, ap->st->T, ap->st->T0, NT, s_sched);
   __syncthreads();
   if (warp >= 8) {  // warpgroup 2: producer, MMA issuer, two idle warps
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_AUX));

@@ -46,7 +46,7 @@ _lib = None
 EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_local_peers", "ss_import_loopback",
            "ss_set_launch_cap", "ss_destroy", "ss_last_error", "ss_load_weights", "ss_synth_weights",
            "ss_set_prefix_kv", "ss_synth_prefix_kv", "ss_read_kv", "ss_set_committed_len",
-           "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_commit_kv",
+           "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_extend_tree", "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
            "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
@@ -91,6 +91,7 @@ def lib():
         "ss_committed_len": (i32, [vp]),
         "ss_verify_tree": (i32, [vp, vp, vp, i32, C.POINTER(VerifyResultC), vp, vp]),
         "ss_verify_tree_dev": (i32, [vp, vp, vp, i32, vp, vp, i32, vp]),
+        "ss_extend_tree": (i32, [vp, vp, vp, i32, i32, C.POINTER(VerifyResultC), vp, vp]),
         "ss_commit_kv": (i32, [vp, vp, i32, vp]),
         "ss_commit_accepted": (i32, [vp, vp]),
         "ss_kernels_per_step": (i32, [vp, i32, i32]),
@@ -263,6 +264,21 @@ class Shard:
         n = res.n_accepted
         return dict(n_accepted=n, accepted=list(res.accepted[:n]), bonus=res.bonus_token,
                     argmax=list(res.argmax[:T]), status=res.status, logits=logits)
+
+    def extend(self, tokens, parents, T0: int, want_logits: bool = False, stream=None):
+        """Non-square forward (ss_extend_tree): w = len(tokens) new nodes
+        T0.. on the first T0 nodes of the pending tree; parents index the whole
+        tree.  argmax covers all T0 + w nodes; logits the new nodes only."""
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        p = np.ascontiguousarray(parents, dtype=np.int32)
+        w = len(t)
+        res = VerifyResultC()
+        logits = np.zeros((w, self.v_l), dtype=np.float32) if want_logits else None
+        self._ck(lib().ss_extend_tree(self.h, _ptr(t), _ptr(p), T0, w, C.byref(res),
+                                    _ptr(logits) if want_logits else None, _stream_handle(stream)))
+        n = res.n_accepted
+        return dict(n_accepted=n, accepted=list(res.accepted[:n]), bonus=res.bonus_token,
+                    argmax=list(res.argmax[:T0 + w]), status=res.status, logits=logits)
 
     def verify_dev(self, d_tokens, d_parents, T: int, d_result=None, d_logits=None,
                    auto_commit: bool = False, stream=None):

@@ -32,6 +32,13 @@ int hl_check_verify(void* p, int T) { return ss::host::check_verify(*static_cast
 int hl_check_commit(void* p, const int32_t* a, int n) {
   return ss::host::check_commit(*static_cast<CallState*>(p), a, n, g_msg);
 }
+int hl_check_extend(void* p, const int32_t* t, const int32_t* par, int T0, int w) {
+  return ss::host::check_extend(*static_cast<CallState*>(p), t, par, T0, w, g_msg);
+}
+void hl_on_extend(void* p, int T0, int w, const int32_t* par) {
+  ss::host::on_extend(*static_cast<CallState*>(p), T0, w, par);
+}
+int hl_last_T(void* p) { return static_cast<CallState*>(p)->last_T; }
 int hl_check_set_len(void* p, int L) { return ss::host::check_set_len(*static_cast<CallState*>(p), L, g_msg); }
 void hl_on_verify(void* p, int T, const int32_t* par, int auto_commit) {
   ss::host::on_verify(*static_cast<CallState*>(p), T, par, auto_commit != 0);

@@ -32,7 +32,9 @@ def hl(tmp_path_factory):
                          ("hl_check_commit", i32, [vp, vp, i32]), ("hl_check_set_len", i32, [vp, i32]),
                          ("hl_on_verify", None, [vp, i32, vp, i32]), ("hl_on_commit", None, [vp, i32]),
                          ("hl_on_set_len", None, [vp, i32]), ("hl_L", i32, [vp]), ("hl_have_verify", i32, [vp]),
-                         ("hl_max_written", i32, [vp]), ("hl_msg", C.c_char_p, [])]:
+                         ("hl_max_written", i32, [vp]), ("hl_msg", C.c_char_p, []),
+                         ("hl_check_extend", i32, [vp, vp, vp, i32, i32]),
+                         ("hl_on_extend", None, [vp, i32, i32, vp]), ("hl_last_T", i32, [vp])]:
         f = getattr(L, n)
         f.restype = res
         f.argtypes = args
@@ -154,3 +156,51 @@ def test_ecuda_without_device():
     h = C.c_void_p()
     assert pkg.lib().ss_init_shard(C.byref(cfg), 0, 1, 0, C.byref(h)) == ECUDA
     assert not h.value and pkg.lib().ss_last_error(None)
+
+
+# ---- non-square forward (ss_extend_tree)
+def test_extend_call_order_and_growth(hl, st):
+    t, tp = _a([5, 6, 7, 8])
+    par, pp = _a([0, 1, 1, 3])
+    assert hl.hl_check_extend(st, tp, pp, 2, 4) == ESTATE        # nothing pending
+    root, rp = _a([-1, 0])
+    assert hl.hl_check_extend(st, tp, rp, 0, 2) == OK             # T0 = 0: a square verify
+    hl.hl_on_verify(st, 2, rp, 0)
+    assert hl.hl_check_extend(st, tp, rp, 0, 2) == ESTATE         # T0 = 0 while pending
+    assert hl.hl_check_extend(st, tp, pp, 3, 4) == ESTATE         # T0 beyond the pending tree
+    assert hl.hl_check_extend(st, tp, pp, 2, 4) == OK
+    hl.hl_on_extend(st, 2, 4, pp)
+    assert hl.hl_last_T(st) == 6 and hl.hl_have_verify(st) == 1 and hl.hl_max_written(st) == 70
+    # the grown tree's chains commit: 0 -> 1 -> 3 -> 5 (nodes 3, 5 added by the extension)
+    ch, chp = _a([0, 1, 3, 5])
+    assert hl.hl_check_commit(st, chp, 4) == OK
+    bad, bp = _a([0, 1, 4, 5])   # 5's parent is 3
+    assert hl.hl_check_commit(st, bp, 4) == EINVAL
+
+
+@pytest.mark.parametrize("T0,w,parents,tokens,code", [
+    (2, 1, [2], [1], EINVAL),          # parent must be < T0 + i
+    (2, 2, [0, 3], [1, 1], EINVAL),    # second new node's parent is itself
+    (2, 1, [-1], [1], EINVAL),         # only node 0 is a root
+    (2, 1, [0], [4096], EINVAL),       # token out of vocab
+    (2, 0, [0], [1], EINVAL),          # w < 1
+    (2, 33, [0] * 33, [1] * 33, EINVAL),  # w > 32
+    (10, 7, [0] * 7, [1] * 7, EINVAL),    # T0 + w > max_tree (16)
+    (2, 2, [0, 2], [1, 1], OK),
+])
+def test_extend_einval(hl, st, T0, w, parents, tokens, code):
+    root, rp = _a([-1, 0] + [0] * 14)
+    hl.hl_on_verify(st, 16, rp, 0)
+    t, tp = _a(tokens)
+    p, pp = _a(parents)
+    assert hl.hl_check_extend(st, tp, pp, T0, w) == code
+
+
+def test_extend_ecapacity(hl, st):
+    root, rp = _a([-1, 0, 1, 2])
+    hl.hl_set(st, 1, 1, 250, 250)
+    hl.hl_on_verify(st, 4, rp, 0)
+    t, tp = _a([1, 1, 1])
+    p, pp = _a([3, 4, 5])
+    assert hl.hl_check_extend(st, tp, pp, 4, 3) == ECAPACITY       # 250 + 4 + 3 > max_ctx 256
+    assert hl.hl_check_extend(st, tp, pp, 4, 2) == OK              # 250 + 4 + 2 = 256 fits

@@ -50,12 +50,11 @@ __device__ inline void accept_walk_dev(DevState* st) {
   const int T0 = st->T0;
   const int T = T0 + st->T;
   ss_verify_result& res = st->result;
-  for (int i = 0; i < SS_MAX_TREE; ++i) {
+  for (int i = T0; i < SS_MAX_TREE; ++i) {
     const int t = i - T0;  // slot of node i
-    unsigned long long k = (t >= 0 && t < st->T) ? __ldcg(&st->argmax_key[t]) : 0ull;
-    if (i >= T0) res.argmax[i] = i < T ? (int)argmax_key_index(k) : 0;
-    if (i < SS_MAX_TREE) st->argmax_key[i] = 0ull;
+    res.argmax[i] = i < T ? (int)argmax_key_index(__ldcg(&st->argmax_key[t])) : 0;
   }
+  for (int t = 0; t < SS_MAX_TREE; ++t) st->argmax_key[t] = 0ull;
   int cur = 0, n = 1;
   res.accepted[0] = 0;
   while (true) {

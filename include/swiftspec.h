@@ -266,6 +266,74 @@ ss_status ss_verify_tree_dev(ss_shard* s, const int32_t* d_tokens, const int32_t
 ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0, int32_t w,
                          ss_verify_result* out, float* logits_out, void* stream);
 
+/* Draft worker.  ss_extend_tree_topk: the same
+ * non-square forward as ss_extend_tree, returning for each new node the K
+ * (1..32) most probable tokens of this rank's vocab slice -- the children the
+ * maximum-likelihood expansion adds -- as global token ids top_tok
+ * [w][K] (-1 past the slice) with their logits top_logit[w][K] (larger first,
+ * ties -> lower id), and the slice's log-sum-exp lse[w].  A node's value
+ * log softmax = logit - log(sum over ranks of exp(lse_rank)).
+ * Host outputs, filled before return.  Errors as ss_extend_tree, plus
+ * SS_EINVAL for K out of range / null outputs. */
+ss_status ss_extend_tree_topk(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0, int32_t w,
+                              int32_t K, int32_t* top_tok, float* top_logit, float* lse, ss_verify_result* out,
+                              void* stream);
+
+/* Re-root with KV reorganisation (draft side): commit the root-
+ * anchored chain path[0..n) of the pending tree (rows L + path[k] -> L + k,
+ * L += n, as ss_commit_kv) and keep the subtree keep[0..m) -- ascending node
+ * indices, keep[0] a child of path[n-1] (or the root 0 when n == 0), every
+ * other kept node's parent kept -- packed right after the new prefix (rows
+ * L_old + keep[j] -> L_new + j): "reorganizes the remaining sub-tree ... into
+ * the next positions available, discarding the KV states that are no longer
+ * useful".  Kept node keep[j] becomes node j of the pending tree
+ * (positions unchanged: pos = L + depth, both shift by n), which a later
+ * ss_extend_tree(T0 <= m) grows; m == 0 leaves nothing pending.  Synchronises.
+ * Errors: SS_ESTATE (no pending tree / its step failed), SS_EINVAL (not a
+ * chain, keep not such a subtree, n + m out of [1, tree size]). */
+ss_status ss_reroot(ss_shard* s, const int32_t* path, int32_t n, const int32_t* keep, int32_t m, void* stream);
+
+/* Parallel tree generation (Alg. 1): greedy
+ * speculative decoding of n_tokens tokens with a draft shard and a target
+ * shard linked only by the a13 mailboxes.  Draft branch (calling thread):
+ * expand the w most probable leaves d times (ss_extend_tree_topk, children =
+ * top-K, K = w when 0, values = log softmax), get the verified path,
+ * re-root and reorganise the draft KV (ss_reroot), expand while the
+ * target root's subtree has < bs nodes, post the most probable bs-node
+ * subgraph.  Target branch (its own thread): mailbox-driven verify
+ * steps with auto-commit (ss_verify_tree_mailbox).  mode 0 = async (the draft
+ * expands while the target verifies -- the paper's design); mode 1 = serial
+ * (draft, then verify; the d expansions precede each post).  eos >= 0 stops
+ * at that bonus token.  Both shards must hold the same committed prefix and
+ * nothing pending; root_token = the last prompt token (in neither cache, R9).
+ * out_tokens[n_tokens] receives the emitted tokens -- with greedy acceptance
+ * exactly the target's greedy continuation of root_token.  Single-
+ * rank shards on one device; run them concurrently by capping their grids
+ * (ss_set_launch_cap) so both fit the SMs.  Afterwards the target has
+ * committed at least the emitted tokens' prefix, the draft's tree is
+ * discarded.  Errors: SS_EINVAL (arguments), SS_ESTATE (a pending verify),
+ * SS_ETIMEOUT (mailbox), errors of the calls above. */
+typedef struct {
+  int32_t bs;        /* target batch: nodes per verified subgraph (paper: 8) */
+  int32_t w;         /* leaves per draft expansion (paper: 8) */
+  int32_t d;         /* expansions per round (t_target / t_draft) */
+  int32_t K;         /* children per expanded node (0: w) */
+  int32_t n_tokens;  /* tokens to generate */
+  int32_t eos;       /* stop token (-1: none) */
+  int32_t mode;      /* 0 async, 1 serial */
+} ss_spec_cfg;
+typedef struct {
+  int32_t n_emitted;     /* tokens written to out_tokens */
+  int32_t steps;         /* verify results received */
+  int32_t target_steps;  /* verify steps the target ran (async: one more may run) */
+  int32_t expansions;    /* draft forwards */
+  int32_t accepted;      /* accepted draft tokens (emitted = accepted + one bonus per step) */
+  double wall_ms;        /* host wall time of the loop */
+} ss_spec_stats;
+ss_status ss_speculative_decode(ss_shard* target, ss_shard* draft, int32_t root_token, const ss_spec_cfg* cfg,
+                                int32_t* out_tokens, ss_spec_stats* stats, void* target_stream,
+                                void* draft_stream);
+
 /* Commit a root-anchored chain of tree nodes from the last verify:
  * accepted[0] == 0 and accepted[k] a child of accepted[k-1] (any such chain,
  * not only the accepted one: chain prefill, EOS truncation).  K/V rows

@@ -99,6 +99,41 @@ inline ss_status check_commit(const CallState& c, const int32_t* accepted, int32
   return SS_OK;
 }
 
+// ss_reroot (draft KV reorganisation): commit a root-anchored
+// chain path[0..n) of the pending tree and keep the subtree keep[0..m)
+// (ascending node indices; keep[0] a child of path[n-1], or the root when
+// n == 0; every other kept node's parent kept before it) as the new pending
+// tree, packed right after the new prefix.
+inline ss_status check_reroot(const CallState& c, const int32_t* path, int32_t n, const int32_t* keep, int32_t m,
+                              std::string& err) {
+  if ((n > 0 && !path) || (m > 0 && !keep)) { err = "null argument"; return SS_EINVAL; }
+  if (!c.have_verify) { err = "re-root without a pending tree"; return SS_ESTATE; }
+  if (n < 0 || m < 0 || n + m < 1 || n + m > c.last_T) { err = "n, m out of range"; return SS_EINVAL; }
+  if (n > 0) {
+    ss_status r = check_commit(c, path, n, err);
+    if (r != SS_OK) return r;
+  }
+  for (int j = 0; j < m; ++j) {
+    if (keep[j] < 0 || keep[j] >= c.last_T || (j > 0 && keep[j] <= keep[j - 1])) {
+      err = "keep must be ascending node indices of the pending tree";
+      return SS_EINVAL;
+    }
+    const int32_t p = c.last_parents[keep[j]];
+    bool ok;
+    if (j == 0) {
+      ok = n > 0 ? p == path[n - 1] : keep[0] == 0;
+    } else {
+      ok = false;
+      for (int i = 0; i < j; ++i) ok = ok || keep[i] == p;
+    }
+    if (!ok) {
+      err = "keep is not a subtree rooted at a child of the chain's last node";
+      return SS_EINVAL;
+    }
+  }
+  return SS_OK;
+}
+
 // ss_set_committed_len: truncate, or grow only over rows that hold data.
 inline ss_status check_set_len(const CallState& c, int32_t L, std::string& err) {
   if (L < 0 || (int64_t)L + c.max_tree > c.max_ctx) { err = "length out of range"; return SS_ECAPACITY; }
@@ -129,6 +164,21 @@ inline void on_commit(CallState& c, int32_t n) {
   c.L += n;
   if (c.L > c.max_written) c.max_written = c.L;
   c.have_verify = false;
+}
+inline void on_reroot(CallState& c, const int32_t* path, int32_t n, const int32_t* keep, int32_t m) {
+  int32_t par[SS_MAX_TREE];
+  for (int j = 0; j < m; ++j) {
+    const int32_t p = c.last_parents[keep[j]];
+    par[j] = -1;
+    for (int i = 0; i < j; ++i)
+      if (keep[i] == p) par[j] = i;
+  }
+  for (int j = 0; j < m; ++j) c.last_parents[j] = par[j];
+  (void)path;
+  c.L += n;
+  if (c.L + m > c.max_written) c.max_written = c.L + m;
+  c.last_T = m;
+  c.have_verify = m > 0;
 }
 inline void on_set_len(CallState& c, int32_t L) {
   c.L = L;

@@ -50,6 +50,10 @@ struct DevState {
   // [T0, T0 + T) of a tree whose nodes [0, T0) are cached at rows [L, L + T0);
   // token slot t is node T0 + t.  0 for a square verify.
   int32_t T0;
+  // ss_reroot (draft KV reorganisation): the kept subtree's nodes,
+  // packed after the committed chain (commit_n / commit_chain)
+  int32_t keep_n;
+  int32_t keep[SS_MAX_TREE];
 };
 
 // One packed linear (W4 format, see common.cuh) or bf16 matrix.
@@ -129,6 +133,7 @@ struct ss_shard {
   ss::DevState* dstate = nullptr;  // device
   ss::DevState* hstate = nullptr;  // pinned host mirror for results
   int32_t* d_tree_in = nullptr;    // device staging for host trees [2*64]
+  int32_t* d_topk = nullptr;       // draft top-K output: tokens [32][32], logits [32][32], lse [32]
   int32_t* h_tree_in = nullptr;    // pinned staging
   ss::host::CallState hs;          // host view: committed length, pending verify, rows written
   std::string err;                 // message of the last failed call on this shard

@@ -130,6 +130,11 @@ void warm_step_kernels();
 void warm_gemm_kernels();
 void warm_attention_kernels();
 void warm_misc_kernels();
+void warm_draft_kernels();
+// draft worker (draft.cu): top-K + log-sum-exp of the last step's logits rows,
+// and the re-root KV reorganisation (DevState commit_chain / keep lists)
+void launch_topk(ss_shard* s, int w, int K, int32_t* d_tok, float* d_val, float* d_lse, cudaStream_t st);
+void launch_reroot(ss_shard* s, cudaStream_t st);
 int launch_attention(const AttnArgs& a, int max_ctas, cudaStream_t st);
 
 // embed + tree metadata (a0, a1) + first RMSNorm into the frag activation

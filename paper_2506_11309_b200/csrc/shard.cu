@@ -287,6 +287,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   warm_gemm_kernels();
   warm_attention_kernels();
   warm_misc_kernels();
+  warm_draft_kernels();
   warm_step_kernels();
   ss_shard* s = new ss_shard();
   s->cfg = c;
@@ -399,6 +400,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   }
   A(s->dstate, sizeof(DevState));
   A(s->d_tree_in, 2 * SS_MAX_TREE * 4);
+  A(s->d_topk, (32 * 32 * 2 + 32) * 4);
   if (cudaMallocHost((void**)&s->hstate, sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost((void**)&s->h_tree_in, 2 * SS_MAX_TREE * 4) != cudaSuccess) {
     set_err("cudaMallocHost failed");
@@ -453,7 +455,8 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
                   s->sc_gu.accum, s->sc_gu.counters, s->sc_down.accum, s->sc_down.counters, s->sc_lm.accum,
                   s->sc_lm.counters, s->sc_o.ss, s->sc_o.nbar, s->sc_down.ss, s->sc_down.nbar, s->step_ctr,
                   s->step_ss, s->qf, s->klo, s->vlo, s->att_ws, s->att_ml, s->layer_tab, s->sc_qkv.ss,
-                  s->sc_qkv.nbar, s->sc_gu.ss, s->sc_gu.nbar, s->sc_lm.ss, s->sc_lm.nbar, s->step_args_dev};
+                  s->sc_qkv.nbar, s->sc_gu.ss, s->sc_gu.nbar, s->sc_lm.ss, s->sc_lm.nbar, s->step_args_dev,
+                  s->d_topk};
   if (s->step_trace_host) cudaFreeHost(s->step_trace_host);
   else if (s->step_trace) cudaFree(s->step_trace);
   for (void* p : ptrs)
@@ -1118,10 +1121,13 @@ extern "C" ss_status ss_verify_tree(ss_shard* s, const int32_t* tokens, const in
   return SS_OK;
 }
 
-extern "C" ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0,
-                                    int32_t w, ss_verify_result* out, float* logits_out, void* stream) {
-  SCOPE(s);
+static ss_status read_last_tree(ss_shard* s, cudaStream_t st, int32_t* status);
+
+static ss_status extend_impl(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0, int32_t w,
+                             ss_verify_result* out, float* logits_out, int32_t K, int32_t* top_tok,
+                             float* top_logit, float* lse, void* stream) {
   if (!s || !out) FAIL(SS_EINVAL, "null argument");
+  if (K != 0 && (K < 1 || K > 32 || !top_tok || !top_logit || !lse)) FAIL(SS_EINVAL, "K out of [1, 32] / null top-K output");
   s->hs.weights_ready = weights_complete(s);
   s->hs.peers_ready = s->P == 1 || s->peers_ready;
   if (!s->hs.L_known) {
@@ -1136,10 +1142,22 @@ extern "C" ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const in
   std::memcpy(s->h_tree_in, tokens, w * 4);
   std::memcpy(s->h_tree_in + SS_MAX_TREE, parents, w * 4);
   CUDA_TRY(cudaMemcpyAsync(s->d_tree_in, s->h_tree_in, 2 * SS_MAX_TREE * 4, cudaMemcpyHostToDevice, st));
-  ss_status r = run_step(s, s->d_tree_in, s->d_tree_in + SS_MAX_TREE, w, 0, logits_out != nullptr, st, false, T0);
+  const bool want = logits_out != nullptr || K > 0;
+  ss_status r = run_step(s, s->d_tree_in, s->d_tree_in + SS_MAX_TREE, w, 0, want, st, false, T0);
   if (r != SS_OK) return r;
   CUDA_TRY(cudaMemcpyAsync(&s->hstate->result, &s->dstate->result, sizeof(ss_verify_result), cudaMemcpyDeviceToHost,
                            st));
+  if (K > 0) {
+    // top-K tokens / logits + log-sum-exp per new node, in the tree-input staging's tail
+    int32_t* d_tok = s->d_topk;
+    float* d_val = reinterpret_cast<float*>(d_tok + 32 * 32);
+    float* d_lse = d_val + 32 * 32;
+    launch_topk(s, w, K, d_tok, d_val, d_lse, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(top_tok, d_tok, (size_t)w * K * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(top_logit, d_val, (size_t)w * K * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(lse, d_lse, (size_t)w * 4, cudaMemcpyDeviceToHost, st));
+  }
   if (logits_out)
     CUDA_TRY(cudaMemcpy2DAsync(logits_out, (size_t)s->V_l * 4, s->logits_dev, (size_t)s->V_l_pad * 4,
                                (size_t)s->V_l * 4, w, cudaMemcpyDeviceToHost, st));
@@ -1151,6 +1169,49 @@ extern "C" ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const in
     FAIL((ss_status)out->status, status_msg(out->status));
   }
   ss::host::on_extend(s->hs, T0, w, parents);
+  return SS_OK;
+}
+
+extern "C" ss_status ss_extend_tree(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0,
+                                    int32_t w, ss_verify_result* out, float* logits_out, void* stream) {
+  SCOPE(s);
+  return extend_impl(s, tokens, parents, T0, w, out, logits_out, 0, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" ss_status ss_extend_tree_topk(ss_shard* s, const int32_t* tokens, const int32_t* parents, int32_t T0,
+                                         int32_t w, int32_t K, int32_t* top_tok, float* top_logit, float* lse,
+                                         ss_verify_result* out, void* stream) {
+  SCOPE(s);
+  return extend_impl(s, tokens, parents, T0, w, out, nullptr, K, top_tok, top_logit, lse, stream);
+}
+
+extern "C" ss_status ss_reroot(ss_shard* s, const int32_t* path, int32_t n, const int32_t* keep, int32_t m,
+                               void* stream) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  if (!s->hs.have_verify) FAIL(SS_ESTATE, "re-root without a pending tree");
+  cudaSetDevice(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t vstatus = 0;
+  ss_status r = read_last_tree(s, st, &vstatus);
+  if (r != SS_OK) return r;
+  if (vstatus != SS_OK) FAIL(SS_ESTATE, "the last step failed on the device; nothing to re-root");
+  HOST_CHECK(check_reroot, s->hs, path, n, keep, m);
+  r = sync_L(s);
+  if (r != SS_OK) return r;
+  std::vector<int32_t> buf(1 + SS_MAX_TREE, 0);
+  buf[0] = n;
+  for (int k = 0; k < n; ++k) buf[1 + k] = path[k];
+  CUDA_TRY(cudaMemcpyAsync(&s->dstate->commit_n, buf.data(), (1 + SS_MAX_TREE) * 4, cudaMemcpyHostToDevice, st));
+  std::vector<int32_t> kb(1 + SS_MAX_TREE, 0);
+  kb[0] = m;
+  for (int j = 0; j < m; ++j) kb[1 + j] = keep[j];
+  static_assert(offsetof(DevState, keep) == offsetof(DevState, keep_n) + 4, "layout");
+  CUDA_TRY(cudaMemcpyAsync(&s->dstate->keep_n, kb.data(), (1 + SS_MAX_TREE) * 4, cudaMemcpyHostToDevice, st));
+  launch_reroot(s, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  ss::host::on_reroot(s->hs, path, n, keep, m);
   return SS_OK;
 }
 

@@ -41,12 +41,22 @@ class VerifyResultC(C.Structure):
                 ("bonus_token", C.c_int32), ("argmax", C.c_int32 * SS_MAX_TREE), ("status", C.c_int32)]
 
 
+class SpecCfgC(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("bs", "w", "d", "K", "n_tokens", "eos", "mode")]
+
+
+class SpecStatsC(C.Structure):
+    _fields_ = [("n_emitted", C.c_int32), ("steps", C.c_int32), ("target_steps", C.c_int32),
+                ("expansions", C.c_int32), ("accepted", C.c_int32), ("wall_ms", C.c_double)]
+
+
 _lib = None
 
 EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_local_peers", "ss_import_loopback",
            "ss_set_launch_cap", "ss_destroy", "ss_last_error", "ss_load_weights", "ss_synth_weights",
            "ss_set_prefix_kv", "ss_synth_prefix_kv", "ss_read_kv", "ss_set_committed_len",
-           "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_extend_tree", "ss_commit_kv",
+           "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_extend_tree", "ss_extend_tree_topk", "ss_reroot", "ss_speculative_decode",
+           "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
            "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
@@ -92,6 +102,9 @@ def lib():
         "ss_verify_tree": (i32, [vp, vp, vp, i32, C.POINTER(VerifyResultC), vp, vp]),
         "ss_verify_tree_dev": (i32, [vp, vp, vp, i32, vp, vp, i32, vp]),
         "ss_extend_tree": (i32, [vp, vp, vp, i32, i32, C.POINTER(VerifyResultC), vp, vp]),
+        "ss_extend_tree_topk": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp, C.POINTER(VerifyResultC), vp]),
+        "ss_reroot": (i32, [vp, vp, i32, vp, i32, vp]),
+        "ss_speculative_decode": (i32, [vp, vp, i32, C.POINTER(SpecCfgC), vp, C.POINTER(SpecStatsC), vp, vp]),
         "ss_commit_kv": (i32, [vp, vp, i32, vp]),
         "ss_commit_accepted": (i32, [vp, vp]),
         "ss_kernels_per_step": (i32, [vp, i32, i32]),
@@ -279,6 +292,38 @@ class Shard:
         n = res.n_accepted
         return dict(n_accepted=n, accepted=list(res.accepted[:n]), bonus=res.bonus_token,
                     argmax=list(res.argmax[:T0 + w]), status=res.status, logits=logits)
+
+    def extend_topk(self, tokens, parents, T0: int, K: int, stream=None):
+        """Draft forward (ss_extend_tree_topk): -> (top_tok [w][K], top_logit [w][K], lse [w])."""
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        p = np.ascontiguousarray(parents, dtype=np.int32)
+        w = len(t)
+        tok = np.zeros((w, K), dtype=np.int32)
+        val = np.zeros((w, K), dtype=np.float32)
+        lse = np.zeros(w, dtype=np.float32)
+        res = VerifyResultC()
+        self._ck(lib().ss_extend_tree_topk(self.h, _ptr(t), _ptr(p), T0, w, K, _ptr(tok), _ptr(val), _ptr(lse),
+                                         C.byref(res), _stream_handle(stream)))
+        return tok, val, lse
+
+    def reroot(self, path, keep, stream=None):
+        """Commit the chain `path`, keep the subtree `keep` (ss_reroot)."""
+        a = np.ascontiguousarray(path, dtype=np.int32)
+        k = np.ascontiguousarray(keep, dtype=np.int32)
+        self._ck(lib().ss_reroot(self.h, _ptr(a) if len(a) else None, len(a), _ptr(k) if len(k) else None,
+                               len(k), _stream_handle(stream)))
+
+    def speculative_decode(self, draft, root_token: int, n_tokens: int, bs: int = 8, w: int = 8, d: int = 1,
+                           K: int = 0, eos: int = -1, mode: str = "async", target_stream=None, draft_stream=None):
+        """Alg. 1 parallel tree generation with this shard as the target and `draft`
+        (ss_speculative_decode) -> (tokens, stats dict)."""
+        cfg = SpecCfgC(bs, w, d, K, n_tokens, eos, 0 if mode == "async" else 1)
+        out = np.zeros(n_tokens, dtype=np.int32)
+        st = SpecStatsC()
+        self._ck(lib().ss_speculative_decode(self.h, draft.h, int(root_token), C.byref(cfg), _ptr(out), C.byref(st),
+                                           _stream_handle(target_stream), _stream_handle(draft_stream)))
+        stats = {k: getattr(st, k) for k, _ in SpecStatsC._fields_}
+        return [int(t) for t in out[:st.n_emitted]], stats
 
     def verify_dev(self, d_tokens, d_parents, T: int, d_result=None, d_logits=None,
                    auto_commit: bool = False, stream=None):

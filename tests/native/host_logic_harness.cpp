@@ -38,6 +38,12 @@ int hl_check_extend(void* p, const int32_t* t, const int32_t* par, int T0, int w
 void hl_on_extend(void* p, int T0, int w, const int32_t* par) {
   ss::host::on_extend(*static_cast<CallState*>(p), T0, w, par);
 }
+int hl_check_reroot(void* p, const int32_t* path, int n, const int32_t* keep, int m) {
+  return ss::host::check_reroot(*static_cast<CallState*>(p), path, n, keep, m, g_msg);
+}
+void hl_on_reroot(void* p, const int32_t* path, int n, const int32_t* keep, int m) {
+  ss::host::on_reroot(*static_cast<CallState*>(p), path, n, keep, m);
+}
 int hl_last_T(void* p) { return static_cast<CallState*>(p)->last_T; }
 int hl_check_set_len(void* p, int L) { return ss::host::check_set_len(*static_cast<CallState*>(p), L, g_msg); }
 void hl_on_verify(void* p, int T, const int32_t* par, int auto_commit) {

@@ -34,7 +34,9 @@ def hl(tmp_path_factory):
                          ("hl_on_set_len", None, [vp, i32]), ("hl_L", i32, [vp]), ("hl_have_verify", i32, [vp]),
                          ("hl_max_written", i32, [vp]), ("hl_msg", C.c_char_p, []),
                          ("hl_check_extend", i32, [vp, vp, vp, i32, i32]),
-                         ("hl_on_extend", None, [vp, i32, i32, vp]), ("hl_last_T", i32, [vp])]:
+                         ("hl_on_extend", None, [vp, i32, i32, vp]), ("hl_last_T", i32, [vp]),
+                         ("hl_check_reroot", i32, [vp, vp, i32, vp, i32]),
+                         ("hl_on_reroot", None, [vp, vp, i32, vp, i32])]:
         f = getattr(L, n)
         f.restype = res
         f.argtypes = args
@@ -204,3 +206,30 @@ def test_extend_ecapacity(hl, st):
     p, pp = _a([3, 4, 5])
     assert hl.hl_check_extend(st, tp, pp, 4, 3) == ECAPACITY       # 250 + 4 + 3 > max_ctx 256
     assert hl.hl_check_extend(st, tp, pp, 4, 2) == OK              # 250 + 4 + 2 = 256 fits
+
+
+# ---- re-root with KV reorganisation (ss_reroot)
+def test_reroot_checks_and_reindex(hl, st):
+    par, pp = _a([-1, 0, 1, 1, 2, 3, 2, 4])   # 0 -> 1 -> {2, 3}; 2 -> {4, 6}; 3 -> 5; 4 -> 7
+    path, p_ = _a([0, 1])
+    keep, k_ = _a([2, 4, 6, 7])
+    assert hl.hl_check_reroot(st, p_, 2, k_, 4) == ESTATE         # nothing pending
+    hl.hl_on_verify(st, 8, pp, 0)
+    for pth, kp in [([0, 2], []), ([0], [2]), ([0, 1], [3, 2]), ([0, 1], [1]), ([], [1]), ([], [])]:
+        a, ap = _a(pth + [0])
+        b, bp = _a(kp + [0])
+        assert hl.hl_check_reroot(st, ap, len(pth), bp, len(kp)) == EINVAL, (pth, kp)
+    assert hl.hl_check_reroot(st, p_, 2, k_, 4) == OK
+    hl.hl_on_reroot(st, p_, 2, k_, 4)
+    assert hl.hl_L(st) == 66 and hl.hl_have_verify(st) == 1 and hl.hl_last_T(st) == 4
+    # the kept tree is re-indexed: its chain 0 -> 1 -> 3 commits next
+    ch, chp = _a([0, 1, 3])
+    assert hl.hl_check_commit(st, chp, 3) == OK
+    # n = m = 0 is refused; keep only (n = 0) must start at the root
+    z, zp = _a([0, 3])
+    assert hl.hl_check_reroot(st, None, 0, zp, 2) == EINVAL        # re-indexed: 3's parent is 1, not kept
+    z, zp = _a([0, 1])
+    assert hl.hl_check_reroot(st, None, 0, zp, 2) == OK            # truncate to nodes 0, 1
+    hl.hl_on_reroot(st, None, 0, zp, 2)
+    assert hl.hl_L(st) == 66 and hl.hl_last_T(st) == 2
+    assert hl.hl_check_reroot(st, None, 0, None, 0) == EINVAL

@@ -264,7 +264,7 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     T, L = args.T, args.L
     n_steps = args.warmup + args.steps
-    max_ctx = L + T * (3 * n_steps + 8) + 64
+    max_ctx = max(L + T * (3 * n_steps + 8) + 64, 8192 + 4 * 64 + 256)  # C-async runs at an 8K context
     sh = pkg.Shard(cfg, rank, world, local, max_ctx=max_ctx, max_tree=max(T, 32))
     sh.synth_weights(args.seed)
     sh.synth_prefix_kv(args.seed + 1, L)
@@ -413,6 +413,11 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_tp_emulate:
         line["decode_planted"] = decode_planted(sh, cfg, T, L)
         line["tp_emulated"] = tp_emulated(args, cfg, local, dev, peak)
+    if world == 1 and not args.no_async and cfg.name == "llama3-70b":
+        try:
+            line["c_async"] = c_async(args, sh, cfg, local, dev)
+        except Exception as ex:  # pragma: no cover
+            line["c_async"] = {"error": str(ex)}
     if rank == 0 and not args.no_cpu_baseline:
         smp = OracleSample(cfg, T, L)
         sec = smp.step_seconds(0)
@@ -581,6 +586,77 @@ def other_configs(args, sh70, cfg70, local, dev, peak):
     return out
 
 
+def c_async(args, sh70, cfg70, local, dev, n_tokens=64, draft_sms=20, bs=8, w=8):
+    """BASELINE configs[4] on one GPU: Alg. 1 parallel tree generation
+    (ss_speculative_decode) with a Llama3-3B-shaped draft and the Llama3-70B-
+    shaped target, 8K-token KV context in both.  The two GPU groups of the paper
+    (2 + 4 GPUs) are emulated by splitting this GPU's SMs (ss_set_launch_cap:
+    the target's grid on 148 - draft_sms SMs, the draft's on draft_sms; HBM is
+    shared), linked by the a13 mailboxes.  d = floor(t_target / t_draft) from a
+    short profile.  Wall-clock tokens/s of one request over
+    n_tokens tokens, async and serial (draft, then verify), and whether the
+    emitted tokens equal the target's own greedy decode.  Random
+    weights: the draft and target disagree, ~1 token per step."""
+    import time as _t
+    import torch
+    import paper_2506_11309_b200 as pkg
+    Lc = 8192
+    c3 = synth.CONFIGS["llama3-3b"]
+    out = {"draft": c3.name, "target": cfg70.name, "L": Lc, "bs": bs, "w": w, "n_tokens": n_tokens,
+           "draft_sms": draft_sms, "target_sms": 148 - draft_sms}
+    dr = pkg.Shard(c3, 0, 1, local, max_ctx=Lc + 4 * n_tokens + 256, max_tree=64)
+    try:
+        dr.synth_weights(args.seed + 17)
+        dr.synth_prefix_kv(args.seed + 18, Lc)
+        sh70.synth_prefix_kv(args.seed + 1, Lc)
+        sh70.set_committed_len(Lc)
+        dr.set_committed_len(Lc)
+        root = 1234
+        # reference: the target's plain greedy decode (T = 1 steps, whole GPU)
+        ref, cur = [], root
+        t0 = _t.perf_counter()
+        for _ in range(n_tokens):
+            r = sh70.verify(np.array([cur], dtype=np.int32), np.array([-1], dtype=np.int32))
+            sh70.commit_accepted()
+            cur = int(r["bonus"])
+            ref.append(cur)
+        out["greedy_tokens_per_s"] = n_tokens / (_t.perf_counter() - t0)
+        # profile for d (P:317-318): one target step and one draft expansion at their SM shares
+        sh70.set_launch_cap(148 - draft_sms)
+        dr.set_launch_cap(draft_sms)
+        sh70.set_committed_len(Lc)
+        tt = time_steps(sh70, cfg70, bs, 2, 4, dev) / 1e3
+        sh70.set_committed_len(Lc)
+        toks = np.arange(1, w + 1, dtype=np.int32)
+        par = np.arange(-1, w - 1, dtype=np.int32)
+        for _ in range(2):
+            dr.extend_topk(toks, par, 0, w)
+            dr.set_committed_len(Lc)
+        t0 = _t.perf_counter()
+        for _ in range(4):
+            dr.extend_topk(toks, par, 0, w)
+            dr.set_committed_len(Lc)
+        td = (_t.perf_counter() - t0) / 4
+        d = max(1, int(tt // td))
+        out.update({"t_target_ms": tt * 1e3, "t_draft_expansion_ms": td * 1e3, "d": d})
+        ts, ds = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        for mode in ("async", "serial"):
+            sh70.set_committed_len(Lc)
+            dr.set_committed_len(Lc)
+            toks_out, st = sh70.speculative_decode(dr, root, n_tokens, bs=bs, w=w, d=d, mode=mode,
+                                                   target_stream=ts, draft_stream=ds)
+            out[mode] = {"tokens_per_s": st["n_emitted"] / (st["wall_ms"] / 1e3),
+                         "mean_emitted_per_step": st["n_emitted"] / max(st["steps"], 1),
+                         "steps": st["steps"], "expansions": st["expansions"], "wall_ms": st["wall_ms"],
+                         "matches_greedy": toks_out == ref[:len(toks_out)]}
+        out["how"] = ("one request, wall clock around ss_speculative_decode (draft thread + target thread, "
+                      "mailbox hand-off); the target's greedy_tokens_per_s is plain T = 1 decoding on the whole GPU")
+    finally:
+        sh70.set_launch_cap(0)
+        dr.close()
+    return out
+
+
 def tp_emulated(args, cfg, local, dev, peak):
     """Per-GPU step latency of ONE rank of a TP = 2/4/8 group, emulated on this
     single GPU (ss_import_loopback: the rank's weight shard, KV heads and LL
@@ -640,6 +716,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tp-emulate", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs (70B T16/32, 1B, 8B)")
+    ap.add_argument("--no-async", action="store_true", help="skip the C-async (Alg. 1, 3B draft + 70B target) line")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -413,6 +413,10 @@ ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eos_token);
  * accept walk.  Asynchronous on `stream`; with auto_commit the accepted path
  * is committed in the same launch sequence.  Errors as ss_verify_tree_dev. */
 ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream);
+/* Same, with the step captured for at most max_nodes (<= max_tree) nodes: the
+ * graph of ceil(max_nodes / 8) token slots (a larger message is refused on the
+ * device, status SS_EINVAL).  The draft side knows its batch size bs. */
+ss_status ss_verify_tree_mailbox_n(ss_shard* s, int32_t max_nodes, int32_t auto_commit, void* stream);
 /* Draft-side helpers: post a tree into an inbox / wait for a verified path in
  * an outbox and copy it to dev_out = [n, bonus, stop, status, (node, token)
  * x n] (int32, device; status != SS_OK -> n = 0; a message that never

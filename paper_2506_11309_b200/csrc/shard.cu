@@ -1508,8 +1508,15 @@ extern "C" ss_status ss_attach_mailbox(ss_shard* s, void* outbox_dev, int32_t eo
 extern "C" ss_status ss_verify_tree_mailbox(ss_shard* s, int32_t auto_commit, void* stream) {
   SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
+  return ss_verify_tree_mailbox_n(s, s->cfg.max_tree, auto_commit, stream);
+}
+
+extern "C" ss_status ss_verify_tree_mailbox_n(ss_shard* s, int32_t max_nodes, int32_t auto_commit, void* stream) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  if (max_nodes < 1 || max_nodes > s->cfg.max_tree) FAIL(SS_EINVAL, "max_nodes out of [1, max_tree]");
   cudaSetDevice(s->device);
-  const int T = s->cfg.max_tree;  // the tree size arrives with the message
+  const int T = max_nodes;  // the tree size arrives with the message; the step's graph holds ceil(T/8)*8 slots
   ss_status r = check_ready(s, T);
   if (r != SS_OK) return r;
   cudaStream_t st = (cudaStream_t)stream;

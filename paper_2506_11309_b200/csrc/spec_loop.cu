@@ -141,7 +141,7 @@ extern "C" ss_status ss_speculative_decode(ss_shard* target, ss_shard* draft, in
       std::this_thread::yield();
     }
     ++tseq;
-    ss_status e = ss_verify_tree_mailbox(target, 1, ts);
+    ss_status e = ss_verify_tree_mailbox_n(target, bs, 1, ts);
     if (e == SS_OK && cudaStreamSynchronize(ts) != cudaSuccess) e = SS_ECUDA;
     // the committed length after the step's device commit, read on the target
     // stream (the generic refresh synchronises the whole device, which would

@@ -58,7 +58,7 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_committed_len", "ss_verify_tree", "ss_verify_tree_dev", "ss_extend_tree", "ss_extend_tree_topk", "ss_reroot", "ss_speculative_decode",
            "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
-           "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
+           "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_verify_tree_mailbox_n", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
            "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
            "ss_step_kernel_active", "ss_step_trace", "ss_read_step_trace", "ss_step_trace_host"]
 SS_DEBUG_CONSISTENCY = 1
@@ -112,6 +112,7 @@ def lib():
         "ss_mailbox_inbox": (i32, [vp, C.POINTER(vp)]),
         "ss_attach_mailbox": (i32, [vp, vp, i32]),
         "ss_verify_tree_mailbox": (i32, [vp, i32, vp]),
+        "ss_verify_tree_mailbox_n": (i32, [vp, i32, i32, vp]),
         "ss_mailbox_post_tree": (i32, [vp, vp, vp, i32, C.c_uint32, vp]),
         "ss_mailbox_recv_result": (i32, [vp, C.c_uint32, vp, vp]),
     }

@@ -669,7 +669,7 @@ def tp_emulated(args, cfg, local, dev, peak):
     out = {"note": "one TP rank on one GPU, loopback all-reduce (timing emulation, not a multi-GPU run)"}
     n = 3 + 10
     for P in (2, 4, 8):
-        sh = pkg.Shard(cfg, 0, P, local, max_ctx=L + T * (3 * n + 8) + 64, max_tree=max(T, 8))
+        sh = pkg.Shard(cfg, 0, P, local, max_ctx=L + 32 * (3 * n + 8) + 64, max_tree=max(T, 32))
         sh.synth_weights(args.seed)
         sh.synth_prefix_kv(args.seed + 1, L)
         sh.import_loopback()
@@ -699,7 +699,21 @@ def tp_emulated(args, cfg, local, dev, peak):
                 out[f"tp{P}"].update(bd)
         except Exception as e:  # measurement extra only
             out[f"tp{P}"]["breakdown_error"] = str(e)
+        if P >= 4:
+            # all-reduce scheme A/B at T = 8 and 32 on the same rank
+            ab = {}
+            for mode in ("one-shot", "two-shot"):
+                sh.set_allreduce(mode)
+                for Tx in (8, 32):
+                    sh.set_committed_len(L)
+                    ab[f"{mode}/T{Tx}"] = time_steps(sh, cfg, Tx, 2, 6, dev) * 1e3
+            sh.set_allreduce("one-shot")
+            out[f"tp{P}"]["allreduce_ab_us"] = ab
         sh.close()
+    out["allreduce_ab_how"] = ("step us per mode on the loopback rank: the two-shot rank stores one partial per "
+                               "non-home tile-group and reduces + broadcasts its home 1/P; loopback stores are "
+                               "local, so NVLink egress savings (7x -> 1.75x T h 8 B per all-reduce at TP 8) "
+                               "do not show here")
     return out
 
 

@@ -347,6 +347,20 @@ ss_status ss_commit_accepted(ss_shard* s, void* stream);
 /* Number of kernels the verify (+ commit) launch sequence contains. */
 int32_t ss_kernels_per_step(ss_shard* s, int32_t T, int32_t auto_commit);
 
+/* Tensor-parallel all-reduce scheme of the persistent step kernel (SURVEY
+ * 8(f) NEXT-2; the paper's fused one-shot design P:413-420 vs a two-shot
+ * variant for large T x h).  mode 0 (default): one-shot LL -- each O / down
+ * tile-group finaliser stores its fp32 partial to every rank, every rank sums
+ * the P partials in rank order (one NVLink hop, (P-1) x T x h x 8 bytes of
+ * LL egress per rank per all-reduce).  mode 1: two-shot LL -- the partial
+ * goes only to the tile-group's home rank (tg mod P), which sums in rank order
+ * and broadcasts the sum (two hops, ~2 (P-1)/P x T x h x 8 bytes).  Both give
+ * bit-identical residuals on every rank; results equal to the logit
+ * tolerance across modes (same rank-ordered sums: bit-identical).  Every rank
+ * of a group must use the same mode.  Synchronises the device; drops the
+ * shard's captured graphs.  The per-phase path (T > 32) is one-shot. */
+ss_status ss_set_allreduce(ss_shard* s, int32_t mode);
+
 /* Kernel organisation of the step.  on != 0 (the default): trees of T <= 32
  * run as ONE persistent kernel per step (every layer's GEMMs, attention,
  * all-reduces, the LM head and the accept walk; phases hand over through

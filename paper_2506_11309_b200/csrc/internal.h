@@ -145,6 +145,7 @@ struct ss_shard {
   float* peer_recv[ss::kMaxPeers] = {nullptr};
   bool peers_ready = false;
   bool loopback = false;            // ss_import_loopback (timing emulation)
+  int ar_mode = 0;                  // ss_set_allreduce: 0 one-shot, 1 two-shot (step kernel)
   bool ipc_opened[ss::kMaxPeers] = {false};
 
   // a13 mailbox: this shard's inbox (written by the draft group)

@@ -421,7 +421,9 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   // consistency area [P] (consistency_line_offset)
   A(s->mbox_in, (size_t)(1 + SS_MAX_TREE) * 16);
   if (tp_size > 1) {
-    s->recv_bytes = ((size_t)2 * tp_size * (h / 128) * 128 * 32 + (size_t)tp_size * 64 + (size_t)tp_size) * 16;
+    // + the two-shot broadcast area [2 parities][n_tg_total][128 rows][32 lines]
+    s->recv_bytes = ((size_t)2 * tp_size * (h / 128) * 128 * 32 + (size_t)tp_size * 64 + (size_t)tp_size +
+                     (size_t)2 * (h / 128) * 128 * 32) * 16;
     A(s->recv, s->recv_bytes);
   }
   if (cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -472,6 +474,19 @@ extern "C" ss_status ss_set_launch_cap(ss_shard* s, int32_t cap) {
   SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
   s->launch_cap = cap > 0 ? cap : 0;
+  for (auto& kv : s->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  s->graphs.clear();
+  return SS_OK;
+}
+
+extern "C" ss_status ss_set_allreduce(ss_shard* s, int32_t mode) {
+  SCOPE(s);
+  if (!s) FAIL(SS_EINVAL, "null shard");
+  if (mode != 0 && mode != 1) FAIL(SS_EINVAL, "mode must be 0 (one-shot) or 1 (two-shot)");
+  cudaSetDevice(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  s->ar_mode = mode;
   for (auto& kv : s->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   s->graphs.clear();
@@ -899,6 +914,8 @@ static StepArgs step_args(ss_shard* s, int want_logits) {
   a.rank = s->rank;
   a.P = s->P;
   a.loopback = s->loopback ? 1 : 0;
+  a.ar_mode = s->ar_mode;
+  a.bc_line0 = consistency_line_offset(s) + (size_t)s->P;
   a.recv = s->recv;
   for (int p = 0; p < s->P; ++p) a.peer_recv[p] = s->peer_recv[p];
   a.V_l = s->V_l;

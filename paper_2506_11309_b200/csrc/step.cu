@@ -955,11 +955,24 @@ SS_DEV void ar_send(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<N
   const uint32_t flag = a.st->epoch + ar_seq;
   const int pairs = (T + 1) >> 1;
   const int ntg = a.h / 128;
+  // two-shot: only the tile-group's home rank receives the partials.
+  // Loopback emulation (one rank, rank 0, standing in for its peers): a home
+  // tile-group receives P stand-in partials as in one-shot; a non-home one
+  // stores its partial once (the remote store) and writes the home's
+  // broadcast line itself (no wait for a real home).
+  const int home = tg % a.P;
+  const bool two = a.ar_mode == 1;
+  const int p0 = two && !(a.loopback && home == a.rank) ? home : 0;
+  const int p1 = two && !(a.loopback && home == a.rank) ? home + 1 : a.P;
+  const size_t bl0 = a.bc_line0 + ((size_t)(ar_seq & 1) * ntg + tg) * 128 * (4 * NT);
   for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
     const int r = idx / pairs, tp = idx - r * pairs;
     const float2 v = *reinterpret_cast<const float2*>(ts.acc + r * TP + 2 * tp);
-    for (int p = 0; p < a.P; ++p) {
-      const int slot = a.loopback ? p : a.rank;
+    if (two && a.loopback && home != a.rank)
+      ll_store(reinterpret_cast<uint4*>(a.recv) + bl0 + (size_t)r * (4 * NT) + tp, __float_as_uint(v.x),
+               __float_as_uint(v.y), flag);
+    for (int p = p0; p < p1; ++p) {
+      const int slot = (a.loopback && !(two && home != a.rank)) ? p : a.rank;
       const size_t line = (((size_t)(ar_seq & 1) * a.P + slot) * ntg + tg) * 128 * (4 * NT) + (size_t)r * (4 * NT) + tp;
       ll_store(reinterpret_cast<uint4*>(a.peer_recv[p]) + line, __float_as_uint(v.x), __float_as_uint(v.y), flag);
     }
@@ -1028,6 +1041,51 @@ SS_DEV void resid_update(const StepArgs& a, int tg, int T, int ar_seq, const Tai
         s0 += __uint_as_float(d1[p]);
         s1 += __uint_as_float(d2[p]);
       }
+    if (a.ar_mode == 1) {
+      // two-shot, home rank: broadcast the rank-ordered sum (every rank adds
+      // it to the same residual: bit-identical rows on all ranks)
+      const size_t bl = a.bc_line0 + ((size_t)(ar_seq & 1) * ntg + tg) * 128 * PP + (size_t)r * PP + tp;
+      for (int p = 0; p < a.P; ++p)
+        if (p != a.rank)  // loopback: peer_recv[p] is this rank's own buffer (stand-in stores)
+          ll_store(reinterpret_cast<uint4*>(a.peer_recv[p]) + bl, __float_as_uint(s0), __float_as_uint(s1), flag);
+    }
+    float* xp = a.x + (size_t)t0 * a.h + tg * 128 + r;
+    *xp = x0 + s0;
+    ts.xn[t0 * 128 + r] = x0 + s0;
+    if (t0 + 1 < T) {
+      xp[a.h] = x1 + s1;
+      ts.xn[(t0 + 1) * 128 + r] = x1 + s1;
+    }
+  }
+}
+
+// Two-shot all-reduce, a rank that is not tile-group tg's home: the home's
+// broadcast of the rank-ordered sum, added to the residual.
+template <int NT>
+SS_DEV void resid_update_bcast(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<NT>& ts) {
+  constexpr int PP = 4 * NT;
+  const uint32_t flag = a.st->epoch + ar_seq;
+  const int pairs = (T + 1) >> 1;
+  const int ntg = a.h / 128;
+  const uint4* src0 = reinterpret_cast<const uint4*>(a.recv) + a.bc_line0 + ((size_t)(ar_seq & 1) * ntg + tg) * 128 * PP;
+  for (int idx = threadIdx.x; idx < 128 * pairs; idx += 256) {
+    const int tp = idx >> 7, r = idx & 127;
+    const int t0 = 2 * tp;
+    const float x0 = __ldcg(a.x + (size_t)t0 * a.h + tg * 128 + r);
+    const float x1 = t0 + 1 < T ? __ldcg(a.x + (size_t)(t0 + 1) * a.h + tg * 128 + r) : 0.f;
+    uint32_t d1 = 0, d2 = 0;
+    unsigned spins = 0;
+    unsigned long long tw = 0;
+    while (!ll_try_load(src0 + (size_t)r * PP + tp, flag, d1, d2)) {
+      if ((++spins & 255u) == 0) {
+        if (!tw) tw = now_ns();
+        if (now_ns() - tw > 2000000000ull || *reinterpret_cast<volatile int*>(&a.st->timeout)) {
+          a.st->timeout = 1;
+          break;
+        }
+      }
+    }
+    const float s0 = __uint_as_float(d1), s1 = __uint_as_float(d2);
     float* xp = a.x + (size_t)t0 * a.h + tg * 128 + r;
     *xp = x0 + s0;
     ts.xn[t0 * 128 + r] = x0 + s0;
@@ -1316,17 +1374,24 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
                                       : (last ? a.final_norm : a.layers[layer + 1].attn_norm);
     float* ssn = a.ss + (size_t)(PH == PH_O ? layer * 2 + 1 : (layer + 1) * 2) * 64;
     uint8_t* act = last ? a.act_lm : a.act_h;
-    for (int i = 0; i < nd; ++i) {
-      if (a.P == 1) {
-        stage_acc<NT>(accb + (size_t)s_done[i] * 128 * TP, ts.acc);
+    // two-shot: the tile-groups this rank is home of first (their sums are
+    // what the other ranks wait for; homes wait only on the sends above)
+    const bool two = a.ar_mode == 1 && a.P > 1;
+    for (int pass = 0; pass < (two ? 2 : 1); ++pass)
+      for (int i = 0; i < nd; ++i) {
+        const bool home = !two || s_done[i] % a.P == a.rank;
+        if (two && home != (pass == 0)) continue;
+        if (a.P == 1) {
+          stage_acc<NT>(accb + (size_t)s_done[i] * 128 * TP, ts.acc);
+          cbar();
+        }
+        if (home) resid_update<NT>(a, s_done[i], T, ar_seq, ts);
+        else resid_update_bcast<NT>(a, s_done[i], T, ar_seq, ts);
+        cbar();
+        if (ttl && i == 0) ttl[3] = clk64();
+        next_input<NT>(a, s_done[i], T, gain, ssn, act, last ? 1 : 0, ts);
         cbar();
       }
-      resid_update<NT>(a, s_done[i], T, ar_seq, ts);
-      cbar();
-      if (ttl && i == 0) ttl[3] = clk64();
-      next_input<NT>(a, s_done[i], T, gain, ssn, act, last ? 1 : 0, ts);
-      cbar();
-    }
     where(a, WCODE(layer, PH, 8));
     if constexpr (PH == PH_O) {
       // zero the down input's X slots (the SwiGLU epilogues of this layer add into them)

@@ -81,6 +81,11 @@ struct StepArgs {
   float* att_ws = nullptr;    // [n_ctas][2 key halves][64 rows][d] unnormalised partial outputs
   float2* att_ml = nullptr;   // [n_ctas][2][64] (running max, sum)
   int rank = 0, P = 1, loopback = 0;
+  // all-reduce scheme: 0 one-shot LL (every finaliser
+  // stores its partial to every rank), 1 two-shot LL (reduce-scatter to the
+  // tile-group's home rank tg % P, which sums and broadcasts the sum)
+  int ar_mode = 0;
+  size_t bc_line0 = 0;        // first LL line of the two-shot broadcast area in every receive buffer
   float* recv = nullptr;
   float* peer_recv[kMaxPeers] = {nullptr};
   int V_l = 0, V_off = 0, logits_ld = 0;

@@ -59,7 +59,7 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_verify_tree_mailbox_n", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
-           "ss_set_debug", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
+           "ss_set_debug", "ss_set_allreduce", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
            "ss_step_kernel_active", "ss_step_trace", "ss_read_step_trace", "ss_step_trace_host"]
 SS_DEBUG_CONSISTENCY = 1
 
@@ -84,6 +84,7 @@ def lib():
         "ss_destroy": (i32, [vp]),
         "ss_last_error": (C.c_char_p, [vp]),
         "ss_set_debug": (i32, [vp, i32]),
+        "ss_set_allreduce": (i32, [vp, i32]),
         "ss_set_step_kernel": (i32, [vp, i32]),
         "ss_step_kernel_active": (i32, [vp, i32]),
         "ss_step_trace": (i32, [vp, i32]),
@@ -415,6 +416,10 @@ class Shard:
     def import_loopback(self):
         """Timing emulation of this rank alone (include/swiftspec.h ss_import_loopback)."""
         self._ck(lib().ss_import_loopback(self.h))
+
+    def set_allreduce(self, mode: str):
+        """'one-shot' (default) or 'two-shot' TP all-reduce in the step kernel (ss_set_allreduce)."""
+        self._ck(lib().ss_set_allreduce(self.h, {"one-shot": 0, "two-shot": 1}[mode]))
 
     def set_launch_cap(self, cap: int):
         self._ck(lib().ss_set_launch_cap(self.h, cap))

@@ -201,8 +201,8 @@ def _oracle_70b_layer(cfg, L, tokens, parents):
     return _ORACLE_70B[key]
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_70b_shaped_layer_tp_fakepeer_sampled(P):
+@pytest.mark.parametrize("P,ar", [(2, "one-shot"), (4, "one-shot"), (8, "one-shot"), (8, "two-shot"), (4, "two-shot")])
+def test_70b_shaped_layer_tp_fakepeer_sampled(P, ar):
     """TP = 2 / 4 / 8 at full Llama3-70B layer shape (h 8192, I 28672, 64/8 heads,
     128256-row vocab-parallel LM head, 4K prefix): P fake-peer shards synthesised on the
     device, the fused all-reduces over h/128 = 64 tile-groups and the argmax exchange;
@@ -219,6 +219,7 @@ def test_70b_shaped_layer_tp_fakepeer_sampled(P):
         sh.set_launch_cap(148 // P)
         sh.synth_weights(0)
         sh.synth_prefix_kv(1, L)
+        sh.set_allreduce(ar)
         shards.append(sh)
     pkg.Shard.import_local_peers(shards)
     rng = np.random.default_rng(72)
@@ -268,3 +269,67 @@ def test_device_synth_shards_match_host_load(P):
         sh.close()
     # run-to-run fp32 reduction order (stream-K red.add) differs by ~1e-3
     np.testing.assert_allclose(b, a, atol=1e-2, rtol=1e-2)
+
+
+# ---------------------------------------------------------------- two-shot all-reduce (NEXT-2)
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_fakepeer_two_shot_allreduce(P):
+    """Two-shot LL all-reduce (ss_set_allreduce): partials
+    reduce-scattered to each tile-group's home rank (tg mod P), which sums in
+    rank order and broadcasts.  Logits within R13 of the sharded oracle, every
+    rank walks the same path, and repeated auto-commit steps (both buffer
+    parities, flag epochs) advance L identically; then back to one-shot on the
+    same shards, with the same accept results for the same tree."""
+    cfg = synth.CONFIGS["small-tp"]
+    L = 64
+    shards, m, kv = _setup(cfg, P, L)
+    for sh in shards:
+        sh.set_allreduce("two-shot")
+    rng = np.random.default_rng(60 + P)
+    tokens, parents = synth.tree_paperlike(8, cfg.vocab, rng)
+    outs = _run(shards, tokens, parents)
+    ro = O.verify_sharded(cfg, m, kv, tokens, parents, P)
+    logits = np.concatenate([lg for _, lg in outs], axis=1)
+    err = np.abs(logits - ro["logits"])
+    assert np.all(err <= 2e-2 + 1e-2 * np.abs(ro["logits"])), err.max()
+    assert all(res["status"] == 0 for res, _ in outs)
+    for res, _ in outs[1:]:
+        assert res["argmax"] == outs[0][0]["argmax"] and res["accepted"] == outs[0][0]["accepted"]
+    for sh in shards:
+        sh.set_committed_len(L)
+    for sh in shards:
+        sh.set_allreduce("one-shot")
+    outs1 = _run(shards, tokens, parents)
+    lg1 = np.concatenate([lg for _, lg in outs1], axis=1)
+    assert np.max(np.abs(lg1 - logits)) <= 5e-3      # same rank-ordered sums; stream-K order differs run to run
+    for sh in shards:
+        sh.set_committed_len(L)
+        sh.set_allreduce("two-shot")
+    total = 0
+    for step in range(4):
+        tokens, parents = synth.tree_random(8 if step % 2 else 13, cfg.vocab, rng)
+        outs = _run(shards, tokens, parents, auto_commit=True)
+        assert all(o[0]["status"] == 0 for o in outs)
+        assert all(o[0]["accepted"] == outs[0][0]["accepted"] for o in outs)
+        total += outs[0][0]["n_accepted"]
+        assert [sh.L for sh in shards] == [L + total] * P
+    for sh in shards:
+        sh.close()
+
+
+def test_loopback_two_shot_runs():
+    """The TP-rank timing emulation also runs the two-shot scheme (home and
+    non-home tile-groups, stand-in broadcasts)."""
+    import paper_2506_11309_b200 as pkg
+    cfg = synth.CONFIGS["small-tp"]
+    sh = pkg.Shard(cfg, 0, 4, 0, max_ctx=64 + 128, max_tree=16)
+    sh.synth_weights(0)
+    sh.synth_prefix_kv(1, 64)
+    sh.import_loopback()
+    sh.set_allreduce("two-shot")
+    for T in (1, 8, 13):
+        tokens, parents = synth.tree_paperlike(T, cfg.vocab, np.random.default_rng(T))
+        r = sh.verify(tokens, parents)
+        assert r["status"] == 0
+        sh.commit_accepted()
+    sh.close()

@@ -135,9 +135,13 @@ SS_DEV void tmark(const StepArgs& a, int slot, int which) {
 
 // tcgen05 (5th-gen tensor cores, TMEM accumulators) ------------------------
 // TMEM map of the CTA (512 columns, lane = output row of the 128-row tile):
-//   [0, 256)   A operand, two buffers of one W4 unit (256 k = 128 fp16x2 columns)
-//   [256, 512) fp32 accumulators, [slot kNacc][AWQ group 2][N columns]
-constexpr uint32_t kTmemCols = 512, kAccCol = 256;
+//   [0, 128 kNbuf)   A operand, kNbuf buffers of one W4 unit (256 k = 128 fp16x2 columns)
+//   [128 kNbuf, 512) fp32 accumulators, [slot kNacc][AWQ group 2][N columns]
+// T <= 8: three A buffers (the dequant of unit k waits for unit k - 3's MMAs,
+// one unit more slack than two buffers); the accumulators fill the rest.
+constexpr uint32_t kTmemCols = 512;
+template <int NT> constexpr int kNbuf = NT == 1 ? 3 : 2;
+template <int NT> constexpr uint32_t kAccColT = 128u * kNbuf<NT>;
 // accumulator slots [kNacc][AWQ group 2][N]: 4 at T <= 16 (the two warp sets
 // alternate two each, so a unit's MMAs never write the accumulator the
 // previous unit's epilogue is reading), 2 at T <= 32
@@ -572,10 +576,31 @@ SS_DEV void wait_counter(const int* p, int target) {
 //   y[t] += s * ((acc_hi[t] + acc_lo[t]) - (1024 + z) * X[t]).
 struct Tc {
   uint32_t tbase;    // TMEM base address
-  uint32_t ardy0;    // mbarrier[2]: the unit's A operand is in TMEM (8 warp arrivals)
-  uint32_t mdone0;   // mbarrier[2 buffers][2 groups]: the unit's MMAs of one AWQ group completed
-  uint32_t* slot;    // shared [2]: smem address of the unit's ring slot (0 = stop)
+  uint32_t ardy0;    // mbarrier[kNbuf]: the unit's A operand is in TMEM (8 warp arrivals)
+  uint32_t mdone0;   // mbarrier[kNbuf buffers][2 groups]: MMAs reading the A buffer completed
+  uint32_t* slot;    // shared [kNbuf]: smem address of the unit's ring slot (0 = stop)
+  uint32_t macc0;    // mbarrier[kNacc slots][2 groups]: MMAs writing the accumulator slot completed
 };
+// Accumulator slot k % kNacc is used by every kNacc-th unit; its epilogue waits
+// on the slot's own barrier (phase parity (k / kNacc) & 1), which cannot
+// complete again before that epilogue (the next writer of the slot is issued
+// after it in program order).  The A buffers have their own barriers.
+template <int NT>
+SS_DEV void tc_wait_acc(const Tc& tc, int k) {
+  constexpr int NA = kNacc<NT>;
+  const int ac = k % NA;
+  mbar_wait_wd(tc.macc0 + 8 * (2 * ac), (uint32_t)((k / NA) & 1));
+  mbar_wait_wd(tc.macc0 + 8 * (2 * ac + 1), (uint32_t)((k / NA) & 1));
+}
+// Before unit k's dequant overwrites A buffer k % kNbuf: unit k - kNbuf's MMAs.
+template <int NT>
+SS_DEV void tc_wait_buf(const Tc& tc, int k) {
+  constexpr int NB = kNbuf<NT>;
+  if (k < NB) return;
+  const int kp = k - NB, b = kp % NB;
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b), (uint32_t)((kp / NB) & 1));
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b + 1), (uint32_t)((kp / NB) & 1));
+}
 
 template <int NT>
 SS_DEV void tc_dequant(const Tc& tc, uint32_t sst, int b, int warp, int lane) {
@@ -648,9 +673,7 @@ SS_DEV void tc_signal_q(const Tc& tc, uint32_t sst, int b, int qd, int lane) {
 template <int NT>
 SS_DEV void tc_epilogue_q(const Tc& tc, uint32_t sst, int k, int qd, int lane, float (&y)[8 * NT]) {
   constexpr int TP = 8 * NT, N = 16 * NT;
-  const int b = k & 1;
-  mbar_wait_wd(tc.mdone0 + 8 * (2 * b), (uint32_t)((k >> 1) & 1));
-  mbar_wait_wd(tc.mdone0 + 8 * (2 * b + 1), (uint32_t)((k >> 1) & 1));
+  tc_wait_acc<NT>(tc, k);
   __syncwarp();
   tc_fence_after();
   const int m = 32 * qd + lane, tile = m >> 4, r16 = m & 15, g8 = r16 & 7, up = r16 >> 3;
@@ -668,7 +691,7 @@ SS_DEV void tc_epilogue_q(const Tc& tc, uint32_t sst, int k, int qd, int lane, f
       X[t] = __uint_as_float(v.x); X[t + 1] = __uint_as_float(v.y);
       X[t + 2] = __uint_as_float(v.z); X[t + 3] = __uint_as_float(v.w);
     }
-    const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccCol + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + hh) * N);
+    const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccColT<NT> + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + hh) * N);
 #pragma unroll
     for (int j = 0; j < (TP + 15) / 16; ++j) {
       uint32_t rh[16], rl[16];
@@ -692,11 +715,10 @@ SS_DEV void tc_epilogue_q(const Tc& tc, uint32_t sst, int k, int qd, int lane, f
 template <int NT>
 SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, float (&y)[8 * NT]) {
   constexpr int TP = 8 * NT, N = 16 * NT;
-  const int qd = warp & 3, hh = warp >> 2, b = k & 1;
-  // both groups' MMAs (two issuers): this warp's next dequant overwrites the
-  // A columns of both groups
-  mbar_wait_wd(tc.mdone0 + 8 * (2 * b), (uint32_t)((k >> 1) & 1));
-  mbar_wait_wd(tc.mdone0 + 8 * (2 * b + 1), (uint32_t)((k >> 1) & 1));
+  const int qd = warp & 3, hh = warp >> 2;
+  // both groups' MMAs (two issuers; the same completion also frees the A
+  // buffer this warp's next-but-one dequant overwrites)
+  tc_wait_acc<NT>(tc, k);
   __syncwarp();
   tc_fence_after();
   // metadata of row m = 32 qd + lane (tile m / 16, fragment row m % 16) in group hh
@@ -713,7 +735,7 @@ SS_DEV void tc_epilogue(const Tc& tc, uint32_t sst, int k, int warp, int lane, f
     X[t] = __uint_as_float(v.x); X[t + 1] = __uint_as_float(v.y);
     X[t + 2] = __uint_as_float(v.z); X[t + 3] = __uint_as_float(v.w);
   }
-  const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccCol + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + hh) * N);
+  const uint32_t ta = tc.tbase + ((uint32_t)(32 * qd) << 16) + kAccColT<NT> + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + hh) * N);
   if constexpr (TP == 8) {
     uint32_t r[16];
     tc_ld_32x32b_x16(ta, r);
@@ -747,9 +769,9 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc, in
   constexpr int N = 16 * NT;
   constexpr uint32_t idesc = idesc_f16(128, N);
   for (int k = 0;; ++k) {
-    const int b = k & 1;
+    const int b = k % kNbuf<NT>;
     where(a, WCODE(k & 0xFFFF, 0x20, 1));
-    mbar_wait_wd(tc.ardy0 + 8 * b, (uint32_t)((k >> 1) & 1));
+    mbar_wait_wd(tc.ardy0 + 8 * b, (uint32_t)((k / kNbuf<NT>) & 1));
     if (g == 0 && a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2] = clk64();
     __syncwarp();
     const uint32_t sst = *reinterpret_cast<volatile uint32_t*>(tc.slot + b);
@@ -757,7 +779,7 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc, in
     tc_fence_after();
     const uint64_t bd0 = smem_desc(sst + kW4UnitBytes, N * 16, 128);
     {
-      const uint32_t d = tc.tbase + kAccCol + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + g) * N);
+      const uint32_t d = tc.tbase + kAccColT<NT> + (uint32_t)(((k & (kNacc<NT> - 1)) * 2 + g) * N);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int i = g * 8 + ks;
@@ -772,9 +794,13 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc, in
             ;
       }
     }
+    // two commits (each tracks every prior MMA of this thread): the A buffer's
+    // barrier and the accumulator slot's
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(tc.mdone0 + 8 * (2 * b + g))
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t}"
+        ::"r"(tc.mdone0 + 8 * (2 * b + g)), "r"(tc.macc0 + 8 * (2 * (k % kNacc<NT>) + g))
         : "memory");
     if (g == 0 && a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2 + 1] = clk64();
   }
@@ -1205,8 +1231,9 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
     const int k0 = ring.k;
     const int ws = warp >> 2, qd = warp & 3;
     unsigned long long* utl =
-        (a.utl && PH == PH_GU && layer == a.n_layers / 2 && blockIdx.x == 0 && threadIdx.x == 0) ? a.utl : nullptr;
-    if (utl) { utl[127 * 8 + 7] = (unsigned long long)tck; utl[127 * 8 + 6] = (unsigned long long)(u1 - u0); }
+        (a.utl && PH == PH_GU && layer == a.n_layers / 2 && blockIdx.x == 0 && (threadIdx.x & 127) == 0) ? a.utl
+                                                                                                        : nullptr;
+    if (utl && threadIdx.x == 0) { utl[127 * 8 + 7] = (unsigned long long)tck; utl[127 * 8 + 6] = (unsigned long long)(u1 - u0); }
     uint32_t sst_prev = 0;
     int u_prev = -1;
     auto release_pair = [&](int q0) {
@@ -1229,24 +1256,20 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
       const int um = p + ws;
       const bool have = um < u1;
       uint32_t sst = 0;
-      if (u_prev >= 0) {
-        // the set's previous unit used the same TMEM A buffer: its MMAs must
-        // be complete before the dequant below overwrites it
-        const int kp = tck + (u_prev - u0);
-        mbar_wait_wd(tc.mdone0 + 8 * (2 * (kp & 1)), (uint32_t)((kp >> 1) & 1));
-        mbar_wait_wd(tc.mdone0 + 8 * (2 * (kp & 1) + 1), (uint32_t)((kp >> 1) & 1));
-      }
+      // the A buffer's previous user (unit k - kNbuf) must have finished its
+      // MMAs before the dequant below overwrites it
+      if (have) tc_wait_buf<NT>(tc, tck + (um - u0));
       if (have) {
         if (utl && um - u0 < 127) utl[(um - u0) * 8 + 0] = clk64();
         sst = ring_wait_at<NT>(ring, k0 + (um - u0));
         if (utl && um - u0 < 127) utl[(um - u0) * 8 + 1] = clk64();
         if (p == u0) tmark(a, tslot, 1);
-        tc_dequant_q(tc, sst, (tck + (um - u0)) & 1, qd, lane);
+        tc_dequant_q(tc, sst, (tck + (um - u0)) % kNbuf<NT>, qd, lane);
         if (utl && um - u0 < 127) utl[(um - u0) * 8 + 2] = clk64();
       }
       // hand the new unit to the MMA warps first: its MMAs then run during
       // the previous unit's epilogue and are done before this set's next dequant
-      if (have) tc_signal_q(tc, sst, (tck + (um - u0)) & 1, qd, lane);
+      if (have) tc_signal_q(tc, sst, (tck + (um - u0)) % kNbuf<NT>, qd, lane);
       if (u_prev >= 0) {
         where(a, WCODE(layer, PH, 3));
         tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y);
@@ -1289,7 +1312,8 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
         sst = ring_wait_at<NT>(ring, k0 + (u - u0));
         if (utl && u - u0 < 127) utl[(u - u0) * 8 + 1] = clk64();
         if (u == u0) tmark(a, tslot, 1);
-        tc_dequant<NT>(tc, sst, (tck + (u - u0)) & 1, warp, lane);
+        tc_wait_buf<NT>(tc, tck + (u - u0));  // satisfied: the epilogue of unit u - 2 waited on the same MMAs
+        tc_dequant<NT>(tc, sst, (tck + (u - u0)) % kNbuf<NT>, warp, lane);
         if (utl && u - u0 < 127) utl[(u - u0) * 8 + 2] = clk64();
       }
       if (u > u0) {
@@ -1298,7 +1322,7 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
         tc_epilogue<NT>(tc, prev, tck + (v - u0), warp, lane, y);
         if (utl && v - u0 < 127) utl[(v - u0) * 8 + 3] = clk64();
       }
-      if (u < u1) tc_signal(tc, sst, (tck + (u - u0)) & 1, warp, lane);
+      if (u < u1) tc_signal(tc, sst, (tck + (u - u0)) % kNbuf<NT>, warp, lane);
       if (u > u0) {
         const int v = u - 1;
         ring_release_at<NT>(ring, k0 + (v - u0));
@@ -1775,13 +1799,13 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     step_kernel(const StepArgs* __restrict__ ap_g) {
   using C = StepCfg<NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[2], mdone[4];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[3], mdone[6], macc[8];
   __shared__ int s_done[128];
   __shared__ int s_nd;
   __shared__ float s_rmax[2 * 64];
   __shared__ Sched s_sched;
   __shared__ __align__(16) float s_merge[8 * 132];
-  __shared__ uint32_t s_tmem, s_slot[2];
+  __shared__ uint32_t s_tmem, s_slot[3];
   // the arguments and the per-layer pointer table live in shared memory: the
   // producer's per-unit address arithmetic must not chase global pointers
   __shared__ __align__(16) StepArgs s_args;
@@ -1801,8 +1825,9 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 8);
     }
-    for (int i = 0; i < 2; ++i) mbar_init(&ardy[i], 8);
-    for (int i = 0; i < 4; ++i) mbar_init(&mdone[i], 1);
+    for (int i = 0; i < kNbuf<NT>; ++i) mbar_init(&ardy[i], 8);
+    for (int i = 0; i < 2 * kNbuf<NT>; ++i) mbar_init(&mdone[i], 1);
+    for (int i = 0; i < 2 * kNacc<NT>; ++i) mbar_init(&macc[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) {  // the whole TMEM of the SM (one CTA per SM)
@@ -1817,7 +1842,7 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
   __syncthreads();
   const StepArgs* __restrict__ ap = &s_args;
   const uint32_t sm0 = smem_u32(smem), full0 = smem_u32(full), empty0 = smem_u32(empty);
-  const Tc tc{s_tmem, smem_u32(ardy), smem_u32(mdone), s_slot};
+  const Tc tc{s_tmem, smem_u32(ardy), smem_u32(mdone), s_slot, smem_u32(macc)};
   // everything below reads the ingest kernel's outputs (T, L, tree, counters)
   pdl_wait();
   pdl_trigger();
@@ -1854,8 +1879,8 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
   }
   // stop the MMA warp: an empty A buffer announcement (thread 0 writes the slot
   // before its own arrival; every consumer warp's lane 0 arrives)
-  if (threadIdx.x == 0) s_slot[tck & 1] = 0;
-  if (lane == 0) mbar_arrive_a(tc.ardy0 + 8 * (tck & 1));
+  if (threadIdx.x == 0) s_slot[tck % kNbuf<NT>] = 0;
+  if (lane == 0) mbar_arrive_a(tc.ardy0 + 8 * (tck % kNbuf<NT>));
   where(*ap, WCODE(0xFFFE, 0, 0));
   gemm_phase<NT, PH_LM>(ap, &s_sched, 0, s_sched.lm0, s_sched.lm1, ring, tc, tck, s_done, &s_nd, s_tail);
   tc_fence_before();

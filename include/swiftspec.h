@@ -178,6 +178,15 @@ const char* ss_last_error(const ss_shard* s);
  * every rank if any two disagree.  Set it identically on all ranks.
  * Errors: SS_EINVAL (unknown flag). */
 #define SS_DEBUG_CONSISTENCY 1
+/* SS_DEBUG_DETERMINISTIC: bit-identical results run to run (the
+ * stream-K float reductions make logits vary by ~1e-3 between runs).  The
+ * persistent step kernel (T <= 32) then gives every GEMM tile-group to one CTA
+ * (no cross-CTA split-K: each accumulator element gets at most two flushes
+ * onto zero, and fp32 addition of two terms commutes) and adds the RMSNorm
+ * partial sums of squares as exact 2^-24 fixed point.  Slower (fewer CTAs
+ * stream the short GEMMs); the per-phase path (T > 32) is not covered.
+ * Results equal the default mode's to the logit tolerance. */
+#define SS_DEBUG_DETERMINISTIC 2
 ss_status ss_set_debug(ss_shard* s, int32_t flags);
 
 /* ---- weights and KV ------------------------------------------------------ */

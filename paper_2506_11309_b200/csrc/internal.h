@@ -154,6 +154,7 @@ struct ss_shard {
   // persistent step kernel (step.cu) state
   int* step_ctr = nullptr;         // phase counters [n_layers][kCtrPerLayerH] + [kCtrGlobalH]
   float* step_ss = nullptr;        // [n_layers + 1][2][64]
+  unsigned long long* step_ssx = nullptr;  // same shape, fixed point (SS_DEBUG_DETERMINISTIC)
   uint16_t* qf = nullptr;          // q fragments hi | lo
   uint16_t* klo = nullptr;         // tree K / V lo window [Hkv_l][128][d]
   uint16_t* vlo = nullptr;

@@ -61,6 +61,7 @@ struct StepIngest {
   int* ctr = nullptr;
   int n_ctr = 0;
   float* ss = nullptr;      // [n_layers + 1][2][64]
+  unsigned long long* ssx = nullptr;  // same shape, fixed point (deterministic mode)
   int n_ss = 0;
   uint8_t* act_o = nullptr;
   uint8_t* act_d = nullptr;
@@ -213,8 +214,10 @@ __global__ void __launch_bounds__(256) embed_meta_kernel(DevState* st, const int
     // per-step counters and sums of squares (ss[0][t < T] is written below)
     const int nb = gridDim.x * gridDim.y, bi = blockIdx.y * gridDim.x + blockIdx.x;
     for (int i = bi * 256 + tid; i < si.n_ctr; i += nb * 256) si.ctr[i] = 0;
-    for (int i = bi * 256 + tid; i < si.n_ss; i += nb * 256)
+    for (int i = bi * 256 + tid; i < si.n_ss; i += nb * 256) {
       if (i >= 64 || i >= T) si.ss[i] = 0.f;
+      if (si.ssx) si.ssx[i] = 0ull;
+    }
   }
   if (t >= T && si.on) {  // padded token slot of every step-kernel input
     zero_a2_slot(act, t, h, NT, part);
@@ -329,6 +332,7 @@ void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parent
     si.ctr = s->step_ctr;
     si.n_ctr = s->cfg.n_layers * kCtrPerLayerH + kCtrGlobalH;
     si.ss = s->step_ss;
+    si.ssx = s->step_ssx;
     si.n_ss = (s->cfg.n_layers + 1) * 2 * 64;
     si.act_o = s->act_o;
     si.act_d = s->act_d;

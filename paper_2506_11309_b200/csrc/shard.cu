@@ -381,6 +381,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   s->step_max_ctas = s->n_sm * 2;
   A(s->step_ctr, ((size_t)c.n_layers * kCtrPerLayer + kCtrGlobal) * 4);
   A(s->step_ss, (size_t)(c.n_layers + 1) * 2 * 64 * 4);
+  A(s->step_ssx, (size_t)(c.n_layers + 1) * 2 * 64 * 8);
   A(s->qf, (size_t)2 * s->Hkv_l * G * 64 * d * 2);
   A(s->klo, (size_t)s->Hkv_l * 128 * d * 2);
   A(s->vlo, (size_t)s->Hkv_l * 128 * d * 2);
@@ -458,7 +459,7 @@ extern "C" ss_status ss_destroy(ss_shard* s) {
                   s->sc_lm.counters, s->sc_o.ss, s->sc_o.nbar, s->sc_down.ss, s->sc_down.nbar, s->step_ctr,
                   s->step_ss, s->qf, s->klo, s->vlo, s->att_ws, s->att_ml, s->layer_tab, s->sc_qkv.ss,
                   s->sc_qkv.nbar, s->sc_gu.ss, s->sc_gu.nbar, s->sc_lm.ss, s->sc_lm.nbar, s->step_args_dev,
-                  s->d_topk};
+                  s->d_topk, s->step_ssx};
   if (s->step_trace_host) cudaFreeHost(s->step_trace_host);
   else if (s->step_trace) cudaFree(s->step_trace);
   for (void* p : ptrs)
@@ -909,6 +910,8 @@ static StepArgs step_args(ss_shard* s, int want_logits) {
   }
   a.ctr = s->step_ctr;
   a.ss = s->step_ss;
+  a.ssx = s->step_ssx;
+  a.det = (s->debug & SS_DEBUG_DETERMINISTIC) ? 1 : 0;
   a.att_ws = s->att_ws;
   a.att_ml = s->att_ml;
   a.rank = s->rank;
@@ -1376,10 +1379,15 @@ extern "C" int32_t ss_step_kernel_active(ss_shard* s, int32_t T) {
 extern "C" ss_status ss_set_debug(ss_shard* s, int32_t flags) {
   SCOPE(s);
   if (!s) FAIL(SS_EINVAL, "null shard");
-  if (flags & ~SS_DEBUG_CONSISTENCY) FAIL(SS_EINVAL, "unknown debug flag");
+  if (flags & ~(SS_DEBUG_CONSISTENCY | SS_DEBUG_DETERMINISTIC)) FAIL(SS_EINVAL, "unknown debug flag");
   cudaSetDevice(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(&s->dstate->debug, &flags, 4, cudaMemcpyHostToDevice));
+  if ((flags ^ s->debug) & SS_DEBUG_DETERMINISTIC) {  // the step kernel's schedule changes
+    for (auto& kv : s->graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    s->graphs.clear();
+  }
   s->debug = flags;
   return SS_OK;
 }

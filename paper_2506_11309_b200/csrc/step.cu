@@ -222,12 +222,29 @@ SS_DEV void gemm_range_tg(int n_tg, int S, int n_ctas, int b, int& u0, int& u1) 
   gemm_range(U, n_ctas, b, u0, u1);
 }
 
+// Deterministic mode: whole tile-groups per CTA (no cross-CTA split-K, so each
+// accumulator element receives one flush per warp set, in a fixed place).
+SS_DEV void gemm_range_whole(int n_tg, int S, int n_ctas, int b, int& u0, int& u1) {
+  int t0, t1;
+  gemm_range(n_tg, n_ctas, b, t0, t1);
+  u0 = t0 * S;
+  u1 = t1 * S;
+}
+
 SS_DEV void make_sched(const StepArgs& a, int b, int L, int T, int T0, int NT, Sched& s) {
-  gemm_range_tg(a.qkv_tg, a.qkv_S, a.n_ctas, b, s.qkv0, s.qkv1);
-  gemm_range_tg(a.o_tg, a.o_S, a.n_ctas, b, s.o0, s.o1);
-  gemm_range_tg(a.gu_tg, a.gu_S, a.n_ctas, b, s.gu0, s.gu1);
-  gemm_range_tg(a.dn_tg, a.dn_S, a.n_ctas, b, s.dn0, s.dn1);
-  gemm_range(a.lm_tg * a.lm_S, a.n_ctas, b, s.lm0, s.lm1);
+  if (a.det) {
+    gemm_range_whole(a.qkv_tg, a.qkv_S, a.n_ctas, b, s.qkv0, s.qkv1);
+    gemm_range_whole(a.o_tg, a.o_S, a.n_ctas, b, s.o0, s.o1);
+    gemm_range_whole(a.gu_tg, a.gu_S, a.n_ctas, b, s.gu0, s.gu1);
+    gemm_range_whole(a.dn_tg, a.dn_S, a.n_ctas, b, s.dn0, s.dn1);
+    gemm_range_whole(a.lm_tg, a.lm_S, a.n_ctas, b, s.lm0, s.lm1);
+  } else {
+    gemm_range_tg(a.qkv_tg, a.qkv_S, a.n_ctas, b, s.qkv0, s.qkv1);
+    gemm_range_tg(a.o_tg, a.o_S, a.n_ctas, b, s.o0, s.o1);
+    gemm_range_tg(a.gu_tg, a.gu_S, a.n_ctas, b, s.gu0, s.gu1);
+    gemm_range_tg(a.dn_tg, a.dn_S, a.n_ctas, b, s.dn0, s.dn1);
+    gemm_range(a.lm_tg * a.lm_S, a.n_ctas, b, s.lm0, s.lm1);
+  }
   const int KT = att_tile_keys(a.d);
   const int ntiles = (L + T0 + T + KT - 1) / KT;  // prefix + cached tree rows + new rows
   const int Z = (a.G * 8 * NT + 63) / 64;           // 64-row chunks of the G x T rows per kv head
@@ -834,6 +851,15 @@ SS_DEV void lm_unit(uint32_t sst, int warp, int lane, float (&acc)[NT][4]) {
 // computes from shared memory.  New residual rows also stay there for the
 // next GEMM's input.
 SS_DEV float norm_scale(const float* ss, int t, int h, float eps) { return rsqrtf(__ldcg(ss + t) / (float)h + eps); }
+// Deterministic mode (SS_DEBUG_DETERMINISTIC): the per-tile-group partial sums
+// of squares are added as 2^-24 fixed point in 64-bit integers (exact, any
+// order); the float entry holds only single-writer sums (the ingest kernel's).
+constexpr double kSsFx = 16777216.0;
+SS_DEV float norm_scale_a(const StepArgs& a, const float* ss, int t) {
+  float v = __ldcg(ss + t);
+  if (a.det) v += (float)((double)__ldcg(a.ssx + (ss - a.ss) + t) * (1.0 / kSsFx));
+  return rsqrtf(v / (float)a.h + a.eps);
+}
 
 template <int NT>
 struct TailSm {
@@ -885,7 +911,7 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
   const size_t qlo = (size_t)a.Hkv_l * rbmax * (d / 16) * 32 * 8;
   stage_acc<NT>(acc, ts.acc);
   if (threadIdx.x < T) {
-    ts.rs[threadIdx.x] = norm_scale(ssa, threadIdx.x, a.h, a.eps);
+    ts.rs[threadIdx.x] = norm_scale_a(a, ssa, threadIdx.x);
     ts.pos[threadIdx.x] = a.st->pos[s.T0 + threadIdx.x];
   }
   cbar();
@@ -952,7 +978,7 @@ SS_DEV void epi_swiglu(const StepArgs& a, int layer, int tg, const float* acc, i
   const int TP = NT * 8;
   const float* ssm = a.ss + (size_t)layer * 2 * 64 + 64;
   stage_acc<NT>(acc, ts.acc);
-  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale(ssm, threadIdx.x, a.h, a.eps);
+  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale_a(a, ssm, threadIdx.x);
   cbar();
   const int warp = threadIdx.x >> 5, cp = threadIdx.x & 31;
   for (int t = warp; t < T; t += 8) {
@@ -1134,7 +1160,10 @@ SS_DEV void next_input(const StepArgs& a, int tg, int T, const uint16_t* gain, f
   for (int t = warp; t < T; t += 8) {
     const float4 v = *reinterpret_cast<const float4*>(ts.xn + t * 128 + lane * 4);
     const float q = warp_sum(v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w);
-    if (lane == 0) atomicAdd(ss + t, q);
+    if (lane == 0) {
+      if (a.det) atomicAdd(a.ssx + (ss - a.ss) + t, __double2ull_rn((double)q * kSsFx));
+      else atomicAdd(ss + t, q);
+    }
     const float y0 = v.x * bf16_lo(gw.x), y1 = v.y * bf16_hi(gw.x), y2 = v.z * bf16_lo(gw.y), y3 = v.w * bf16_hi(gw.y);
     if (lm) {
       const uint32_t h01 = pack_bf16x2(y0, y1), h23 = pack_bf16x2(y2, y3);
@@ -1162,7 +1191,7 @@ SS_DEV void epi_argmax(const StepArgs& a, int tg, const float* acc, int T, const
   const int TP = NT * 8;
   const float* ssf = a.ss + (size_t)a.n_layers * 2 * 64;
   stage_acc<NT>(acc, ts.acc);
-  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale(ssf, threadIdx.x, a.h, a.eps);
+  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale_a(a, ssf, threadIdx.x);
   cbar();
   const int r = threadIdx.x & 127;
   const int v = tg * 128 + r;

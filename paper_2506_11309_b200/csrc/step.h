@@ -78,6 +78,8 @@ struct StepArgs {
   int* arr[5] = {nullptr};    // arrival counters per tile-group (self-cleaning)
   int* ctr = nullptr;         // [n_layers][kCtrPerLayer] + [kCtrGlobal]
   float* ss = nullptr;        // [n_layers + 1][2][64] sums of squares (0: attn-norm input, 1: mlp-norm input)
+  unsigned long long* ssx = nullptr;  // same shape, 2^-24 fixed point (deterministic mode)
+  int det = 0;                // SS_DEBUG_DETERMINISTIC: whole tile-groups per CTA, fixed-point norm sums
   float* att_ws = nullptr;    // [n_ctas][2 key halves][64 rows][d] unnormalised partial outputs
   float2* att_ml = nullptr;   // [n_ctas][2][64] (running max, sum)
   int rank = 0, P = 1, loopback = 0;

@@ -62,6 +62,7 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_set_debug", "ss_set_allreduce", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
            "ss_step_kernel_active", "ss_step_trace", "ss_read_step_trace", "ss_step_trace_host"]
 SS_DEBUG_CONSISTENCY = 1
+SS_DEBUG_DETERMINISTIC = 2
 
 
 def lib():

@@ -253,3 +253,37 @@ def test_duplicate_sibling_tokens_accept_lowest_index():
     acc, bonus = O.accept_walk(toks, par, rg["argmax"])
     assert rg["accepted"] == acc and rg["bonus"] == bonus
     sh.close()
+
+
+# ---------------------------------------------------------------- deterministic mode
+@pytest.mark.parametrize("cfg_name,L,T", [("tiny", 64, 8), ("small-tp", 64, 13), ("llama3-1b", 256, 16)])
+def test_deterministic_mode_bit_identical(cfg_name, L, T):
+    """SS_DEBUG_DETERMINISTIC: the same step run three times
+    gives bit-identical logits, argmax and tree K/V, and stays within the
+    oracle tolerance (R13)."""
+    import paper_2506_11309_b200 as pkg
+    from paper_2506_11309_b200 import swiftspec as ssp
+    from test_gpu_parity import build, check_logits, oracle_setup
+    cfg = synth.CONFIGS[cfg_name]
+    sh = build(cfg, L=L, max_ctx=L + 64, max_tree=32)
+    try:
+        sh.set_debug(ssp.SS_DEBUG_DETERMINISTIC)
+        toks, parents = synth.tree_paperlike(T, cfg.vocab, np.random.default_rng(T))
+        outs = []
+        for _ in range(3):
+            sh.set_committed_len(L)
+            r = sh.verify(toks, parents, want_logits=True)
+            k, v = sh.read_kv(cfg.n_layers - 1, L, T)
+            outs.append((r["logits"].copy(), list(r["argmax"]), k, v))
+        for lg, am, k, v in outs[1:]:
+            assert np.array_equal(lg, outs[0][0]) and am == outs[0][1]
+            assert np.array_equal(k, outs[0][2]) and np.array_equal(v, outs[0][3])
+        if cfg_name != "llama3-1b":
+            m, kv = oracle_setup(cfg, L=L, max_ctx=L + 64)
+            check_logits(outs[0][0], O.verify(cfg, m, kv, toks, parents)["logits"])
+        sh.set_debug(0)
+        sh.set_committed_len(L)
+        r = sh.verify(toks, parents, want_logits=True)
+        check_logits(r["logits"], outs[0][0])          # default mode: same values to the tolerance
+    finally:
+        sh.close()

@@ -140,7 +140,7 @@ SS_DEV void tmark(const StepArgs& a, int slot, int which) {
 // T <= 8: three A buffers (the dequant of unit k waits for unit k - 3's MMAs,
 // one unit more slack than two buffers); the accumulators fill the rest.
 constexpr uint32_t kTmemCols = 512;
-template <int NT> constexpr int kNbuf = NT == 1 ? 3 : 2;
+template <int NT> constexpr int kNbuf = 2;  // a third buffer at T <= 8 measured neutral (DESIGN 6b)
 template <int NT> constexpr uint32_t kAccColT = 128u * kNbuf<NT>;
 // accumulator slots [kNacc][AWQ group 2][N]: 4 at T <= 16 (the two warp sets
 // alternate two each, so a unit's MMAs never write the accumulator the
@@ -596,18 +596,17 @@ struct Tc {
   uint32_t ardy0;    // mbarrier[kNbuf]: the unit's A operand is in TMEM (8 warp arrivals)
   uint32_t mdone0;   // mbarrier[kNbuf buffers][2 groups]: MMAs reading the A buffer completed
   uint32_t* slot;    // shared [kNbuf]: smem address of the unit's ring slot (0 = stop)
-  uint32_t macc0;    // mbarrier[kNacc slots][2 groups]: MMAs writing the accumulator slot completed
 };
-// Accumulator slot k % kNacc is used by every kNacc-th unit; its epilogue waits
-// on the slot's own barrier (phase parity (k / kNacc) & 1), which cannot
-// complete again before that epilogue (the next writer of the slot is issued
-// after it in program order).  The A buffers have their own barriers.
+// The epilogue of unit k waits for its MMAs on the A buffer's barrier (phase
+// parity (k / kNbuf) & 1).  The barrier cannot complete again before: the next
+// user of the buffer, unit k + kNbuf, belongs to the same warp set (kNbuf = 2,
+// sets on alternating units) and is dequantised after this epilogue.
 template <int NT>
 SS_DEV void tc_wait_acc(const Tc& tc, int k) {
-  constexpr int NA = kNacc<NT>;
-  const int ac = k % NA;
-  mbar_wait_wd(tc.macc0 + 8 * (2 * ac), (uint32_t)((k / NA) & 1));
-  mbar_wait_wd(tc.macc0 + 8 * (2 * ac + 1), (uint32_t)((k / NA) & 1));
+  constexpr int NB = kNbuf<NT>;
+  const int b = k % NB;
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b), (uint32_t)((k / NB) & 1));
+  mbar_wait_wd(tc.mdone0 + 8 * (2 * b + 1), (uint32_t)((k / NB) & 1));
 }
 // Before unit k's dequant overwrites A buffer k % kNbuf: unit k - kNbuf's MMAs.
 template <int NT>
@@ -811,13 +810,10 @@ __device__ __noinline__ void mma_warp(const StepArgs* __restrict__ ap, Tc tc, in
             ;
       }
     }
-    // two commits (each tracks every prior MMA of this thread): the A buffer's
-    // barrier and the accumulator slot's
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t}"
-        ::"r"(tc.mdone0 + 8 * (2 * b + g)), "r"(tc.macc0 + 8 * (2 * (k % kNacc<NT>) + g))
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+        ::"r"(tc.mdone0 + 8 * (2 * b + g))
         : "memory");
     if (g == 0 && a.utl && blockIdx.x == 0 && lane_id() == 0 && k < 4096) a.utl[4096 + k * 2 + 1] = clk64();
   }
@@ -1828,13 +1824,13 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     step_kernel(const StepArgs* __restrict__ ap_g) {
   using C = StepCfg<NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[3], mdone[6], macc[8];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], ardy[2], mdone[4];
   __shared__ int s_done[128];
   __shared__ int s_nd;
   __shared__ float s_rmax[2 * 64];
   __shared__ Sched s_sched;
   __shared__ __align__(16) float s_merge[8 * 132];
-  __shared__ uint32_t s_tmem, s_slot[3];
+  __shared__ uint32_t s_tmem, s_slot[2];
   // the arguments and the per-layer pointer table live in shared memory: the
   // producer's per-unit address arithmetic must not chase global pointers
   __shared__ __align__(16) StepArgs s_args;
@@ -1856,7 +1852,6 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     }
     for (int i = 0; i < kNbuf<NT>; ++i) mbar_init(&ardy[i], 8);
     for (int i = 0; i < 2 * kNbuf<NT>; ++i) mbar_init(&mdone[i], 1);
-    for (int i = 0; i < 2 * kNacc<NT>; ++i) mbar_init(&macc[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) {  // the whole TMEM of the SM (one CTA per SM)
@@ -1871,7 +1866,7 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
   __syncthreads();
   const StepArgs* __restrict__ ap = &s_args;
   const uint32_t sm0 = smem_u32(smem), full0 = smem_u32(full), empty0 = smem_u32(empty);
-  const Tc tc{s_tmem, smem_u32(ardy), smem_u32(mdone), s_slot, smem_u32(macc)};
+  const Tc tc{s_tmem, smem_u32(ardy), smem_u32(mdone), s_slot};
   // everything below reads the ingest kernel's outputs (T, L, tree, counters)
   pdl_wait();
   pdl_trigger();

@@ -333,3 +333,41 @@ def test_loopback_two_shot_runs():
         assert r["status"] == 0
         sh.commit_accepted()
     sh.close()
+
+
+@pytest.mark.parametrize("ar", ["one-shot", "two-shot"])
+def test_ll_stress_million_lines(ar):
+    """LL protocol stress ("10^6-message stress"): 64 steps of
+    the 2-layer small-tp model at TP 2 over fake peers move 4 all-reduces x
+    8 tile-groups x 128 rows x 4 LL lines = 16K lines per rank per step (one-
+    shot; about half with two-shot), > 10^6 over the run, through both buffer
+    parities and 64 flag epochs.  Every step completes with SS_OK on both
+    ranks, the ranks agree, and since only the root is committed each step
+    (a chain the test controls) the oracle follows the same cache: the last
+    step's logits match it (R13)."""
+    cfg = synth.CONFIGS["small-tp"]
+    L = 64
+    P = 2
+    shards, m, kv = _setup(cfg, P, L)
+    for sh in shards:
+        sh.set_allreduce(ar)
+    rng = np.random.default_rng(99)
+    kvo = kv.copy()
+    for step in range(64):
+        tokens, parents = synth.tree_random(8, cfg.vocab, rng)
+        outs = _run(shards, tokens, parents)
+        assert all(o[0]["status"] == 0 for o in outs), (step, [o[0]["status"] for o in outs])
+        assert outs[0][0]["argmax"] == outs[1][0]["argmax"]
+        for sh in shards:
+            sh.commit_kv([0])
+        if step == 63:
+            ro = O.verify_sharded(cfg, m, kvo, tokens, parents, P)
+            logits = np.concatenate([lg for _, lg in outs], axis=1)
+            err = np.abs(logits - ro["logits"])
+            assert np.all(err <= 2e-2 + 1e-2 * np.abs(ro["logits"])), err.max()
+        else:
+            r = O.verify(cfg, m, kvo, tokens[:1], parents[:1])
+            O.commit(kvo, r, [0])
+    assert [sh.L for sh in shards] == [L + 64] * P
+    for sh in shards:
+        sh.close()

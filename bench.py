@@ -586,7 +586,7 @@ def other_configs(args, sh70, cfg70, local, dev, peak):
     return out
 
 
-def c_async(args, sh70, cfg70, local, dev, n_tokens=64, draft_sms=20, bs=8, w=8):
+def c_async(args, sh70, cfg70, local, dev, n_tokens=64, draft_sms=20, bs=8, w=8, spare_sms=8):
     """BASELINE configs[4] on one GPU: Alg. 1 parallel tree generation
     (ss_speculative_decode) with a Llama3-3B-shaped draft and the Llama3-70B-
     shaped target, 8K-token KV context in both.  The two GPU groups of the paper
@@ -603,7 +603,7 @@ def c_async(args, sh70, cfg70, local, dev, n_tokens=64, draft_sms=20, bs=8, w=8)
     Lc = 8192
     c3 = synth.CONFIGS["llama3-3b"]
     out = {"draft": c3.name, "target": cfg70.name, "L": Lc, "bs": bs, "w": w, "n_tokens": n_tokens,
-           "draft_sms": draft_sms, "target_sms": 148 - draft_sms}
+           "draft_sms": draft_sms, "target_sms": 148 - draft_sms - spare_sms}
     dr = pkg.Shard(c3, 0, 1, local, max_ctx=Lc + 4 * n_tokens + 256, max_tree=64)
     try:
         dr.synth_weights(args.seed + 17)
@@ -622,7 +622,7 @@ def c_async(args, sh70, cfg70, local, dev, n_tokens=64, draft_sms=20, bs=8, w=8)
             ref.append(cur)
         out["greedy_tokens_per_s"] = n_tokens / (_t.perf_counter() - t0)
         # profile for d: one target step and one draft expansion at their SM shares
-        sh70.set_launch_cap(148 - draft_sms)
+        sh70.set_launch_cap(148 - draft_sms - spare_sms)
         dr.set_launch_cap(draft_sms)
         sh70.set_committed_len(Lc)
         tt = time_steps(sh70, cfg70, bs, 2, 4, dev) / 1e3
@@ -654,6 +654,55 @@ def c_async(args, sh70, cfg70, local, dev, n_tokens=64, draft_sms=20, bs=8, w=8)
     finally:
         sh70.set_launch_cap(0)
         dr.close()
+    try:
+        out["self_draft_1b"] = self_draft(args, local, dev)
+    except Exception as ex:  # pragma: no cover
+        out["self_draft_1b"] = {"error": str(ex)}
+    return out
+
+
+def self_draft(args, local, dev, n_tokens=96, bs=8, w=8, draft_sms=64, spare_sms=8):
+    """Alg. 1 where the draft predicts the target: a Llama3-1B-shaped target and a
+    draft with the SAME weights (random weights give no real draft/target pair,
+    so this is the one setting whose acceptance is not ~0).  The draft's top-1
+    chain is the target's greedy path, so subtrees survive re-roots and the
+    draft's expansions during a verify are reused -- the async overlap of P:228
+    becomes visible (async vs serial tokens/s).  SM split as in c_async."""
+    import torch
+    import paper_2506_11309_b200 as pkg
+    c1 = synth.CONFIGS["llama3-1b"]
+    Lc = 1024
+    t = pkg.Shard(c1, 0, 1, local, max_ctx=Lc + 4 * n_tokens + 256, max_tree=bs)
+    d = pkg.Shard(c1, 0, 1, local, max_ctx=Lc + 4 * n_tokens + 256, max_tree=64)
+    out = {"model": c1.name, "L": Lc, "bs": bs, "w": w, "n_tokens": n_tokens, "draft_sms": draft_sms,
+           "target_sms": 148 - draft_sms - spare_sms}
+    try:
+        for sh in (t, d):
+            sh.synth_weights(args.seed)
+            sh.synth_prefix_kv(args.seed + 1, Lc)
+        t.set_launch_cap(148 - draft_sms - spare_sms)
+        d.set_launch_cap(draft_sms)
+        ts, ds = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        root = 4321
+        res = {}
+        for dd in (1, 2, 4):
+            for mode in ("async", "serial"):
+                t.set_committed_len(Lc)
+                d.set_committed_len(Lc)
+                toks, st = t.speculative_decode(d, root, n_tokens, bs=bs, w=w, d=dd, mode=mode,
+                                                target_stream=ts, draft_stream=ds)
+                res[f"{mode}/d{dd}"] = {"tokens_per_s": st["n_emitted"] / (st["wall_ms"] / 1e3),
+                                        "mean_emitted_per_step": st["n_emitted"] / max(st["steps"], 1),
+                                        "expansions": st["expansions"], "tokens": toks}
+        ref = res["serial/d1"]["tokens"]
+        for k, v in res.items():
+            v["matches_serial_d1"] = v.pop("tokens") == ref
+        out["runs"] = res
+        out["how"] = ("wall clock around ss_speculative_decode; identical draft and target weights; d = expansions "
+                      "per round; outputs must agree across modes (all are the target's greedy decode)")
+    finally:
+        t.close()
+        d.close()
     return out
 
 

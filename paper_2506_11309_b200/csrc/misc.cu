@@ -340,10 +340,12 @@ void launch_embed_meta(ss_shard* s, const int32_t* tokens, const int32_t* parent
     si.K_o = s->Hq_l * s->cfg.head_dim;
     si.K_d = s->I_l;
   }
+  ss_pdl_off = s->launch_cap > 0 && !s->loopback;  // capped grids share the GPU (kernels.h)
   launch_pdl(embed_meta_kernel, dim3(8 * NT, kNormSplit), dim3(256), 0, st, s->dstate, tokens, parents, T,
              (const uint16_t*)s->embed, s->cfg.vocab, s->cfg.hidden, s->x, g0, s->act_h, NT, s->cfg.rms_eps,
              2 * s->cfg.n_layers + 2, from_mailbox ? (const uint4*)s->mbox_in : (const uint4*)nullptr,
              s->cfg.max_tree, ca, si, T0);
+  ss_pdl_off = false;
 }
 
 // ---------------------------------------------------------------- a13 draft-side helpers

@@ -952,7 +952,7 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
   const ss_model_cfg& c = s->cfg;
   int n = 0;
   if (step_path(s, NT)) {
-    ss_pdl_off = s->P > 1 && s->launch_cap > 0 && !s->loopback;
+    ss_pdl_off = s->launch_cap > 0 && !s->loopback;  // capped: shares the GPU (fake peers, async split)
     StepArgs a = step_args(s, want_logits);
     a.n_ctas = step_ctas(NT, c.head_dim, s->launch_cap);
     PROF_BEGIN(9);
@@ -979,8 +979,9 @@ static int enqueue_body(ss_shard* s, int NT, int auto_commit, int want_logits, c
   constexpr int skip = 0;
 #endif
   const int cap = s->launch_cap;
-  // fake-peer TP (ranks share this GPU): no PDL, see ss_pdl_off
-  ss_pdl_off = s->P > 1 && cap > 0 && !s->loopback;
+  // capped grids share this GPU (fake-peer TP ranks, the two groups of the
+  // async split): no PDL, see ss_pdl_off
+  ss_pdl_off = cap > 0 && !s->loopback;
   for (int l = 0; l < c.n_layers; ++l) {
     LayerW& lw = s->layers[l];
     GemmArgs g = gemm_args(s, lw.qkv, s->act_h, s->sc_qkv, EPI_QKV, l);
@@ -1648,7 +1649,7 @@ extern "C" ss_status ss_debug_gemm(ss_shard* s, int32_t layer, int32_t which, co
   g.epi.h = pl.N;
   g.epi.P = allreduce ? s->P : 1;
   g.epi.ar_seq = 0;
-  ss_pdl_off = s->P > 1 && s->launch_cap > 0 && !s->loopback;
+  ss_pdl_off = s->launch_cap > 0 && !s->loopback;  // capped: shares the GPU (fake peers, async split)
   launch_gemm(g, 0, NT, s->launch_cap, st);
   ss_pdl_off = false;
   CUDA_TRY(cudaGetLastError());

@@ -27,6 +27,8 @@ ss_status fail(ss_shard* s, ss_status code, const std::string& m) {
   return code;
 }
 
+constexpr int kSpareSms = 8;
+
 struct Outbox {
   void* dev = nullptr;     // (1 + SS_MAX_TREE) LL lines the target posts into
   int32_t* res = nullptr;  // device copy of a received result: [4 + 2 * SS_MAX_TREE]
@@ -54,8 +56,13 @@ extern "C" ss_status ss_speculative_decode(ss_shard* target, ss_shard* draft, in
     // async: both groups' kernels must be resident at once -- the target's
     // step (launched early under PDL) waits on the inbox the draft fills
     if (ts == ds) return fail(target, SS_EINVAL, "async mode needs two different streams");
-    if (target->launch_cap <= 0 || draft->launch_cap <= 0 || target->launch_cap + draft->launch_cap > target->n_sm)
-      return fail(target, SS_EINVAL, "async mode: cap both grids (ss_set_launch_cap) to a split of the SMs");
+    // the two persistent grids plus room for the small kernels (ingest, commit,
+    // top-K, re-root, mailbox): a persistent grid that waits for an SM held by
+    // a small kernel of the other group would deadlock on the group hand-off
+    if (target->launch_cap <= 0 || draft->launch_cap <= 0 ||
+        target->launch_cap + draft->launch_cap > target->n_sm - kSpareSms)
+      return fail(target, SS_EINVAL, "async mode: cap both grids (ss_set_launch_cap) to a split of the SMs "
+                                     "that leaves 8 SMs free");
   }
 
   Outbox ob;

@@ -141,8 +141,8 @@ def test_speculative_decode_is_target_greedy(mode, draft_seed):
     cfg, t, dr, m, kv = _pair(draft_seed)
     try:
         if mode == "async":
-            t.set_launch_cap(100)
-            dr.set_launch_cap(48)
+            t.set_launch_cap(96)
+            dr.set_launch_cap(44)
         ts, ds = torch.cuda.Stream(), torch.cuda.Stream()
         root, n = 321, 40
         out, st = t.speculative_decode(dr, root, n, bs=8, w=8, d=2, mode=mode, target_stream=ts, draft_stream=ds)

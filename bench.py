@@ -316,6 +316,7 @@ def run_ours(args, cfg):
 
     # ---- e2e: same metric through the public C-ABI with HOST buffers
     # (H2D of the tree, D2H of the result inside ss_verify_tree, every step)
+    _skip = set(os.environ.get("SS_BENCH_SKIP", "").split(","))  # debugging aid (bisection)
     e2e_steps = max(3, args.steps // 2)
     torch.cuda.synchronize()
     if world > 1:
@@ -337,7 +338,7 @@ def run_ours(args, cfg):
     prof = None
     try:
         i0 = n_steps - 1
-        for _ in range(2):
+        for _ in range(0 if "prof" in _skip else 2):
             prof = sh.profile_step(d_tok[i0], d_par[i0], T, stream=stream)
     except Exception as ex:  # pragma: no cover
         prof = {"error": str(ex)}
@@ -403,7 +404,7 @@ def run_ours(args, cfg):
         line["kernel_times_us"] = {k: {"total": v[0] * 1e3, "launches": v[1]} for k, v in prof.items()}
     try:  # where the step's time goes (extra traced step, outside the timed region)
         sm_mhz = line["clocks"].get("sm_mhz") or 1965.0
-        bd = phase_breakdown(sh, cfg, d_tok, d_par, T, n_steps - 2, stream, sm_mhz)
+        bd = None if "breakdown" in _skip else phase_breakdown(sh, cfg, d_tok, d_par, T, n_steps - 2, stream, sm_mhz)
         if bd:
             line["breakdown"] = bd
     except Exception as ex:  # pragma: no cover
@@ -415,11 +416,27 @@ def run_ours(args, cfg):
             line[key] = fn()
         except Exception as ex:  # pragma: no cover
             line[key] = {"error": str(ex)[:300]}
-    if world == 1 and not args.no_extra:
+    if world == 1 and not args.no_extra and "other" not in _skip:
         extra("other_configs", lambda: other_configs(args, sh, cfg, local, dev, peak))
     if world == 1 and not args.no_tp_emulate:
+        diag = os.environ.get("SS_BENCH_DIAG") == "1"  # debugging aid: hang/fault progress words
+        if diag:
+            sh.step_trace(2)
         extra("decode_planted", lambda: decode_planted(sh, cfg, T, L))
-        extra("tp_emulated", lambda: tp_emulated(args, cfg, local, dev, peak))
+        if diag and "error" in line["decode_planted"]:
+            from collections import Counter
+            wh = sh.step_trace_where()
+            cnt = Counter()
+            for c_ in range(148):
+                words = []
+                for w_ in range(12):
+                    code = int(wh[c_, w_]) >> 32
+                    words.append(f"{code >> 16}.{(code >> 8) & 0xFF:x}.{code & 0xFF:x}")
+                cnt[tuple(words)] += 1
+            for k_, v_ in cnt.most_common(8):
+                print("DIAG", v_, "CTAs:", " | ".join(k_), file=sys.stderr, flush=True)
+        if "tp" not in _skip:
+            extra("tp_emulated", lambda: tp_emulated(args, cfg, local, dev, peak))
     if world == 1 and not args.no_async and cfg.name == "llama3-70b":
         extra("c_async", lambda: c_async(args, sh, cfg, local, dev))
     if rank == 0 and not args.no_cpu_baseline:
@@ -479,8 +496,11 @@ def decode_planted(sh, cfg, T, L, n_steps=24, mean_emit=3.1, seed=5):
     need = n_steps * (T + 1) + T + 2
     sh.set_committed_len(L)
     seq = [1]
-    for _ in range(need):
-        r = sh.verify(np.array([seq[-1]], dtype=np.int32), np.array([-1], dtype=np.int32))
+    for k in range(need):
+        try:
+            r = sh.verify(np.array([seq[-1]], dtype=np.int32), np.array([-1], dtype=np.int32))
+        except Exception as ex:
+            raise RuntimeError(f"greedy T=1 step {k} (L = {L + k}): {ex}") from ex
         sh.commit_accepted()
         seq.append(int(r["bonus"]))
     sh.set_committed_len(L)
@@ -491,7 +511,10 @@ def decode_planted(sh, cfg, T, L, n_steps=24, mean_emit=3.1, seed=5):
     for _ in range(n_steps):
         d = int(min(T - 1, 7, rng.geometric(1.0 / mean_emit) - 1))
         toks, par = planted_tree(seq, pos, d, T, cfg.vocab, rng)
-        r = sh.verify(toks, par)
+        try:
+            r = sh.verify(toks, par)
+        except Exception as ex:
+            raise RuntimeError(f"planted step {len(mism_steps)}: {ex}") from ex
         sh.commit_accepted()
         n = int(r["n_accepted"])                     # root + accepted draft nodes
         got = [int(toks[i]) for i in r["accepted"][1:]] + [int(r["bonus"])]

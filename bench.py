@@ -496,13 +496,35 @@ def decode_planted(sh, cfg, T, L, n_steps=24, mean_emit=3.1, seed=5):
     need = n_steps * (T + 1) + T + 2
     sh.set_committed_len(L)
     seq = [1]
-    for k in range(need):
+    dmode = os.environ.get("SS_BENCH_DECODE", "")  # debugging aid (the open decode fault, DESIGN 10)
+    import torch
+    for k in range(need * (int(dmode[3:]) if dmode.startswith("rep") else 1)):
+        import time as _tt
+        _t0 = _tt.perf_counter()
         try:
             r = sh.verify(np.array([seq[-1]], dtype=np.int32), np.array([-1], dtype=np.int32))
         except Exception as ex:
-            raise RuntimeError(f"greedy T=1 step {k} (L = {L + k}): {ex}") from ex
+            from paper_2506_11309_b200 import swiftspec as _ssp
+            raise RuntimeError(f"greedy T=1 step {k} (L = {L + k}, {_tt.perf_counter() - _t0:.3f} s, "
+                               f"watchdog {_ssp.watchdog_record(6)}, ctr {sh.debug_ctr_base()}): {ex}") from ex
         sh.commit_accepted()
+        if dmode == "sync":
+            torch.cuda.synchronize()
         seq.append(int(r["bonus"]))
+        if dmode.startswith("rep") and k % need == need - 1:
+            sh.set_committed_len(L)
+            seq = [1]
+    if dmode.startswith("rep"):  # the last round's sequence is the one used below
+        sh.set_committed_len(L)
+        seq = [1]
+        for k in range(need):
+            _t0 = _tt.perf_counter()
+            try:
+                r = sh.verify(np.array([seq[-1]], dtype=np.int32), np.array([-1], dtype=np.int32))
+            except Exception as ex:
+                raise RuntimeError(f"greedy T=1 last-round step {k} ({_tt.perf_counter() - _t0:.3f} s): {ex}") from ex
+            sh.commit_accepted()
+            seq.append(int(r["bonus"]))
     sh.set_committed_len(L)
     pos, emitted, match = 0, 0, True
     mism, mism_steps = [], []

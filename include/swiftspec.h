@@ -189,6 +189,18 @@ const char* ss_last_error(const ss_shard* s);
 #define SS_DEBUG_DETERMINISTIC 2
 ss_status ss_set_debug(ss_shard* s, int32_t flags);
 
+/* Watchdog record (debugging aid): every wait of the persistent step kernel is
+ * bounded (~10 s of SM clock); the first one that times out writes
+ * out[0] = 1 + site (0 idle producer, 1 mbarrier, 2 global counter), out[1] =
+ * the barrier's shared address or the counter's global address, out[2] =
+ * parity / target, out[3] = the counter value seen, out[4] = blockIdx.x,
+ * out[5] = threadIdx.x, then traps (the launch fails).  Process-wide, readable
+ * after the failure (mapped host memory).  n <= 512. */
+ss_status ss_watchdog_record(uint64_t* out, int32_t n);
+/* Device address of the shard's per-layer phase counters ([n_layers][48] int32 +
+ * globals), to decode a counter address of the watchdog record. */
+uint64_t ss_debug_ctr_base(ss_shard* s);
+
 /* ---- weights and KV ------------------------------------------------------ */
 
 /* Copy one canonical host tensor (layer ignored for global kinds) into the

@@ -126,6 +126,9 @@ struct StepArgs;
 int launch_step(const StepArgs& a, const StepArgs* dev_args, int NT, int max_ctas, cudaStream_t st);
 int step_ctas(int NT, int d, int max_ctas);
 void warm_step_kernels();
+// watchdog panic record of the step kernel (mapped host memory; debugging aid)
+void arm_watchdog_record();
+const unsigned long long* watchdog_record();
 // force-load every kernel (lazy module loading vs cross-kernel flag waits)
 void warm_gemm_kernels();
 void warm_attention_kernels();

@@ -288,6 +288,7 @@ extern "C" ss_status ss_init_shard(const ss_model_cfg* cfg, int32_t tp_rank, int
   warm_attention_kernels();
   warm_misc_kernels();
   warm_draft_kernels();
+  arm_watchdog_record();
   warm_step_kernels();
   ss_shard* s = new ss_shard();
   s->cfg = c;
@@ -1375,6 +1376,15 @@ extern "C" ss_status ss_read_step_trace(ss_shard* s, uint64_t* host, size_t n, i
 extern "C" int32_t ss_step_kernel_active(ss_shard* s, int32_t T) {
   if (!s || T < 1 || T > SS_MAX_TREE) return -1;
   return step_path(s, nt_of(T)) ? 1 : 0;
+}
+
+extern "C" uint64_t ss_debug_ctr_base(ss_shard* s) { return s ? (uint64_t)(uintptr_t)s->step_ctr : 0; }
+
+extern "C" ss_status ss_watchdog_record(uint64_t* out, int32_t n) {
+  const unsigned long long* r = watchdog_record();
+  if (!out || n < 0 || n > 64 * 1024) return SS_EINVAL;
+  for (int i = 0; i < n; ++i) out[i] = r ? r[i] : 0;
+  return SS_OK;
 }
 
 extern "C" ss_status ss_set_debug(ss_shard* s, int32_t flags) {

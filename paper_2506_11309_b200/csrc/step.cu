@@ -81,8 +81,38 @@ SS_DEV unsigned long long clk64() {
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
   return c;
 }
+// Panic record of the first wait that times out (mapped host memory, read by
+// ss_watchdog_record after the failed launch): [0] = 1 + site, [1] = address
+// (shared-memory barrier or global counter), [2] = parity / target, [3] =
+// value seen, [4] = blockIdx.x, [5] = threadIdx.x, [6] = ring / unit info.
+__device__ unsigned long long* g_panic = nullptr;
+// Every timed-out waiter also fills its warp's slot [64 + (block * 16 + warp) * 4]
+// (site + 1, address, parity / target, seen) and lingers ~1 s before trapping,
+// so the other waiters of a deadlock record themselves too.
+SS_DEV void panic_trap(int site, unsigned long long addr, unsigned long long want, unsigned long long seen) {
+  unsigned long long* p = g_panic;
+  if (p) {
+    if (atomicCAS(p, 0ull, (unsigned long long)(1 + site)) == 0ull) {
+      p[1] = addr;
+      p[2] = want;
+      p[3] = seen;
+      p[4] = blockIdx.x;
+      p[5] = threadIdx.x;
+    }
+    unsigned long long* q = p + 64 + ((size_t)blockIdx.x * 16 + (threadIdx.x >> 5)) * 4;
+    q[0] = 1 + site;
+    q[1] = addr;
+    q[2] = want;
+    q[3] = seen;
+    __threadfence_system();
+    const unsigned long long t = clk64();
+    while (clk64() - t < 2000000000ull) __nanosleep(1000);
+  }
+  asm volatile("trap;");
+}
 SS_DEV void watchdog(unsigned long long t0) {
-  if (clk64() - t0 > kWatchdogClk) asm volatile("trap;");
+  // the producer's idle wait: twice the bound, so the wait that starved it is recorded first
+  if (clk64() - t0 > 2 * kWatchdogClk) panic_trap(0, 0, 0, 0);
 }
 SS_DEV bool mbar_try_a(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -98,7 +128,8 @@ SS_DEV bool mbar_try_a(uint32_t bar, uint32_t parity) {
 SS_DEV void mbar_wait_wd(uint32_t bar, uint32_t parity) {
   if (mbar_try_a(bar, parity)) return;
   const unsigned long long t0 = clk64();
-  while (!mbar_try_a(bar, parity)) watchdog(t0);
+  while (!mbar_try_a(bar, parity))
+    if (clk64() - t0 > kWatchdogClk) panic_trap(1, bar, parity, 0);
 }
 SS_DEV int ld_relaxed_gpu(const int* p) {
   int v;
@@ -112,7 +143,7 @@ SS_DEV void spin_until_geq(const int* p, int target) {
   const unsigned long long t0 = clk64();
   while (ld_relaxed_gpu(p) < target) {
     __nanosleep(64);
-    watchdog(t0);
+    if (clk64() - t0 > kWatchdogClk) panic_trap(2, (unsigned long long)p, target, ld_relaxed_gpu(p));
   }
   (void)ld_acquire_gpu(p);
 }
@@ -687,9 +718,15 @@ SS_DEV void tc_signal_q(const Tc& tc, uint32_t sst, int b, int qd, int lane) {
 }
 // Epilogue of unit k for rows 32 qd + lane, both AWQ groups.
 template <int NT>
-SS_DEV void tc_epilogue_q(const Tc& tc, uint32_t sst, int k, int qd, int lane, float (&y)[8 * NT]) {
+// waited: the set already observed unit k's MMA completion (its tc_wait_buf
+// for unit k + 2).  The epilogue must not wait on the buffer's barrier after
+// unit k + 2 was handed to the MMA warps: if k + 2's MMAs completed first, the
+// barrier's phase parity would read as k's phase still pending (two phases
+// later) and the set would wait for unit k + 4, which only it can produce --
+// the intermittent deadlock (watchdog trap) of round 2's T = 1 decode steps.
+SS_DEV void tc_epilogue_q(const Tc& tc, uint32_t sst, int k, int qd, int lane, float (&y)[8 * NT], bool waited) {
   constexpr int TP = 8 * NT, N = 16 * NT;
-  tc_wait_acc<NT>(tc, k);
+  if (!waited) tc_wait_acc<NT>(tc, k);
   __syncwarp();
   tc_fence_after();
   const int m = 32 * qd + lane, tile = m >> 4, r16 = m & 15, g8 = r16 & 7, up = r16 >> 3;
@@ -1297,7 +1334,8 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
       if (have) tc_signal_q(tc, sst, (tck + (um - u0)) % kNbuf<NT>, qd, lane);
       if (u_prev >= 0) {
         where(a, WCODE(layer, PH, 3));
-        tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y);
+        // have: tc_wait_buf above waited for exactly u_prev's MMAs (unit k - 2)
+        tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y, have);
         if (utl && u_prev - u0 < 127) utl[(u_prev - u0) * 8 + 3] = clk64();
         flush_prev(u_prev);
       }
@@ -1307,7 +1345,7 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
       sst_prev = sst;
     }
     if (u_prev >= 0) {
-      tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y);
+      tc_epilogue_q<NT>(tc, sst_prev, tck + (u_prev - u0), qd, lane, y, false);
       if (utl && u_prev - u0 < 127) utl[(u_prev - u0) * 8 + 3] = clk64();
       flush_prev(u_prev);
     }
@@ -1845,6 +1883,13 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     const int nl = ap_g->n_layers;
     for (int i = threadIdx.x; i < nl * (int)(sizeof(LayerPtrs) / 8); i += blockDim.x) ldst[i] = lsrc[i];
   }
+  if (threadIdx.x == 0 && blockIdx.x == 0 && g_panic) {  // barrier map for the watchdog record
+    g_panic[8] = smem_u32(full);
+    g_panic[9] = smem_u32(empty);
+    g_panic[10] = smem_u32(ardy);
+    g_panic[11] = smem_u32(mdone);
+    g_panic[12] = C::STAGES;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -1962,6 +2007,22 @@ int launch_step(const StepArgs& a, const StepArgs* dev_args, int NT, int max_cta
     default: return launch_step_t<4, 128>(a, dev_args, max_ctas, st);
   }
 }
+
+// Watchdog panic record (debugging aid, always armed: one mapped host page).
+static unsigned long long* g_panic_host = nullptr;
+void arm_watchdog_record() {
+  if (g_panic_host) return;
+  unsigned long long* dev = nullptr;
+  if (cudaHostAlloc((void**)&g_panic_host, 64 * 1024 * 8, cudaHostAllocMapped) != cudaSuccess) {
+    g_panic_host = nullptr;
+    cudaGetLastError();
+    return;
+  }
+  memset(g_panic_host, 0, 64 * 1024 * 8);
+  cudaHostGetDevicePointer((void**)&dev, g_panic_host, 0);
+  cudaMemcpyToSymbol(g_panic, &dev, sizeof(dev));
+}
+const unsigned long long* watchdog_record() { return g_panic_host; }
 
 void warm_step_kernels() {
   cudaFuncAttributes at;

@@ -59,10 +59,17 @@ EXPORTS = ["ss_init_shard", "ss_export_handle", "ss_import_peers", "ss_import_lo
            "ss_commit_kv",
            "ss_commit_accepted", "ss_kernels_per_step", "ss_profile_step", "ss_mailbox_inbox",
            "ss_attach_mailbox", "ss_verify_tree_mailbox", "ss_verify_tree_mailbox_n", "ss_mailbox_post_tree", "ss_mailbox_recv_result",
-           "ss_set_debug", "ss_set_allreduce", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
+           "ss_set_debug", "ss_watchdog_record", "ss_debug_ctr_base", "ss_set_allreduce", "ss_read_tree_meta", "ss_read_packed", "ss_debug_gemm", "ss_set_step_kernel",
            "ss_step_kernel_active", "ss_step_trace", "ss_read_step_trace", "ss_step_trace_host"]
 SS_DEBUG_CONSISTENCY = 1
 SS_DEBUG_DETERMINISTIC = 2
+
+
+def watchdog_record(n: int = 8):
+    """The step kernel's watchdog panic record (ss_watchdog_record)."""
+    out = np.zeros(n, dtype=np.uint64)
+    lib().ss_watchdog_record(out.ctypes.data_as(C.c_void_p), n)
+    return [int(x) for x in out]
 
 
 def lib():
@@ -86,6 +93,8 @@ def lib():
         "ss_last_error": (C.c_char_p, [vp]),
         "ss_set_debug": (i32, [vp, i32]),
         "ss_set_allreduce": (i32, [vp, i32]),
+        "ss_watchdog_record": (i32, [vp, i32]),
+        "ss_debug_ctr_base": (u64, [vp]),
         "ss_set_step_kernel": (i32, [vp, i32]),
         "ss_step_kernel_active": (i32, [vp, i32]),
         "ss_step_trace": (i32, [vp, i32]),
@@ -417,6 +426,9 @@ class Shard:
     def import_loopback(self):
         """Timing emulation of this rank alone (include/swiftspec.h ss_import_loopback)."""
         self._ck(lib().ss_import_loopback(self.h))
+
+    def debug_ctr_base(self) -> int:
+        return int(lib().ss_debug_ctr_base(self.h))
 
     def set_allreduce(self, mode: str):
         """'one-shot' (default) or 'two-shot' TP all-reduce in the step kernel (ss_set_allreduce)."""

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "swiftspec.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:ss_status|int32_t|const char\*|void\*)\s+(ss_[a-z_]+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:ss_status|int32_t|uint64_t|const char\*|void\*)\s+(ss_[a-z_]+)\s*\(", src, re.M)))
 
 
 def test_header_symbols_exported():

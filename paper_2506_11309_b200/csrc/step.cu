@@ -86,10 +86,12 @@ SS_DEV unsigned long long clk64() {
 // (shared-memory barrier or global counter), [2] = parity / target, [3] =
 // value seen, [4] = blockIdx.x, [5] = threadIdx.x, [6] = ring / unit info.
 __device__ unsigned long long* g_panic = nullptr;
+__device__ int g_panic_map = 0;
 // Every timed-out waiter also fills its warp's slot [64 + (block * 16 + warp) * 4]
 // (site + 1, address, parity / target, seen) and lingers ~1 s before trapping,
 // so the other waiters of a deadlock record themselves too.
 SS_DEV void panic_trap(int site, unsigned long long addr, unsigned long long want, unsigned long long seen) {
+#ifdef SS_WATCHDOG_RECORD  // debugging builds (tools/wd70.py): record every timed-out waiter
   unsigned long long* p = g_panic;
   if (p) {
     if (atomicCAS(p, 0ull, (unsigned long long)(1 + site)) == 0ull) {
@@ -108,6 +110,9 @@ SS_DEV void panic_trap(int site, unsigned long long addr, unsigned long long wan
     const unsigned long long t = clk64();
     while (clk64() - t < 2000000000ull) __nanosleep(1000);
   }
+#else
+  (void)site; (void)addr; (void)want; (void)seen;
+#endif
   asm volatile("trap;");
 }
 SS_DEV void watchdog(unsigned long long t0) {
@@ -1883,13 +1888,16 @@ __global__ void __launch_bounds__(StepCfg<NT>::THREADS, StepCfg<NT>::CTAS_PER_SM
     const int nl = ap_g->n_layers;
     for (int i = threadIdx.x; i < nl * (int)(sizeof(LayerPtrs) / 8); i += blockDim.x) ldst[i] = lsrc[i];
   }
-  if (threadIdx.x == 0 && blockIdx.x == 0 && g_panic) {  // barrier map for the watchdog record
+#ifdef SS_WATCHDOG_RECORD
+  if (threadIdx.x == 0 && blockIdx.x == 0 && !g_panic_map && g_panic) {  // barrier map (first launch)
+    g_panic_map = 1;
     g_panic[8] = smem_u32(full);
     g_panic[9] = smem_u32(empty);
     g_panic[10] = smem_u32(ardy);
     g_panic[11] = smem_u32(mdone);
     g_panic[12] = C::STAGES;
   }
+#endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);

@@ -953,40 +953,51 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
     ts.pos[threadIdx.x] = a.st->pos[s.T0 + threadIdx.x];
   }
   cbar();
-  float2 cs[IT];
+  // each thread: a pair of adjacent rows (features j, j + 1 of one head) of one
+  // token, so every q-fragment / cache store writes both halves at once
+  constexpr int IT2 = IT / 2;
+  float4 cs[IT2];
 #pragma unroll
-  for (int i = 0; i < IT; ++i) {  // RoPE table entries first (independent loads)
-    const int idx = threadIdx.x + i * 256, r = idx / TP, t = idx % TP;
+  for (int i = 0; i < IT2; ++i) {  // RoPE table entries first (independent loads)
+    const int idx = threadIdx.x + i * 256, r = 2 * (idx / TP), t = idx % TP;
     const int row = tg * 128 + r, j = row % d;
-    cs[i] = (t < T && row < nq + nk) ? __ldg(&a.rope_cs[(size_t)ts.pos[t] * half + (j % half)]) : make_float2(1.f, 0.f);
+    cs[i] = (t < T && row < nq + nk)
+                ? __ldg(reinterpret_cast<const float4*>(&a.rope_cs[(size_t)ts.pos[t] * half + (j % half)]))
+                : make_float4(1.f, 0.f, 1.f, 0.f);
   }
 #pragma unroll
-  for (int i = 0; i < IT; ++i) {
-    const int idx = threadIdx.x + i * 256, r = idx / TP, t = idx % TP;
+  for (int i = 0; i < IT2; ++i) {
+    const int idx = threadIdx.x + i * 256, r = 2 * (idx / TP), t = idx % TP;
     if (t >= T) continue;
     const int row = tg * 128 + r, j = row % d;
     const float rs = ts.rs[t];
-    float x = ts.acc[r * TP + t] * rs;
+    float x0 = ts.acc[r * TP + t] * rs, x1 = ts.acc[(r + 1) * TP + t] * rs;
     if (row < nq + nk) {
       const int pr = (j < half) ? r + half : r - half;
-      const float pv = ts.acc[pr * TP + t] * rs;
-      x = (j < half) ? (x * cs[i].x - pv * cs[i].y) : (x * cs[i].x + pv * cs[i].y);
+      const float p0 = ts.acc[pr * TP + t] * rs, p1 = ts.acc[(pr + 1) * TP + t] * rs;
+      if (j < half) {
+        x0 = x0 * cs[i].x - p0 * cs[i].y;
+        x1 = x1 * cs[i].z - p1 * cs[i].w;
+      } else {
+        x0 = x0 * cs[i].x + p0 * cs[i].y;
+        x1 = x1 * cs[i].z + p1 * cs[i].w;
+      }
     }
-    const __half hh = __float2half_rn(x);
-    const __half hl = __float2half_rn(x - __half2float(hh));
+    uint32_t hi, lo2;
+    split16(x0, x1, hi, lo2);
     if (row < nq) {
       const int hq = row / d, kvh = hq / a.G, jj = hq - kvh * a.G;
-      const uint32_t fi = q_frag_index(t * a.G + jj, j, d, rbmax, kvh);
-      a.qf[fi] = __half_as_ushort(hh);
-      a.qf[qlo + fi] = __half_as_ushort(hl);
+      const uint32_t fi = q_frag_index(t * a.G + jj, j, d, rbmax, kvh);  // j even: j + 1 at fi + 1
+      *reinterpret_cast<uint32_t*>(a.qf + fi) = hi;
+      *reinterpret_cast<uint32_t*>(a.qf + qlo + fi) = lo2;
     } else if (row < nq + 2 * nk) {
       const bool isk = row < nq + nk;
       const int kvh = (isk ? row - nq : row - nq - nk) / d;
       uint16_t* c = isk ? a.kc : a.vc;
       uint16_t* lo = isk ? a.klo : a.vlo;
       const size_t base = ((size_t)layer * a.Hkv_l + kvh) * a.max_ctx_pad * d;
-      c[base + kv_elem_offset(R + t, j, d)] = __half_as_ushort(hh);
-      lo[(size_t)kvh * 128 * d + kv_elem_offset(R + t - wb, j, d)] = __half_as_ushort(hl);
+      *reinterpret_cast<uint32_t*>(c + base + kv_elem_offset(R + t, j, d)) = hi;
+      *reinterpret_cast<uint32_t*>(lo + (size_t)kvh * 128 * d + kv_elem_offset(R + t - wb, j, d)) = lo2;
     }
   }
   // zero the lo window rows outside this step's new rows of this tile-group's

@@ -201,3 +201,88 @@ def test_cpp_tree_matches_reference(dt, seed):
         assert _nodes(dt, h) == _ref_nodes(ref) and dt.dt_troot(h) == ref.troot
         assert dt.dt_n_slots(h) == ref.n_slots
     dt.dt_free(h)
+
+
+# ---------------------------------------------------------------- Alg. 1 end to end (reference)
+def _toy_models(V, agree, seed):
+    """A deterministic toy target (greedy next token = hash of the last two
+    tokens) and a toy draft that proposes the target's token first with
+    probability `agree` (else a different one), with log-probabilities."""
+    rng = np.random.default_rng(seed)
+    table = rng.integers(0, V, size=(V, V))
+    flip = rng.random((V, V)) < agree
+
+    def target_next(seq):
+        a, b = (seq[-2], seq[-1]) if len(seq) > 1 else (0, seq[-1])
+        return int(table[a, b])
+
+    def draft_topk(seq, K):
+        a, b = (seq[-2], seq[-1]) if len(seq) > 1 else (0, seq[-1])
+        t = int(table[a, b])
+        first = t if flip[a, b] else (t + 1) % V
+        toks = [first] + [(first + 7 * (i + 1)) % V for i in range(K - 1)]
+        lps = [-0.2 - 0.5 * i for i in range(K)]
+        return toks, lps
+    return target_next, draft_topk
+
+
+@pytest.mark.parametrize("agree,d", [(0.9, 2), (0.5, 1), (0.0, 3)])
+def test_ref_alg1_loop_emits_target_greedy(agree, d):
+    """Alg. 1 run on the reference tree with toy models: whatever
+    the draft proposes, the emitted tokens are the target's greedy sequence
+    (S:453); the committed draft prefix is always a prefix of the target's
+    committed tokens; commit slots form a root-anchored chain and kept slots
+    ascend (the device re-root's contract)."""
+    V, K, w, bs = 40, 4, 4, 6
+    target_next, draft_topk = _toy_models(V, agree, seed=int(agree * 10) + d)
+    root = 3
+    ref = [root]
+    for _ in range(60):
+        ref.append(target_next(ref))
+    tree = DraftTreeRef(root, max_slots=48)
+    draft_prefix = []            # tokens whose draft K/V is committed
+    emitted = [root]
+    accepted_total = steps = 0
+
+    def seq_of(node):
+        toks = [tree.nodes[j]["token"] for j in tree.ancestors_or_self(node)][::-1]
+        return draft_prefix + toks
+
+    def expand():
+        sel = tree.select(w)
+        tree.computed(sel)
+        for n in sel:
+            toks, lps = draft_topk(seq_of(n), K)
+            tree.add_children(n, toks, lps)
+        return len(sel)
+
+    while len(emitted) < 50:
+        for _ in range(d):
+            expand()
+        while tree.tree_size() < bs:
+            if not expand():
+                break
+        toks, pars, chosen = tree.subgraph(bs)
+        # target: greedy acceptance on the subgraph (a11)
+        base = emitted[:]          # committed target tokens + the root (= emitted so far)
+        path, cur = [0], 0
+        while True:
+            nxt_tok = target_next(base + [toks[i] for i in path[1:]])
+            kids = [i for i in range(len(toks)) if pars[i] == cur and toks[i] == nxt_tok]
+            if not kids:
+                bonus = nxt_tok
+                break
+            cur = kids[0]
+            path.append(cur)
+        emitted += [toks[i] for i in path[1:]] + [bonus]
+        accepted_total += len(path) - 1
+        steps += 1
+        nodes = [chosen[i] for i in path]
+        commit, keep, n = tree.reroot(nodes, bonus)
+        assert keep == sorted(keep) and len(set(commit) | set(keep)) == len(commit) + len(keep)
+        # the committed draft tokens are the verified ones, in order
+        draft_prefix = emitted[:len(draft_prefix) + n]
+        assert len(draft_prefix) <= len(emitted) - 1          # the target's root is never committed by the draft
+    assert emitted[:50] == ref[:50]
+    if agree >= 0.9:
+        assert accepted_total / steps > 0.8                   # a good draft gets tokens accepted

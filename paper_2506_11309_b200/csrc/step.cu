@@ -1788,33 +1788,39 @@ __device__ __forceinline__ int attn_item(const StepArgs* __restrict__ ap, const 
     float mx = -INFINITY, l = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (act) {
-      for (int p0 = sub; p0 < P2; p0 += 4 * W) {
-        float m8[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) m8[j] = p0 + j * W < P2 ? __ldcg(&a.att_ml[(pb0 + p0 + j * W) * 64 + rr].x) : -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) mx = fmaxf(mx, m8[j]);
-      }
+      // one pass: online log-sum-exp (the running max rescales what was summed),
+      // so every partial's (m, l) and O are requested together
       for (int p0 = sub; p0 < P2; p0 += 4 * W) {
         float2 v8[4];
         float4 o8[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+          v8[j] = make_float2(-INFINITY, 0.f);
           if (p0 + j * W < P2) {
             const size_t pp = pb0 + p0 + j * W;
             v8[j] = __ldcg(&a.att_ml[pp * 64 + rr]);
             o8[j] = __ldcg(reinterpret_cast<const float4*>(a.att_ws + (pp * 64 + rr) * D + c4));
           }
+        }
+        float mn = mx;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (p0 + j * W < P2) {
-            const float w = (v8[j].x == -INFINITY) ? 0.f : exp2f(v8[j].x - mx);
-            l += w * v8[j].y;
-            acc.x += w * o8[j].x;
-            acc.y += w * o8[j].y;
-            acc.z += w * o8[j].z;
-            acc.w += w * o8[j].w;
-          }
+        for (int j = 0; j < 4; ++j) mn = fmaxf(mn, v8[j].x);
+        if (mn != -INFINITY) {
+          const float sc = (mx == -INFINITY) ? 0.f : exp2f(mx - mn);
+          l *= sc;
+          acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (p0 + j * W < P2 && v8[j].x != -INFINITY) {
+              const float w = exp2f(v8[j].x - mn);
+              l += w * v8[j].y;
+              acc.x += w * o8[j].x;
+              acc.y += w * o8[j].y;
+              acc.z += w * o8[j].z;
+              acc.w += w * o8[j].w;
+            }
+          mx = mn;
+        }
       }
       if (W > 1) {
         float* sm = s_merge + warp * 132;

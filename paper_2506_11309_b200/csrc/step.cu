@@ -1084,21 +1084,25 @@ SS_DEV void ar_send(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<N
 // of every rank's partial (TP all-reduce receive); the new rows also go to
 // ts.xn for the next GEMM's input.
 template <int NT>
-SS_DEV void resid_update(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<NT>& ts) {
+SS_DEV void resid_update(const StepArgs& a, int tg, int T, int ar_seq, const TailSm<NT>& ts,
+                         const float* accg = nullptr) {
   constexpr int TP = NT * 8;
   if (a.P == 1) {
+    // the tile-group's sums straight from the split-K accumulator (no shared
+    // staging): old residual and sums requested together, one round trip
     constexpr int IT = 128 * TP / 256;
-    float xo[IT];
+    float xo[IT], ao[IT];
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
       const int idx = threadIdx.x + i * 256, t = idx >> 7, r = idx & 127;
       xo[i] = t < T ? __ldcg(a.x + (size_t)t * a.h + tg * 128 + r) : 0.f;
+      ao[i] = t < T ? __ldcg(accg + r * TP + t) : 0.f;
     }
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
       const int idx = threadIdx.x + i * 256, t = idx >> 7, r = idx & 127;
       if (t < T) {
-        const float v = xo[i] + ts.acc[r * TP + t];
+        const float v = xo[i] + ao[i];
         a.x[(size_t)t * a.h + tg * 128 + r] = v;
         ts.xn[t * 128 + r] = v;
       }
@@ -1201,11 +1205,10 @@ SS_DEV void resid_update_bcast(const StepArgs& a, int tg, int T, int ar_seq, con
 // GEMM's input for its 128 columns (x * g, fp16 hi/lo + X; or bf16 hi/lo for
 // the LM head) and the token's sum of squares (the deferred RMSNorm scale, R5).
 template <int NT>
-SS_DEV void next_input(const StepArgs& a, int tg, int T, const uint16_t* gain, float* ss, uint8_t* act, int lm,
+SS_DEV void next_input(const StepArgs& a, int tg, int T, uint2 gw, float* ss, uint8_t* act, int lm,
                        const TailSm<NT>& ts) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = tg * 128 + lane * 4;
-  const uint2 gw = *reinterpret_cast<const uint2*>(gain + k);
   for (int t = warp; t < T; t += 8) {
     const float4 v = *reinterpret_cast<const float4*>(ts.xn + t * 128 + lane * 4);
     const float q = warp_sum(v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w);
@@ -1484,15 +1487,14 @@ __device__ __noinline__ int2 gemm_phase(const StepArgs* __restrict__ ap, const S
       for (int i = 0; i < nd; ++i) {
         const bool home = !two || s_done[i] % a.P == a.rank;
         if (two && home != (pass == 0)) continue;
-        if (a.P == 1) {
-          stage_acc<NT>(accb + (size_t)s_done[i] * 128 * TP, ts.acc);
-          cbar();
-        }
-        if (home) resid_update<NT>(a, s_done[i], T, ar_seq, ts);
+        // the next norm's gains for this tile-group's 128 columns, requested
+        // before the residual's round trips
+        const uint2 gw = __ldg(reinterpret_cast<const uint2*>(gain + s_done[i] * 128 + (threadIdx.x & 31) * 4));
+        if (home) resid_update<NT>(a, s_done[i], T, ar_seq, ts, accb + (size_t)s_done[i] * 128 * TP);
         else resid_update_bcast<NT>(a, s_done[i], T, ar_seq, ts);
         cbar();
         if (ttl && i == 0) ttl[3] = clk64();
-        next_input<NT>(a, s_done[i], T, gain, ssn, act, last ? 1 : 0, ts);
+        next_input<NT>(a, s_done[i], T, gw, ssn, act, last ? 1 : 0, ts);
         cbar();
       }
     where(a, WCODE(layer, PH, 8));

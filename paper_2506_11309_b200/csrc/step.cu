@@ -1026,16 +1026,28 @@ template <int NT>
 SS_DEV void epi_swiglu(const StepArgs& a, int layer, int tg, const float* acc, int T, const TailSm<NT>& ts) {
   const int TP = NT * 8;
   const float* ssm = a.ss + (size_t)layer * 2 * 64 + 64;
-  stage_acc<NT>(acc, ts.acc);
-  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale_a(a, ssm, threadIdx.x);
-  cbar();
   const int warp = threadIdx.x >> 5, cp = threadIdx.x & 31;
+  if constexpr (NT != 1) {  // several tokens per warp: stage the block once
+    stage_acc<NT>(acc, ts.acc);
+    if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale_a(a, ssm, threadIdx.x);
+    cbar();
+  }
   for (int t = warp; t < T; t += 8) {
-    const float rs = ts.rs[t];
-    const float g0 = ts.acc[(2 * cp) * TP + t] * rs;
-    const float g1 = ts.acc[(2 * cp + 1) * TP + t] * rs;
-    const float u0 = ts.acc[(64 + 2 * cp) * TP + t] * rs;
-    const float u1 = ts.acc[(64 + 2 * cp + 1) * TP + t] * rs;
+    float g0, g1, u0, u1;
+    if constexpr (NT == 1) {
+      // one token per warp: its sums straight from the split-K accumulator
+      // with the token's norm scale, one round trip, no shared staging
+      const float a0 = __ldcg(acc + (2 * cp) * TP + t), a1 = __ldcg(acc + (2 * cp + 1) * TP + t);
+      const float a2 = __ldcg(acc + (64 + 2 * cp) * TP + t), a3 = __ldcg(acc + (64 + 2 * cp + 1) * TP + t);
+      const float rs = norm_scale_a(a, ssm, t);
+      g0 = a0 * rs; g1 = a1 * rs; u0 = a2 * rs; u1 = a3 * rs;
+    } else {
+      const float rs = ts.rs[t];
+      g0 = ts.acc[(2 * cp) * TP + t] * rs;
+      g1 = ts.acc[(2 * cp + 1) * TP + t] * rs;
+      u0 = ts.acc[(64 + 2 * cp) * TP + t] * rs;
+      u1 = ts.acc[(64 + 2 * cp + 1) * TP + t] * rs;
+    }
     const float h0 = g0 / (1.f + __expf(-g0)) * u0;
     const float h1 = g1 / (1.f + __expf(-g1)) * u1;
     const int k = tg * 64 + 2 * cp;
@@ -1242,14 +1254,25 @@ template <int NT>
 SS_DEV void epi_argmax(const StepArgs& a, int tg, const float* acc, int T, const TailSm<NT>& ts) {
   const int TP = NT * 8;
   const float* ssf = a.ss + (size_t)a.n_layers * 2 * 64;
-  stage_acc<NT>(acc, ts.acc);
-  if (threadIdx.x < T) ts.rs[threadIdx.x] = norm_scale_a(a, ssf, threadIdx.x);
-  cbar();
+  (void)ts;
   const int r = threadIdx.x & 127;
   const int v = tg * 128 + r;
   const bool valid = v < a.V_l;
-  for (int t = threadIdx.x >> 7; t < T; t += 2) {
-    const float val = valid ? ts.acc[r * TP + t] * ts.rs[t] : -INFINITY;
+  constexpr int NI = NT * 4;  // tokens per thread (t = threadIdx.x / 128 + 2 i)
+  float av[NI], rv[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {  // sums and norm scales straight from global, all requested first
+    const int t = (threadIdx.x >> 7) + 2 * i;
+    if (t < T) {
+      av[i] = __ldcg(acc + r * TP + t);
+      rv[i] = norm_scale_a(a, ssf, t);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int t = (threadIdx.x >> 7) + 2 * i;
+    if (t >= T) continue;
+    const float val = valid ? av[i] * rv[i] : -INFINITY;
     if (valid && a.logits) a.logits[(size_t)t * a.logits_ld + v] = val;
     unsigned long long key = valid ? argmax_key(val, (uint32_t)(a.V_off + v)) : 0ull;
 #pragma unroll

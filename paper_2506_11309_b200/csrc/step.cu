@@ -1002,9 +1002,11 @@ SS_DEV void epi_qkv(const StepArgs& a, int layer, int tg, const float* acc, cons
   }
   // zero the lo window rows outside this step's new rows of this tile-group's
   // K / V heads (a tree tile's prefix rows -- and the cached tree rows of a
-  // non-square forward, fp16 like committed rows -- add q . 0)
+  // non-square forward, fp16 like committed rows -- add q . 0).  The window is
+  // per kv head, shared by the layers, and every layer of a step writes the
+  // same rows [R, R + T): only the first layer has to clear the rest.
   const int row0 = tg * 128;
-  if (row0 + 127 >= nq && row0 < nq + 2 * nk) {
+  if (layer == 0 && row0 + 127 >= nq && row0 < nq + 2 * nk) {
     for (int hd = 0; hd < 128 / d; ++hd) {
       const int row = row0 + hd * d;
       if (row < nq || row >= nq + 2 * nk) continue;
